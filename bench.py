@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""MCI benchmark (BASELINE.json metric: output samples/s (fp32) and achieved HBM GB/s).
+
+Default workload = BASELINE.json configs[1] ("config 2"): 65536 real signals,
+M=3 channels (f, f', f''), N=1024 samples each -> L=16384 outputs, fp32.
+A step is one pass of the whole hot path (forward DFTs, per-class solves,
+assembly, inverse FFTs, stores) over the batch, i.e. one mci_execute_1d.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl mci|reference]
+
+N > 1: one process per GPU (torchrun), each rank runs its own batch (rows are
+independent: weak scaling, no collective on the data path); time = max over
+ranks of the CUDA-event time.  Rank 0 prints ONE JSON line.
+--impl reference times the fp64 CPU oracle (the tier's reference arm) on a
+bounded sample on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MCI output samples/sec (fp32) and achieved HBM GB/s vs B200 peak"
+UNIT = "samples/s"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth, burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload(cfg):
+    c = synth.CONFIGS[cfg]
+    if cfg == 5:
+        n = c["N"]
+        return dict(name=f"cfg5: {c['batch']} images, 4 channel images 512x512 -> 2048x2048 (separable, bank {{1,ik}}^2)",
+                    units=c["batch"], outs_per_unit=c["size"] ** 2, in_per_unit=4 * n * n,
+                    out_floats_per_unit=c["size"] ** 2)
+    M, N, L, B = c["M"], c["N"], c["L"], c["batch"]
+    nout = 2 if c.get("hilbert") else 1
+    bank = {1: "1, ik", 2: "1, ik, -k^2", 3: "1, ik (+Hf)", 4: "delays 2 pi m/(4N)"}[cfg]
+    return dict(name=f"cfg{cfg}: {B} x (M={M}, N={N}) -> L={L} x {nout} out, bank {bank}",
+                units=B, outs_per_unit=L * nout, in_per_unit=M * N, out_floats_per_unit=L * nout)
+
+
+def make_inputs(cfg, rank):
+    """Host inputs of the configuration (seeded; rank-offset seeds for N>1)."""
+    c = synth.CONFIGS[cfg]
+    if cfg == 1:
+        return synth.cfg1(seed=rank)["g"]
+    if cfg == 2:
+        return synth.cfg2_batch_fast(c["batch"], seed=2 + 1000 * rank)
+    if cfg == 3:
+        return synth.cfg3_rows(np.arange(c["batch"]), seed=3 + 1000 * rank)
+    if cfg == 4:
+        return synth.cfg4_signals(np.arange(c["batch"]), seed=4 + 1000 * rank)[0]
+    # cfg5: generate a few distinct images and tile them to the batch (content does not
+    # change the arithmetic or the bytes; generation of 64 2048^2 images would dominate)
+    distinct = 4
+    g, _ = synth.cfg5_images(range(rank * distinct, rank * distinct + distinct))
+    reps = c["batch"] // distinct
+    return np.ascontiguousarray(np.tile(g, (reps, 1, 1, 1, 1)))
+
+
+def make_plan(cfg):
+    import paper_1802_10291_b200 as mci
+    c = synth.CONFIGS[cfg]
+    if cfg == 5:
+        return mci.Plan2D(2, c["N"], c["bank"], 2, c["N"], c["bank"], c["scale"])
+    return mci.Plan(c["M"], c["N"], c["L"], c["bank"], dtype="f64" if cfg == 1 else "f32",
+                    hilbert=bool(c.get("hilbert")))
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, dev_index):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def oracle_sample(cfg, budget_s=12.0, max_steps=None):
+    """Time the fp64 oracle on a bounded sample of the workload on the host cores.
+    Returns (samples_per_s, description, threads, per-step seconds list)."""
+    import oracle
+    c = synth.CONFIGS[cfg]
+    threads = os.cpu_count() or 1
+    if cfg == 4:
+        M, N, L = c["M"], c["N"], c["L"]
+        g, _ = synth.cfg4_signals([0])
+        pts = np.random.default_rng(0).integers(0, L, 64)
+        t0 = time.perf_counter()
+        n = 0
+        while True:
+            oracle.delay_eval_points(M, N, L, g[0], pts, threads=threads)
+            n += len(pts)
+            if time.perf_counter() - t0 > budget_s / 2:
+                break
+        dt = time.perf_counter() - t0
+        return n / dt, f"signal 0, {n} output points (closed-form delay kernel), M*N={M*N} terms each", threads
+    if cfg == 5:
+        px = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=threads)
+        px.kernel_table()
+        g, _ = synth.cfg5_images([0])
+        cols = np.arange(0, 2048, 2048 // 16)
+        t0 = time.perf_counter()
+        oracle.eval_2d_columns(g[0], px, px, cols)
+        dt = time.perf_counter() - t0
+        return len(cols) * 2048 / dt, f"image 0, {len(cols)} full output columns (2048 px each)", threads
+    M, N, L = c["M"], c["N"], c["L"]
+    P = oracle.OraclePlan(M, N, L, c["bank"], threads=threads)
+    P.kernel_table()
+    if c.get("hilbert"):
+        P.kernel_table(True)
+    rows = 0
+    t0 = time.perf_counter()
+    while True:
+        g = make_row(cfg, rows)
+        P.eval(g)
+        if c.get("hilbert"):
+            P.eval(g, hilbert=True)
+        rows += 1
+        if time.perf_counter() - t0 > budget_s or (max_steps and rows >= max_steps):
+            break
+    dt = time.perf_counter() - t0
+    nout = 2 if c.get("hilbert") else 1
+    return rows * L * nout / dt, f"{rows} rows of the workload (kernel table built before timing)", threads
+
+
+def make_row(cfg, r):
+    if cfg == 1:
+        return synth.cfg1()["g"]
+    if cfg == 2:
+        return synth.cfg2_rows([r])
+    return synth.cfg3_rows([r])
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import oracle
+    cfg = args.config
+    c = synth.CONFIGS[cfg]
+    w = workload(cfg)
+    threads = os.cpu_count() or 1
+    # each step = one row (cfg1-3), 64 points (cfg4) or 4 columns (cfg5) of the workload
+    if cfg in (1, 2, 3):
+        P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
+        P.kernel_table()
+        if c.get("hilbert"):
+            P.kernel_table(True)
+        nout = 2 if c.get("hilbert") else 1
+
+        def step(i):
+            g = make_row(cfg, i)
+            P.eval(g)
+            if c.get("hilbert"):
+                P.eval(g, hilbert=True)
+            return c["L"] * nout
+        sample = "one row per step"
+    elif cfg == 4:
+        gg, _ = synth.cfg4_signals([0])
+        pts = np.random.default_rng(0).integers(0, c["L"], 64)
+
+        def step(i):
+            oracle.delay_eval_points(c["M"], c["N"], c["L"], gg[0], pts, threads=threads)
+            return len(pts)
+        sample = "64 output points of signal 0 per step (closed-form delay kernel)"
+    else:
+        px = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=threads)
+        px.kernel_table()
+        gi, _ = synth.cfg5_images([0])
+
+        def step(i):
+            oracle.eval_2d_columns(gi[0], px, px, [(i * 131) % 2048, (i * 131 + 1) % 2048])
+            return 2 * 2048
+        sample = "two full output columns of image 0 per step"
+    for i in range(args.warmup):
+        step(i)
+    t0 = time.perf_counter()
+    done = 0
+    for i in range(args.steps):
+        done += step(i)
+    dt = time.perf_counter() - t0
+    v = done / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": w["name"], "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def load_traffic(workload_name):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get(workload_name)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_10291_b200 as mci
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = args.config
+    w = workload(cfg)
+    tdt = torch.float64 if cfg == 1 else torch.float32
+    esz = 8 if cfg == 1 else 4
+
+    g_host = make_inputs(cfg, rank)
+    plan = make_plan(cfg)
+    g = torch.from_numpy(g_host).to("cuda", dtype=tdt)
+    units = w["units"]
+    c = synth.CONFIGS[cfg]
+    hilbert = bool(c.get("hilbert"))
+    if cfg == 5:
+        out = torch.empty((units, c["size"], c["size"]), dtype=tdt, device="cuda")
+        hf = None
+    else:
+        out = torch.empty((units, c["L"]), dtype=tdt, device="cuda")
+        hf = torch.empty_like(out) if hilbert else None
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if cfg == 5:
+            plan.execute(g, out)
+        else:
+            plan.execute(g, out, hf)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    total_samples = units * w["outs_per_unit"] * world
+    value = total_samples / (ms_step / 1e3)
+
+    # roofline of the dominant kernel: algorithmic bytes per launch / launch time.
+    # (cfg2: one fused launch per step, so the kernel time is the step time on the stream.)
+    peak, peak_src = load_peaks()
+    launches = plan.launches(units)
+    alg_bytes = units * (w["in_per_unit"] + w["out_floats_per_unit"]) * esz
+    per_launch_ms = ms_step / launches if cfg in (1, 2, 3) else ms_step
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9 if cfg in (1, 2, 3) else alg_bytes / (ms_step / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": load_traffic(w["name"]), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes if cfg in (1, 2, 3) else None,
+            "algorithmic_bytes_per_step": alg_bytes}
+
+    # end-to-end through the host-buffer C-ABI call (H2D + compute + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        gh = torch.from_numpy(g_host).to(tdt).pin_memory()
+        oh = torch.empty(out.shape, dtype=tdt).pin_memory()
+        hh = torch.empty(out.shape, dtype=tdt).pin_memory() if hilbert else None
+        e_steps = max(3, min(args.steps, 10))
+
+        def estep():
+            if cfg == 5:
+                plan.execute_host(gh, oh)
+            else:
+                plan.execute_host(gh, oh, hh)
+        estep()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            estep()
+        et = (time.perf_counter() - t0) / e_steps
+        if world > 1:
+            t = torch.tensor([et], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            et = float(t.item())
+        e2e = {"value": total_samples / et, "unit": UNIT,
+               "h2d_bytes_per_step": int(gh.numel() * esz),
+               "d2h_bytes_per_step": int(oh.numel() * esz * (2 if hilbert else 1)),
+               "ms_per_step": et * 1e3, "steps": e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, sample, thr = oracle_sample(cfg)
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64" if cfg == 1 else "f32",
+                "data": "synthetic",
+                "config": {"workload": w["name"], "units_per_gpu": units,
+                           "l2": "inputs+outputs exceed the 126 MB L2 (no flush needed)" if cfg != 1 else
+                           "tiny (latency-bound), L2-resident",
+                           "parallelism": f"dp{world} (independent rows per rank)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": int(launches * args.steps),
+                "clocks": clk.summary(),
+                "hbm_gbs_algorithmic": achieved}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,131 @@
+/*
+ * mci.h -- C ABI of the B200-native multichannel-interpolation (MCI) library.
+ *
+ * Method: arXiv 1802.10291, "fast multichannel interpolation".
+ * A real 2*pi-periodic signal f whose spectrum lies in the band
+ * I^N = {K1 .. K1+M*N-1}, K1 = -M*N/2, is reconstructed from N uniform
+ * samples g_m(t_n), t_n = 2*pi*n/N, of each of M channel responses
+ * g_m = h_m * f (Eq. sysfunction).  The output is
+ *   f(t_p) = Re T_N f(t_p),  t_p = 2*pi*p/L,  p = 0..L-1,
+ * with T_N the operator of Eq. (appxi operator) PAPER.md:542-545, computed by
+ * the FFT form Eq. (DFTexpression) PAPER.md:316-323:
+ *   forward DFT of each channel (Lemma 1),
+ *   per-bin M x M solve A_n = D_n H_n^{-1} (Eq. matrixeqn1),
+ *   Hermitian-part assembly and zero-padding to L, inverse real FFT.
+ * Optional Hilbert twin Hf = H(Re T_N f), multiplier -i*sgn(k)
+ * (Example 6 PAPER.md:522-531), via one analytic inverse
+ * transform (Example 4).
+ * Notation: this header's N is the paper's L (samples per channel) and this
+ * header's L is the paper's N_out.
+ *
+ * Conventions (all entry points):
+ *  - Status codes, never exceptions.  On create failure *out is set to NULL.
+ *  - Device pointers are CUDA device pointers (e.g. torch data_ptr()); the
+ *    caller owns them and the stream.  mci_execute_* never allocate, never
+ *    synchronise the device, and only enqueue work on `cuda_stream`
+ *    (a cudaStream_t; NULL = legacy default stream).
+ *  - The plan owns its device tables (inverse matrices, twiddles) and any
+ *    workspace; it is immutable after create and may be used concurrently
+ *    from several streams except that plans with workspace (four-step and
+ *    2D paths) serialise on their workspace: use one plan per stream there.
+ *  - Results are deterministic for a given plan and batch (no atomics).
+ *  - Arithmetic type is the plan dtype (MCI_F32: float, MCI_F64: double);
+ *    host-side plan construction is always fp64.
+ */
+#ifndef MCI_H
+#define MCI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mci_plan_s *mci_plan; /* opaque */
+
+typedef enum {
+    MCI_OK = 0,
+    MCI_E_ARG = 1,         /* NULL pointer, non-positive size, bad enum            */
+    MCI_E_BAND = 2,        /* M*N odd or band invalid                               */
+    MCI_E_ALIAS = 3,       /* L < M*N, L odd, or L not a multiple of N */
+    MCI_E_SINGULAR = 4,    /* some H_n singular (see mci_last_singular_bin)         */
+    MCI_E_SIZE = 5,        /* sizes not supported (non powers of two, too large)    */
+    MCI_E_CUDA = 6,        /* a CUDA runtime call or kernel launch failed           */
+    MCI_E_UNSUPPORTED = 7  /* valid request this build does not implement           */
+} mci_status;
+
+typedef enum { MCI_F32 = 0, MCI_F64 = 1 } mci_dtype;
+
+/* Channel system h_m given by its Fourier multiplier b_m(k) (Eq. sysfunction). */
+typedef enum {
+    MCI_SYS_IDENTITY = 0,   /* b(k) = 1                                  */
+    MCI_SYS_DERIVATIVE = 1, /* b(k) = (i k)^order   (Example 2)          */
+    MCI_SYS_HILBERT = 2,    /* b(k) = -i sgn(k)     (Examples 3, 5)      */
+    MCI_SYS_DELAY = 3,      /* b(k) = exp(i k tau)  (interlaced sampling) */
+    MCI_SYS_TABLE = 4       /* b(k) = table[2(k-K1)] + i table[2(k-K1)+1], k in band */
+} mci_sys_kind;
+
+typedef struct {
+    int kind;            /* mci_sys_kind                                    */
+    int order;           /* derivative order (MCI_SYS_DERIVATIVE)           */
+    double tau;          /* delay in radians (MCI_SYS_DELAY)                */
+    const double *table; /* host, 2*M*N doubles (MCI_SYS_TABLE); copied     */
+} mci_system;
+
+enum { MCI_OUT_HILBERT = 1u }; /* plan also produces Hf */
+
+/* ---- plans ------------------------------------------------------------------------ */
+
+/* 1D plan: M channels (1..8), N samples per channel, L output points.
+ * Requirements: N and L powers of two, M*N even, L >= M*N, L % N == 0,
+ * Hermitian bank (b_m(-k) = conj b_m(k), true for every built-in kind).
+ * H_n (entry (l,m) = b_m(n + l N), Eq. defH) must be
+ * invertible for every n in I_1 except the listed Remark-1 null bins
+ * (PAPER.md:325-327), whose inverse is set to zero.  Singular: some pivot
+ * < 1e-12 * max row norm (SPEC.md:184 reading).  Host arrays are copied. */
+mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci_system *sys,
+                           const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags);
+
+/* 2D separable plan: tensor bank {sx} x {sy}; channel images
+ * g[n][My][Mx][Ny][Nx]; output [n][scale*Ny][scale*Nx].  Re is taken after
+ * each 1D pass.  flags must be 0. */
+mci_status mci_plan_create_2d(mci_plan *out, int Mx, int64_t Nx, const mci_system *sx, int My,
+                              int64_t Ny, const mci_system *sy, int scale, mci_dtype dtype,
+                              unsigned flags);
+
+void mci_plan_destroy(mci_plan p);
+
+/* ---- execution (device buffers) ---------------------------------------------------- */
+
+/* g:  device, [batch][M][N] row-major, plan dtype.
+ * f:  device, [batch][L]; hf: device [batch][L] (required iff MCI_OUT_HILBERT, else NULL).
+ * Input and output must not overlap.  Asynchronous on cuda_stream. */
+mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf,
+                          void *cuda_stream);
+
+/* g: device [n_images][My][Mx][Ny][Nx]; out: device [n_images][Ly][Lx]. */
+mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out,
+                          void *cuda_stream);
+
+/* ---- execution (host buffers) -------------------------------------------------------
+ * Same layouts, but g/f/hf/out are HOST pointers (page-locked for full speed).
+ * The library streams the batch through plan-owned device staging buffers in
+ * chunks, overlapping host->device copy, compute and device->host copy on
+ * internal streams; returns after the results are in host memory. */
+mci_status mci_execute_1d_host(mci_plan p, int64_t batch, const void *g, void *f, void *hf);
+mci_status mci_execute_2d_host(mci_plan p, int64_t n_images, const void *g, void *out);
+
+/* ---- introspection ------------------------------------------------------------------- */
+double mci_plan_cond_max(mci_plan p);          /* max ||H_n||_1 ||H_n^{-1}||_1 */
+int64_t mci_last_singular_bin(void);           /* n of the last MCI_E_SINGULAR (this thread) */
+size_t mci_plan_workspace_bytes(mci_plan p);   /* device bytes owned by the plan            */
+int mci_plan_path(mci_plan p);                 /* 0 fused 1D, 1 four-step 1D, 2 separable 2D */
+int64_t mci_plan_launches(mci_plan p, int64_t batch); /* kernels one execute enqueues       */
+const char *mci_status_str(mci_status s);
+const char *mci_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCI_H */

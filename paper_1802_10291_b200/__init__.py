@@ -1,0 +1,240 @@
+"""B200-native fast multichannel interpolation (MCI, arXiv 1802.10291).
+
+Thin Python binding over the C ABI in ``include/mci.h`` (``libmci.so``, built
+in-tree for sm_100a by ``_build.py``).  This module only marshals arguments:
+every step of the hot path runs in the CUDA kernels behind the ABI.  There is
+no CPU fallback -- if the library cannot be loaded, importing or calling
+raises.  PyTorch is used only to hand device buffers and streams over.
+
+Bank description: one tuple per channel,
+    ("identity",) | ("derivative", order) | ("hilbert",) | ("delay", tau) | ("table", b[k-K1] complex array)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmci.so")
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "mci.h")
+
+MCI_OK, MCI_E_ARG, MCI_E_BAND, MCI_E_ALIAS, MCI_E_SINGULAR, MCI_E_SIZE, MCI_E_CUDA, MCI_E_UNSUPPORTED = range(8)
+MCI_F32, MCI_F64 = 0, 1
+MCI_OUT_HILBERT = 1
+_KIND = {"identity": 0, "derivative": 1, "hilbert": 2, "delay": 3, "table": 4}
+PATH_NAMES = {0: "fused", 1: "fourstep", 2: "2d"}
+
+
+class MCIError(RuntimeError):
+    def __init__(self, status, what=""):
+        self.status = status
+        msg = _lib_handle().mci_status_str(status).decode() if _lib is not None else str(status)
+        super().__init__(f"{what}: {msg} (status {status})")
+
+
+class _System(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("order", ctypes.c_int), ("tau", ctypes.c_double),
+                ("table", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def _lib_handle():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run __graft_entry__.build() "
+                              "(no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint
+        L.mci_plan_create.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, i32, i32, u32]
+        L.mci_plan_create.restype = i32
+        L.mci_plan_create_2d.argtypes = [ctypes.POINTER(vp), i32, i64, vp, i32, i64, vp, i32, i32, u32]
+        L.mci_plan_create_2d.restype = i32
+        L.mci_plan_destroy.argtypes = [vp]
+        L.mci_plan_destroy.restype = None
+        L.mci_execute_1d.argtypes = [vp, i64, vp, vp, vp, vp]
+        L.mci_execute_1d.restype = i32
+        L.mci_execute_2d.argtypes = [vp, i64, vp, vp, vp]
+        L.mci_execute_2d.restype = i32
+        L.mci_execute_1d_host.argtypes = [vp, i64, vp, vp, vp]
+        L.mci_execute_1d_host.restype = i32
+        L.mci_execute_2d_host.argtypes = [vp, i64, vp, vp]
+        L.mci_execute_2d_host.restype = i32
+        L.mci_plan_cond_max.argtypes = [vp]
+        L.mci_plan_cond_max.restype = ctypes.c_double
+        L.mci_last_singular_bin.argtypes = []
+        L.mci_last_singular_bin.restype = i64
+        L.mci_plan_workspace_bytes.argtypes = [vp]
+        L.mci_plan_workspace_bytes.restype = ctypes.c_size_t
+        L.mci_plan_path.argtypes = [vp]
+        L.mci_plan_path.restype = i32
+        L.mci_plan_launches.argtypes = [vp, i64]
+        L.mci_plan_launches.restype = i64
+        L.mci_status_str.argtypes = [i32]
+        L.mci_status_str.restype = ctypes.c_char_p
+        L.mci_version.argtypes = []
+        L.mci_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def header_functions():
+    """Function names declared in include/mci.h (for the ABI export test)."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(mci_[a-z0-9_]+)\s*\(", txt)))
+
+
+def _systems(bank):
+    arr = (_System * len(bank))()
+    keep = []
+    for i, spec in enumerate(bank):
+        kind = spec[0]
+        arr[i].kind = _KIND[kind]
+        arr[i].order = int(spec[1]) if kind == "derivative" else 0
+        arr[i].tau = float(spec[1]) if kind == "delay" else 0.0
+        if kind == "table":
+            t = np.ascontiguousarray(np.asarray(spec[1], dtype=np.complex128).view(np.float64))
+            keep.append(t)
+            arr[i].table = t.ctypes.data
+        else:
+            arr[i].table = None
+    return arr, keep
+
+
+def _dptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _check(status, what):
+    if status != MCI_OK:
+        if status == MCI_E_SINGULAR:
+            raise MCIError(status, f"{what} (singular bin n={_lib_handle().mci_last_singular_bin()})")
+        raise MCIError(status, what)
+
+
+class Plan:
+    """1D MCI plan: M channels x N samples -> L outputs (f, optionally Hf)."""
+
+    def __init__(self, M, N, L, bank, null_bins=(), dtype="f32", hilbert=False):
+        lib = _lib_handle()
+        self.M, self.N, self.L = int(M), int(N), int(L)
+        self.dtype = dtype
+        self.hilbert = bool(hilbert)
+        sys_arr, self._keep = _systems(bank)
+        nb = np.ascontiguousarray(np.asarray(list(null_bins), dtype=np.int64))
+        h = ctypes.c_void_p()
+        st = lib.mci_plan_create(ctypes.byref(h), self.M, self.N, self.L, ctypes.addressof(sys_arr),
+                                 nb.ctypes.data if len(nb) else None, len(nb),
+                                 MCI_F64 if dtype == "f64" else MCI_F32, MCI_OUT_HILBERT if hilbert else 0)
+        _check(st, "mci_plan_create")
+        self._h = h
+
+    @property
+    def path(self):
+        return PATH_NAMES[_lib_handle().mci_plan_path(self._h)]
+
+    @property
+    def cond_max(self):
+        return _lib_handle().mci_plan_cond_max(self._h)
+
+    def launches(self, batch):
+        return int(_lib_handle().mci_plan_launches(self._h, int(batch)))
+
+    @property
+    def workspace_bytes(self):
+        return int(_lib_handle().mci_plan_workspace_bytes(self._h))
+
+    def torch_dtype(self):
+        import torch
+        return torch.float64 if self.dtype == "f64" else torch.float32
+
+    def execute(self, g, f=None, hf=None, stream=None):
+        """g: CUDA tensor [batch][M][N] (contiguous, plan dtype).  Returns f (and hf)."""
+        import torch
+        assert g.is_cuda and g.is_contiguous() and g.dtype == self.torch_dtype()
+        assert g.shape[-2:] == (self.M, self.N)
+        batch = g.numel() // (self.M * self.N)
+        if f is None:
+            f = torch.empty((batch, self.L), dtype=g.dtype, device=g.device)
+        if self.hilbert and hf is None:
+            hf = torch.empty((batch, self.L), dtype=g.dtype, device=g.device)
+        st = _lib_handle().mci_execute_1d(self._h, batch, _dptr(g), _dptr(f), _dptr(hf) if self.hilbert else None,
+                                          _stream(stream))
+        _check(st, "mci_execute_1d")
+        return (f, hf) if self.hilbert else f
+
+    def execute_host(self, g, f, hf=None):
+        """Host buffers (numpy arrays or CPU tensors, ideally pinned): H2D, compute, D2H inside."""
+        def p(x):
+            return ctypes.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data)
+        batch = int(np.prod(g.shape)) // (self.M * self.N)
+        st = _lib_handle().mci_execute_1d_host(self._h, batch, p(g), p(f), p(hf) if self.hilbert else None)
+        _check(st, "mci_execute_1d_host")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mci_plan_destroy(h)
+            self._h = None
+
+
+class Plan2D:
+    """Separable 2D MCI: channel images [n][My][Mx][Ny][Nx] -> [n][scale*Ny][scale*Nx]."""
+
+    def __init__(self, Mx, Nx, bank_x, My, Ny, bank_y, scale, dtype="f32"):
+        lib = _lib_handle()
+        self.Mx, self.Nx, self.My, self.Ny, self.scale = int(Mx), int(Nx), int(My), int(Ny), int(scale)
+        self.dtype = dtype
+        sx, self._kx = _systems(bank_x)
+        sy, self._ky = _systems(bank_y)
+        h = ctypes.c_void_p()
+        st = lib.mci_plan_create_2d(ctypes.byref(h), self.Mx, self.Nx, ctypes.addressof(sx), self.My, self.Ny,
+                                    ctypes.addressof(sy), self.scale, MCI_F64 if dtype == "f64" else MCI_F32, 0)
+        _check(st, "mci_plan_create_2d")
+        self._h = h
+
+    def launches(self, n):
+        return int(_lib_handle().mci_plan_launches(self._h, int(n)))
+
+    @property
+    def workspace_bytes(self):
+        return int(_lib_handle().mci_plan_workspace_bytes(self._h))
+
+    def execute(self, g, out=None, stream=None):
+        import torch
+        dt = torch.float64 if self.dtype == "f64" else torch.float32
+        assert g.is_cuda and g.is_contiguous() and g.dtype == dt
+        n = g.numel() // (self.My * self.Mx * self.Ny * self.Nx)
+        if out is None:
+            out = torch.empty((n, self.scale * self.Ny, self.scale * self.Nx), dtype=dt, device=g.device)
+        st = _lib_handle().mci_execute_2d(self._h, n, _dptr(g), _dptr(out), _stream(stream))
+        _check(st, "mci_execute_2d")
+        return out
+
+    def execute_host(self, g, out):
+        def p(x):
+            return ctypes.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data)
+        n = int(np.prod(g.shape)) // (self.My * self.Mx * self.Ny * self.Nx)
+        st = _lib_handle().mci_execute_2d_host(self._h, n, p(g), p(out))
+        _check(st, "mci_execute_2d_host")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mci_plan_destroy(h)
+            self._h = None
+
+
+def version():
+    return _lib_handle().mci_version().decode()

@@ -1,0 +1,49 @@
+// Internal structures shared by the plan builder (mci_plan.cpp) and the CUDA
+// launchers (*.cu).  Not part of the ABI.
+#pragma once
+
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+#include "../../include/mci.h"
+
+namespace mci {
+
+// Per-plan device tables for one 1D axis (fused or four-step path).
+struct Axis1D {
+    int M = 0;
+    int64_t N = 0, L = 0, K = 0;  // K = M*N/2, band {-K .. K-1}
+    int64_t S = 0, R = 0;         // inverse FFT length and decimation: L = R*S
+    int analytic = 0;             // 1: produce f + i Hf (one-sided spectrum)
+    int dtype = MCI_F32;
+    // Device tables (element type = plan dtype, complex = 2 scalars):
+    void *Qt = nullptr;   // [(N/2+1)][M][M] complex: Q_q[m][l] / N for class q (j_q = q - N*ceil)
+    void *twF = nullptr;  // [TW] complex e^{-2 pi i m / TW}, TW = max(N, S, 1024)
+    int64_t TW = 0;
+    void *twLhi = nullptr;  // [L/LO] complex e^{+2 pi i (h*LO) / L}
+    void *twLlo = nullptr;  // [LO]   complex e^{+2 pi i l / L}
+    int64_t LO = 0;
+};
+
+enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2 };
+
+// Row addressing of the fused kernel: row r starts at
+//   (r / (D0*D1)) * s2 + ((r / D0) % D1) * s1 + (r % D0) * s0
+// channel m adds m*cs, sample n adds n*ss; output row r is at r*L.
+struct RowAddr {
+    int64_t D0 = 1, D1 = 1, s0 = 0, s1 = 0, s2 = 0, cs = 0, ss = 1;
+};
+
+// Launchers (mci_fused.cu / mci_fourstep.cu).  All async on `st`.
+cudaError_t launch_fused(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f,
+                         void *hf, cudaStream_t st, int *n_launches);
+size_t fused_smem_bytes(const Axis1D &ax);
+bool fused_supported(const Axis1D &ax);
+
+cudaError_t launch_fourstep(const Axis1D &ax, int64_t batch, const void *g, void *f, void *ws,
+                            int64_t ws_signals, cudaStream_t st, int *n_launches);
+size_t fourstep_ws_bytes_per_signal(const Axis1D &ax);
+bool fourstep_supported(const Axis1D &ax);
+
+}  // namespace mci

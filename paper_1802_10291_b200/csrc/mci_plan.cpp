@@ -1,0 +1,508 @@
+// Plan builder and C-ABI entry points (include/mci.h).
+//
+// Host side, fp64: for every class q = 0..N/2 (j_q in I_1 = {-K .. -K+N-1},
+// j_q = q mod N) build H_{j_q}[l][m] = b_m(j_q + l N) (Eq. defH),
+// invert it by LU with partial pivoting, and pack Qt_q = H_{j_q}^{-1} / N
+// (the 1/N of d_m = G_m/N, Lemma 1, is folded in).  Classes
+// N/2+1..N-1 are never needed: for a Hermitian bank they are the conjugate
+// mirrors of classes N-q.  Remark 1 null bins get Qt = 0.
+// Twiddle tables are rounded from fp64.  Nothing here runs per execute.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "mci_internal.h"
+
+using cd = std::complex<double>;
+
+namespace {
+
+thread_local int64_t g_last_singular = 0;
+const double PI = 3.14159265358979323846264338327950288;
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+int64_t next_pow2(int64_t x) {
+    int64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+cd sys_multiplier(const mci_system &s, int64_t K1, int64_t k) {
+    switch (s.kind) {
+    case MCI_SYS_IDENTITY: return 1.0;
+    case MCI_SYS_DERIVATIVE: {
+        cd v = 1.0;
+        for (int i = 0; i < s.order; ++i) v *= cd(0.0, (double)k);
+        return v;
+    }
+    case MCI_SYS_HILBERT: return k > 0 ? cd(0, -1) : (k < 0 ? cd(0, 1) : cd(0, 0));
+    case MCI_SYS_DELAY: {
+        double ang = std::fmod((double)k * s.tau, 2 * PI);
+        return cd(std::cos(ang), std::sin(ang));
+    }
+    case MCI_SYS_TABLE: return cd(s.table[2 * (k - K1)], s.table[2 * (k - K1) + 1]);
+    }
+    return 0.0;
+}
+
+// LU with partial pivoting; returns false if a pivot < thresh.  inv = A^{-1}.
+bool lu_inverse(int M, std::vector<cd> A, std::vector<cd> &inv, double thresh) {
+    std::vector<int> piv(M);
+    for (int i = 0; i < M; ++i) piv[i] = i;
+    for (int c = 0; c < M; ++c) {
+        int p = c;
+        for (int r = c + 1; r < M; ++r)
+            if (std::abs(A[r * M + c]) > std::abs(A[p * M + c])) p = r;
+        if (!(std::abs(A[p * M + c]) >= thresh) || std::abs(A[p * M + c]) == 0.0) return false;
+        if (p != c) {
+            for (int j = 0; j < M; ++j) std::swap(A[c * M + j], A[p * M + j]);
+            std::swap(piv[c], piv[p]);
+        }
+        for (int r = c + 1; r < M; ++r) {
+            cd f = A[r * M + c] / A[c * M + c];
+            A[r * M + c] = f;
+            for (int j = c + 1; j < M; ++j) A[r * M + j] -= f * A[c * M + j];
+        }
+    }
+    inv.assign(M * M, 0.0);
+    for (int col = 0; col < M; ++col) {
+        std::vector<cd> y(M);
+        for (int i = 0; i < M; ++i) {  // forward substitution on P e_col
+            cd s = (piv[i] == col) ? 1.0 : 0.0;
+            for (int j = 0; j < i; ++j) s -= A[i * M + j] * y[j];
+            y[i] = s;
+        }
+        for (int i = M - 1; i >= 0; --i) {
+            cd s = y[i];
+            for (int j = i + 1; j < M; ++j) s -= A[i * M + j] * inv[j * M + col];
+            inv[i * M + col] = s / A[i * M + i];
+        }
+    }
+    return true;
+}
+
+template <typename T> void push_c(std::vector<T> &v, cd z) {
+    v.push_back((T)z.real());
+    v.push_back((T)z.imag());
+}
+
+// e^{sign 2 pi i m / P} for m in [0, count) at stride `stride` (exact integer reduction)
+template <typename T> void push_roots(std::vector<T> &v, int64_t P, int64_t count, int64_t stride, int sign) {
+    for (int64_t i = 0; i < count; ++i) {
+        int64_t m = (i * stride) % P;
+        double a = 2.0 * PI * (double)m / (double)P;
+        push_c(v, cd(std::cos(a), sign * std::sin(a)));
+    }
+}
+
+}  // namespace
+
+struct mci_plan_s {
+    int path = mci::PATH_FUSED;
+    int dtype = MCI_F32;
+    unsigned flags = 0;
+    mci::Axis1D ax;          // 1D plan, or the x axis (row pass) of a 2D plan
+    mci::Axis1D ay;          // y axis (column pass) of a 2D plan
+    int Mx = 0, My = 0;
+    int64_t Nx = 0, Ny = 0, Lx = 0, Ly = 0;
+    void *tables = nullptr;  // one device block for every table
+    void *ws = nullptr;      // workspace (four-step / 2D intermediate)
+    size_t ws_bytes = 0;
+    int64_t ws_units = 0;    // signals (four-step) or images (2D) per workspace fill
+    double cond_max = 0.0;
+    // host-buffer execution (allocated on first use)
+    void *stage[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t stage_bytes[2] = {0, 0};
+    int64_t stage_rows = 0;
+    cudaStream_t hs[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+size_t esize(int dtype) { return dtype == MCI_F64 ? 8 : 4; }
+
+// Build one axis: validation, inverse tables, twiddles (host vectors, scalar type T).
+template <typename T>
+mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_system *sys, const int64_t *null_bins,
+                      int n_null, bool analytic, bool fourstep, std::vector<T> &blob, std::vector<size_t> &offs,
+                      double &cond_max) {
+    if (M < 1 || M > 8 || !sys) return MCI_E_ARG;
+    if (!is_pow2(N) || N < 2) return MCI_E_SIZE;
+    if ((M * N) % 2) return MCI_E_BAND;
+    if (!is_pow2(L) || L < M * N || L % N) return MCI_E_ALIAS;
+    const int64_t K = (int64_t)M * N / 2, K1 = -K;
+    for (int m = 0; m < M; ++m) {
+        const mci_system &s = sys[m];
+        if (s.kind < MCI_SYS_IDENTITY || s.kind > MCI_SYS_TABLE) return MCI_E_ARG;
+        if (s.kind == MCI_SYS_DERIVATIVE && s.order < 0) return MCI_E_ARG;
+        if (s.kind == MCI_SYS_TABLE) {
+            if (!s.table) return MCI_E_ARG;
+            for (int64_t k = 1; k < K; ++k) {  // Hermitian requirement of the real-output path
+                cd a = sys_multiplier(s, K1, k), b = sys_multiplier(s, K1, -k);
+                if (std::abs(a - std::conj(b)) > 1e-12 * (1 + std::abs(a))) return MCI_E_UNSUPPORTED;
+            }
+        }
+    }
+    ax.M = M; ax.N = N; ax.L = L; ax.K = K; ax.analytic = analytic ? 1 : 0;
+    ax.S = analytic ? next_pow2(K) : next_pow2(2 * K);
+    if (ax.S < 16) ax.S = std::min<int64_t>(16, L);
+    ax.R = L / ax.S;
+    // ---- inverse tables per class q = 0..N/2
+    offs.push_back(blob.size());  // Qt
+    std::vector<cd> H(M * M), inv;
+    cond_max = 0.0;
+    for (int64_t q = 0; q <= N / 2; ++q) {
+        const int64_t jq = -K + (((q + K) % N) + N) % N;
+        bool is_null = false;
+        for (int z = 0; z < n_null; ++z)
+            if (null_bins[z] == jq) is_null = true;
+        double rowmax = 0.0;
+        for (int l = 0; l < M; ++l) {
+            double rm = 0.0;
+            for (int m = 0; m < M; ++m) {
+                H[l * M + m] = sys_multiplier(sys[m], K1, jq + (int64_t)l * N);
+                rm = std::max(rm, std::abs(H[l * M + m]));
+            }
+            rowmax = std::max(rowmax, rm);
+        }
+        if (is_null) {
+            inv.assign(M * M, 0.0);
+        } else {
+            if (!lu_inverse(M, H, inv, 1e-12 * rowmax)) {
+                g_last_singular = jq;
+                return MCI_E_SINGULAR;
+            }
+            double n1 = 0, n2 = 0;
+            for (int c = 0; c < M; ++c) {
+                double s1 = 0, s2 = 0;
+                for (int r = 0; r < M; ++r) { s1 += std::abs(H[r * M + c]); s2 += std::abs(inv[r * M + c]); }
+                n1 = std::max(n1, s1);
+                n2 = std::max(n2, s2);
+            }
+            cond_max = std::max(cond_max, n1 * n2);
+        }
+        for (int m = 0; m < M; ++m)
+            for (int l = 0; l < M; ++l) push_c(blob, inv[m * M + l] / (double)N);
+    }
+    // ---- forward-sign root table e^{-2 pi i m/TW}
+    if (fourstep) ax.TW = std::max<int64_t>({1024, N / 1024, ax.S / 1024});
+    else ax.TW = std::max<int64_t>({N, ax.S, 1024});
+    offs.push_back(blob.size());
+    push_roots(blob, ax.TW, ax.TW, 1, -1);
+    // ---- two-level tables: [L/LO hi][LO lo] of e^{+2 pi i m/L} (+ N (forward), S (inverse) for four-step)
+    ax.LO = std::min<int64_t>(L, 1024);
+    offs.push_back(blob.size());
+    push_roots(blob, L, L / ax.LO, ax.LO, +1);
+    push_roots(blob, L, ax.LO, 1, +1);
+    if (fourstep) {
+        push_roots(blob, N, N / ax.LO, ax.LO, -1);
+        push_roots(blob, N, ax.LO, 1, -1);
+        push_roots(blob, ax.S, ax.S / ax.LO, ax.LO, +1);
+        push_roots(blob, ax.S, ax.LO, 1, +1);
+    }
+    return MCI_OK;
+}
+
+template <typename T>
+mci_status upload(mci_plan p, std::vector<T> &blob) {
+    void *d = nullptr;
+    if (cudaMalloc(&d, blob.size() * sizeof(T)) != cudaSuccess) return MCI_E_CUDA;
+    if (cudaMemcpy(d, blob.data(), blob.size() * sizeof(T), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return MCI_E_CUDA;
+    }
+    p->tables = d;
+    return MCI_OK;
+}
+
+void set_ptrs(mci::Axis1D &ax, void *base, const std::vector<size_t> &offs, size_t elem) {
+    char *b = (char *)base;
+    ax.Qt = b + offs[0] * elem;
+    ax.twF = b + offs[1] * elem;
+    ax.twLhi = b + offs[2] * elem;
+    ax.twLlo = b + (offs[2] + 2 * (ax.L / ax.LO)) * elem;
+}
+
+template <typename T>
+mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *sys, const int64_t *null_bins,
+                     int n_null, unsigned flags) {
+    std::vector<T> blob;
+    std::vector<size_t> offs;
+    const bool analytic = flags & MCI_OUT_HILBERT;
+    // try the fused path first
+    mci::Axis1D ax;
+    ax.dtype = p->dtype;
+    mci_status s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, false, blob, offs, p->cond_max);
+    if (s != MCI_OK) return s;
+    if (!mci::fused_supported(ax)) {
+        blob.clear();
+        offs.clear();
+        s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, true, blob, offs, p->cond_max);
+        if (s != MCI_OK) return s;
+        if (!mci::fourstep_supported(ax)) return MCI_E_UNSUPPORTED;
+        p->path = mci::PATH_FOURSTEP;
+    }
+    if ((s = upload<T>(p, blob)) != MCI_OK) return s;
+    set_ptrs(ax, p->tables, offs, sizeof(T));
+    p->ax = ax;
+    if (p->path == mci::PATH_FOURSTEP) {
+        // workspace for a chunk of signals; sized so intermediates stay L2-resident (~80 MB)
+        const size_t per = mci::fourstep_ws_bytes_per_signal(ax);
+        int64_t units = std::max<int64_t>(1, (int64_t)((96u << 20) / per));
+        units = std::min<int64_t>(units, 8);
+        p->ws_units = units;
+        p->ws_bytes = per * units;
+        if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
+    }
+    return MCI_OK;
+}
+
+template <typename T>
+mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int My, int64_t Ny,
+                     const mci_system *sy, int scale) {
+    std::vector<T> bx, by;
+    std::vector<size_t> ox, oy;
+    double cx = 0, cy = 0;
+    mci::Axis1D ax, ay;
+    ax.dtype = ay.dtype = p->dtype;
+    mci_status s = build_axis<T>(ax, Mx, Nx, (int64_t)scale * Nx, sx, nullptr, 0, false, false, bx, ox, cx);
+    if (s != MCI_OK) return s;
+    s = build_axis<T>(ay, My, Ny, (int64_t)scale * Ny, sy, nullptr, 0, false, false, by, oy, cy);
+    if (s != MCI_OK) return s;
+    if (!mci::fused_supported(ax) || !mci::fused_supported(ay)) return MCI_E_UNSUPPORTED;
+    p->cond_max = std::max(cx, cy);
+    const size_t nx = bx.size();
+    bx.insert(bx.end(), by.begin(), by.end());
+    if ((s = upload<T>(p, bx)) != MCI_OK) return s;
+    set_ptrs(ax, p->tables, ox, sizeof(T));
+    set_ptrs(ay, (char *)p->tables + nx * sizeof(T), oy, sizeof(T));
+    p->ax = ax;
+    p->ay = ay;
+    p->Mx = Mx; p->My = My; p->Nx = Nx; p->Ny = Ny; p->Lx = ax.L; p->Ly = ay.L;
+    p->path = mci::PATH_2D;
+    const size_t per = (size_t)Mx * Nx * ay.L * sizeof(T);  // column-pass intermediate per image
+    int64_t units = std::max<int64_t>(1, (int64_t)((64u << 20) / per));
+    p->ws_units = units;
+    p->ws_bytes = per * units;
+    if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
+    return MCI_OK;
+}
+
+mci_status from_cuda(cudaError_t e) { return e == cudaSuccess ? MCI_OK : MCI_E_CUDA; }
+
+mci_status exec_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf, cudaStream_t st, int *nl) {
+    if (p->path == mci::PATH_FUSED) {
+        mci::RowAddr ra;
+        ra.s2 = (int64_t)p->ax.M * p->ax.N;
+        ra.cs = p->ax.N;
+        ra.ss = 1;
+        return from_cuda(mci::launch_fused(p->ax, ra, batch, g, f, hf, st, nl));
+    }
+    return from_cuda(mci::launch_fourstep(p->ax, batch, g, f, p->ws, p->ws_units, st, nl));
+}
+
+mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t st, int *nl) {
+    const size_t es = esize(p->dtype);
+    const int64_t Mx = p->Mx, My = p->My, Nx = p->Nx, Ny = p->Ny, Lx = p->Lx, Ly = p->Ly;
+    const int64_t in_img = My * Mx * Ny * Nx, out_img = Ly * Lx;
+    for (int64_t i0 = 0; i0 < n; i0 += p->ws_units) {
+        const int64_t ni = std::min<int64_t>(p->ws_units, n - i0);
+        const char *gi = (const char *)g + i0 * in_img * es;
+        char *oi = (char *)out + i0 * out_img * es;
+        // column pass (along y, channels my) on the input -> ws[img][mx][nx][Ly]
+        mci::RowAddr rc;
+        rc.D0 = Nx; rc.D1 = Mx; rc.s0 = 1; rc.s1 = Ny * Nx; rc.s2 = My * Mx * Ny * Nx;
+        rc.cs = Mx * Ny * Nx; rc.ss = Nx;
+        cudaError_t e = mci::launch_fused(p->ay, rc, ni * Mx * Nx, gi, p->ws, nullptr, st, nl);
+        if (e != cudaSuccess) return MCI_E_CUDA;
+        // row pass (along x, channels mx) on ws -> out[img][py][Lx]
+        mci::RowAddr rr;
+        rr.D0 = Ly; rr.D1 = 1; rr.s0 = 1; rr.s1 = 0; rr.s2 = Mx * Nx * Ly;
+        rr.cs = Nx * Ly; rr.ss = Ly;
+        e = mci::launch_fused(p->ax, rr, ni * Ly, p->ws, oi, nullptr, st, nl);
+        if (e != cudaSuccess) return MCI_E_CUDA;
+    }
+    return MCI_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci_system *sys,
+                           const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags) {
+    if (!out) return MCI_E_ARG;
+    *out = nullptr;
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~MCI_OUT_HILBERT) || n_null < 0 ||
+        (n_null > 0 && !null_bins))
+        return MCI_E_ARG;
+    mci_plan p = new (std::nothrow) mci_plan_s();
+    if (!p) return MCI_E_ARG;
+    p->dtype = dtype;
+    p->flags = flags;
+    mci_status s = dtype == MCI_F64 ? create_1d<double>(p, M, N, L, sys, null_bins, n_null, flags)
+                                    : create_1d<float>(p, M, N, L, sys, null_bins, n_null, flags);
+    if (s != MCI_OK) {
+        mci_plan_destroy(p);
+        return s;
+    }
+    *out = p;
+    return MCI_OK;
+}
+
+mci_status mci_plan_create_2d(mci_plan *out, int Mx, int64_t Nx, const mci_system *sx, int My, int64_t Ny,
+                              const mci_system *sy, int scale, mci_dtype dtype, unsigned flags) {
+    if (!out) return MCI_E_ARG;
+    *out = nullptr;
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || flags != 0 || scale < 1) return MCI_E_ARG;
+    mci_plan p = new (std::nothrow) mci_plan_s();
+    if (!p) return MCI_E_ARG;
+    p->dtype = dtype;
+    mci_status s = dtype == MCI_F64 ? create_2d<double>(p, Mx, Nx, sx, My, Ny, sy, scale)
+                                    : create_2d<float>(p, Mx, Nx, sx, My, Ny, sy, scale);
+    if (s != MCI_OK) {
+        mci_plan_destroy(p);
+        return s;
+    }
+    *out = p;
+    return MCI_OK;
+}
+
+void mci_plan_destroy(mci_plan p) {
+    if (!p) return;
+    for (int i = 0; i < 2; ++i)
+        if (p->hs[i]) cudaStreamDestroy(p->hs[i]);
+    for (int i = 0; i < 4; ++i)
+        if (p->stage[i]) cudaFree(p->stage[i]);
+    if (p->ws) cudaFree(p->ws);
+    if (p->tables) cudaFree(p->tables);
+    delete p;
+}
+
+mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf, void *stream) {
+    if (!p || p->path == mci::PATH_2D || batch < 0) return MCI_E_ARG;
+    if (batch == 0) return MCI_OK;
+    if (!g || !f) return MCI_E_ARG;
+    if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
+    return exec_1d(p, batch, g, f, hf, (cudaStream_t)stream, nullptr);
+}
+
+mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out, void *stream) {
+    if (!p || p->path != mci::PATH_2D || n_images < 0) return MCI_E_ARG;
+    if (n_images == 0) return MCI_OK;
+    if (!g || !out) return MCI_E_ARG;
+    return exec_2d(p, n_images, g, out, (cudaStream_t)stream, nullptr);
+}
+
+// Host-buffer execution: two streams ping-pong over chunks (H2D, compute, D2H).
+static mci_status exec_host(mci_plan p, int64_t units, const void *g, void *f, void *hf) {
+    const size_t es = esize(p->dtype);
+    size_t in_u, out_u;
+    int nout = 1;
+    if (p->path == mci::PATH_2D) {
+        in_u = (size_t)p->My * p->Mx * p->Ny * p->Nx * es;
+        out_u = (size_t)p->Ly * p->Lx * es;
+    } else {
+        in_u = (size_t)p->ax.M * p->ax.N * es;
+        out_u = (size_t)p->ax.L * es;
+        nout = (p->flags & MCI_OUT_HILBERT) ? 2 : 1;
+    }
+    int64_t chunk = std::max<int64_t>(1, (int64_t)((64u << 20) / (out_u * nout)));
+    if (p->path == mci::PATH_2D) chunk = std::max<int64_t>(chunk, p->ws_units);
+    if (p->path == mci::PATH_FOURSTEP) chunk = std::max<int64_t>(chunk, p->ws_units);
+    chunk = std::min(chunk, units);
+    if (p->stage_rows < chunk) {
+        for (int i = 0; i < 4; ++i)
+            if (p->stage[i]) { cudaFree(p->stage[i]); p->stage[i] = nullptr; }
+        for (int b = 0; b < 2; ++b) {
+            if (cudaMalloc(&p->stage[2 * b], in_u * chunk) != cudaSuccess) return MCI_E_CUDA;
+            if (cudaMalloc(&p->stage[2 * b + 1], out_u * nout * chunk) != cudaSuccess) return MCI_E_CUDA;
+        }
+        p->stage_rows = chunk;
+    }
+    for (int b = 0; b < 2; ++b)
+        if (!p->hs[b] && cudaStreamCreateWithFlags(&p->hs[b], cudaStreamNonBlocking) != cudaSuccess) return MCI_E_CUDA;
+    // Chunk i on stream i&1: H2D_i, [wait compute_{i-1} if the plan has a
+    // shared workspace], compute_i, record, D2H_i.  Copies of one chunk overlap
+    // compute of the neighbouring chunk.
+    cudaEvent_t done[2];
+    for (int b = 0; b < 2; ++b)
+        if (cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) return MCI_E_CUDA;
+    mci_status s = MCI_OK;
+    int it = 0;
+    for (int64_t u0 = 0; u0 < units && s == MCI_OK; u0 += chunk, ++it) {
+        const int64_t n = std::min(chunk, units - u0);
+        const int b = it & 1;
+        cudaStream_t st = p->hs[b];
+        char *din = (char *)p->stage[2 * b], *dout = (char *)p->stage[2 * b + 1];
+        if (cudaMemcpyAsync(din, (const char *)g + u0 * in_u, n * in_u, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+            s = MCI_E_CUDA;
+            break;
+        }
+        if (p->ws && it > 0) cudaStreamWaitEvent(st, done[b ^ 1], 0);
+        if (p->path == mci::PATH_2D) s = exec_2d(p, n, din, dout, st, nullptr);
+        else s = exec_1d(p, n, din, dout, nout == 2 ? dout + n * out_u : nullptr, st, nullptr);
+        if (s != MCI_OK) break;
+        cudaEventRecord(done[b], st);
+        if (cudaMemcpyAsync((char *)f + u0 * out_u, dout, n * out_u, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            s = MCI_E_CUDA;
+        else if (nout == 2 && cudaMemcpyAsync((char *)hf + u0 * out_u, dout + n * out_u, n * out_u,
+                                               cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            s = MCI_E_CUDA;
+    }
+    for (int b = 0; b < 2; ++b)
+        if (cudaStreamSynchronize(p->hs[b]) != cudaSuccess) s = MCI_E_CUDA;
+    for (int b = 0; b < 2; ++b) cudaEventDestroy(done[b]);
+    return s;
+}
+
+mci_status mci_execute_1d_host(mci_plan p, int64_t batch, const void *g, void *f, void *hf) {
+    if (!p || p->path == mci::PATH_2D || batch < 0) return MCI_E_ARG;
+    if (batch == 0) return MCI_OK;
+    if (!g || !f) return MCI_E_ARG;
+    if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
+    return exec_host(p, batch, g, f, hf);
+}
+
+mci_status mci_execute_2d_host(mci_plan p, int64_t n_images, const void *g, void *out) {
+    if (!p || p->path != mci::PATH_2D || n_images < 0) return MCI_E_ARG;
+    if (n_images == 0) return MCI_OK;
+    if (!g || !out) return MCI_E_ARG;
+    return exec_host(p, n_images, g, out, nullptr);
+}
+
+double mci_plan_cond_max(mci_plan p) { return p ? p->cond_max : 0.0; }
+int64_t mci_last_singular_bin(void) { return g_last_singular; }
+size_t mci_plan_workspace_bytes(mci_plan p) { return p ? p->ws_bytes : 0; }
+int mci_plan_path(mci_plan p) { return p ? p->path : -1; }
+
+int64_t mci_plan_launches(mci_plan p, int64_t batch) {
+    if (!p || batch <= 0) return 0;
+    if (p->path == mci::PATH_FUSED) return 1;
+    const int64_t chunks = (batch + p->ws_units - 1) / p->ws_units;
+    return p->path == mci::PATH_FOURSTEP ? 3 * chunks : 2 * chunks;
+}
+
+const char *mci_status_str(mci_status s) {
+    switch (s) {
+    case MCI_OK: return "ok";
+    case MCI_E_ARG: return "invalid argument";
+    case MCI_E_BAND: return "invalid band (M*N must be even)";
+    case MCI_E_ALIAS: return "L must be a power of two, >= M*N and a multiple of N";
+    case MCI_E_SINGULAR: return "system matrix H_n singular (see mci_last_singular_bin)";
+    case MCI_E_SIZE: return "unsupported size (N must be a power of two)";
+    case MCI_E_CUDA: return "CUDA error";
+    case MCI_E_UNSUPPORTED: return "unsupported configuration";
+    }
+    return "unknown status";
+}
+
+const char *mci_version(void) { return "mci-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

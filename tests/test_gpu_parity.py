@@ -1,0 +1,251 @@
+"""GPU parity: CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerances: fp32 relative L2 per row <= 2e-6
+(BASELINE.json north_star), fp64 <= 1e-11.  Inputs are the seeded
+generators of synth/; the oracle consumes exactly the fp32 inputs the GPU
+gets, promoted to fp64."""
+import math
+import zlib
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 2e-6
+F64_TOL = 1e-11
+
+
+def mci():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1802_10291_b200 as m
+    return m
+
+
+def row_rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.linalg.norm(a - b, axis=-1) / np.linalg.norm(b, axis=-1)
+
+
+def run_plan(plan, g_np, dtype=torch.float32):
+    g = torch.from_numpy(np.ascontiguousarray(g_np)).to(device="cuda", dtype=dtype)
+    out = plan.execute(g)
+    torch.cuda.synchronize()
+    if isinstance(out, tuple):
+        return tuple(o.double().cpu().numpy() for o in out)
+    return out.double().cpu().numpy()
+
+
+BANKS = {
+    "f": [("identity",)],
+    "f_df": [("identity",), ("derivative", 1)],
+    "f_df_ddf": [("identity",), ("derivative", 1), ("derivative", 2)],
+    "f_hf": [("identity",), ("hilbert",)],
+}
+
+
+def delay_bank(M, N):
+    return [("delay", 2 * math.pi * m / (M * N)) for m in range(M)]
+
+
+# -------------------------------------------------------------------------- config 1
+def test_cfg1_fp64_exact():
+    """configs[0]: fp64, exact vs closed form and vs oracle (<= 1e-11)."""
+    m = mci()
+    c = synth.CONFIGS[1]
+    d = synth.cfg1()
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"], dtype="f64")
+    out = run_plan(plan, d["g"], torch.float64)
+    ref = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"]).eval(d["g"])
+    assert row_rel(out, d["truth"]).max() < F64_TOL
+    assert row_rel(out, ref).max() < F64_TOL
+
+
+# -------------------------------------------------------------------------- generic sweep
+SWEEP = [
+    # name, N, L, hilbert, rows
+    ("f_df", 32, 256, False, 300),      # R=4, many rows > grid (persistent loop)
+    ("f_df", 32, 64, False, 7),         # L = MN (S = 2K alias at K), R = 1
+    ("f_df_ddf", 64, 1024, False, 37),  # odd M: class q* = N/2 Hermitian averaging
+    ("f_df_ddf", 16, 64, False, 5),     # R=1 odd M
+    ("f_hf", 64, 512, False, 19),
+    ("f", 256, 4096, False, 11),
+    ("delay4", 16, 256, False, 9),
+    ("f_df", 128, 2048, True, 13),      # analytic (f + i Hf)
+    ("f_df_ddf", 64, 512, True, 9),
+    ("f_df", 512, 2048, False, 33),     # 2D pass shape
+]
+
+
+@pytest.mark.parametrize("name,N,L,hilbert,rows", SWEEP, ids=lambda v: str(v))
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_sweep_nonbandlimited(name, N, L, hilbert, rows, dtype):
+    """Arbitrary (non band-limited) channel data: every row vs the oracle."""
+    m = mci()
+    bank = delay_bank(4, N) if name == "delay4" else BANKS[name]
+    M = len(bank)
+    g = np.random.default_rng(zlib.crc32(f"{name}{N}{L}".encode())).standard_normal((rows, M, N))
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    g = g.astype(np.float64 if dtype == "f64" else np.float32)
+    plan = m.Plan(M, N, L, bank, dtype=dtype, hilbert=hilbert)
+    assert plan.path == "fused"
+    out = run_plan(plan, g, tdt)
+    P = oracle.OraclePlan(M, N, L, bank)
+    tol = F64_TOL if dtype == "f64" else F32_TOL
+    sub = g[: min(rows, 8)]
+    if hilbert:
+        f, hf = out
+        assert row_rel(f[: len(sub)], P.eval(sub)).max() < tol
+        assert row_rel(hf[: len(sub)], P.eval(sub, hilbert=True)).max() < tol
+        f_all = f
+    else:
+        assert row_rel(out[: len(sub)], P.eval(sub)).max() < tol
+        f_all = out
+    # every row: consistency at the coarse sites
+    if bank[0][0] == "identity":
+        assert np.max(np.abs(f_all[:, :: L // N] - g[:, 0])) < (1e-4 if dtype == "f32" else 1e-10) * np.abs(g).max() * M
+    # last rows too (persistent-loop tail)
+    tail = g[-3:]
+    ref_tail = P.eval(tail)
+    assert row_rel(f_all[-3:], ref_tail).max() < tol
+
+
+def test_batch_zero_and_one():
+    m = mci()
+    plan = m.Plan(2, 32, 256, BANKS["f_df"])
+    g = torch.zeros((0, 2, 32), device="cuda")
+    f = plan.execute(g)
+    assert f.shape == (0, 256)
+    g1 = np.random.default_rng(0).standard_normal((1, 2, 32)).astype(np.float32)
+    out = run_plan(plan, g1)
+    assert row_rel(out, oracle.OraclePlan(2, 32, 256, BANKS["f_df"]).eval(g1)).max() < F32_TOL
+
+
+# -------------------------------------------------------------------------- config 2
+def test_cfg2_shape_subset():
+    """configs[1] shape (M=3, N=1024, L=16384) on a seeded subset with ragged count."""
+    m = mci()
+    c = synth.CONFIGS[2]
+    rows = np.arange(45)
+    g, truth = synth.cfg2_rows(rows, with_truth=True)
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"])
+    out = run_plan(plan, g)
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    pick = [0, 17, 44]
+    assert row_rel(out[pick], P.eval(g[pick])).max() < F32_TOL
+    assert row_rel(out, truth).max() < 1e-5   # vs analytic truth (fp32 input rounding included)
+
+
+# -------------------------------------------------------------------------- config 3
+def test_cfg3_shape_hilbert():
+    """configs[2] shape: M=2 (f, f'), N=4096, L=65536, f and Hf."""
+    m = mci()
+    c = synth.CONFIGS[3]
+    g = synth.cfg3_rows(np.arange(6))
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"], hilbert=True)
+    f, hf = run_plan(plan, g)
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    pick = [0, 5]
+    assert row_rel(f[pick], P.eval(g[pick])).max() < F32_TOL
+    assert row_rel(hf[pick], P.eval(g[pick], hilbert=True)).max() < F32_TOL
+    fr, hr = synth.cfg3_reference(0)
+    assert row_rel(f[0], fr) < 1e-5 and row_rel(hf[0], hr) < 1e-5
+
+
+# -------------------------------------------------------------------------- config 4
+def test_fourstep_small_delay():
+    """Four-step path at a size the oracle tabulates: M=4, N=4096, L=65536."""
+    m = mci()
+    M, N, L = 4, 4096, 65536
+    bank = delay_bank(M, N)
+    g, _ = synth.cfg4_signals([0, 1, 2], M=M, N=N)
+    plan = m.Plan(M, N, L, bank)
+    assert plan.path == "fourstep"
+    out = run_plan(plan, g)
+    pts = np.random.default_rng(1).integers(0, L, 512)
+    for i in range(3):
+        ref = oracle.delay_eval_points(M, N, L, g[i], pts)
+        assert np.linalg.norm(out[i, pts] - ref) / np.linalg.norm(ref) < F32_TOL
+
+
+def test_fourstep_nonbandlimited_generic_bank():
+    m = mci()
+    M, N, L = 2, 8192, 32768
+    bank = BANKS["f_df"]
+    g = np.random.default_rng(3).standard_normal((2, M, N)).astype(np.float32)
+    plan = m.Plan(M, N, L, bank)
+    assert plan.path == "fourstep"
+    out = run_plan(plan, g)
+    P = oracle.OraclePlan(M, N, L, bank)
+    assert row_rel(out, P.eval(g)).max() < F32_TOL
+
+
+def test_cfg4_full_size_sampled():
+    """configs[3] at full size (batch 16, the bench launch): sampled outputs vs
+    the closed-form delay oracle, and coarse-site consistency on every signal."""
+    m = mci()
+    c = synth.CONFIGS[4]
+    M, N, L = c["M"], c["N"], c["L"]
+    g, _ = synth.cfg4_signals(np.arange(16))
+    plan = m.Plan(M, N, L, c["bank"])
+    gt = torch.from_numpy(g).cuda()
+    f = plan.execute(gt)
+    torch.cuda.synchronize()
+    pts = np.random.default_rng(4).integers(0, L, 48)
+    for i in (0, 15):
+        ref = oracle.delay_eval_points(M, N, L, g[i], pts)
+        got = f[i, torch.from_numpy(pts).cuda()].double().cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < F32_TOL
+    # P6: output at (L/N) n + (L/MN) m equals g_m[n] for every signal
+    fv = f.view(16, N, M, L // (M * N))[:, :, :, 0]          # [sig][n][m]
+    err = (fv.permute(0, 2, 1) - gt).abs().max().item()
+    assert err < 1e-5 * gt.abs().max().item()
+
+
+# -------------------------------------------------------------------------- config 5 (2D)
+def test_2d_small_vs_oracle():
+    m = mci()
+    Nn, scale = 32, 4
+    bank = BANKS["f_df"]
+    g = np.random.default_rng(5).standard_normal((3, 2, 2, Nn, Nn)).astype(np.float32)
+    plan = m.Plan2D(2, Nn, bank, 2, Nn, bank, scale)
+    gt = torch.from_numpy(g).cuda()
+    out = plan.execute(gt).double().cpu().numpy()
+    px = oracle.OraclePlan(2, Nn, Nn * scale, bank)
+    for i in range(3):
+        ref = oracle.eval_2d(g[i], px, px)
+        assert np.linalg.norm(out[i] - ref) / np.linalg.norm(ref) < F32_TOL
+
+
+def test_cfg5_full_size_sampled():
+    """configs[4] shape: 2 synthetic 2048^2 images, sampled columns vs oracle; PSNR sane."""
+    m = mci()
+    g, truths = synth.cfg5_images([0, 1])
+    plan = m.Plan2D(2, 512, BANKS["f_df"], 2, 512, BANKS["f_df"], 4)
+    out = plan.execute(torch.from_numpy(g).cuda()).double().cpu().numpy()
+    px = oracle.OraclePlan(2, 512, 2048, BANKS["f_df"])
+    cols = [0, 777, 2047]
+    for i in range(2):
+        ref = oracle.eval_2d_columns(g[i], px, px, cols)
+        assert np.linalg.norm(out[i][:, cols] - ref) / np.linalg.norm(ref) < F32_TOL
+        mse = np.mean((np.clip(out[i], 0, 255) - truths[i]) ** 2)
+        assert 10 * np.log10(255 ** 2 / mse) > 15.0
+
+
+# -------------------------------------------------------------------------- host API
+def test_host_execute_matches_device():
+    m = mci()
+    c = synth.CONFIGS[2]
+    g = synth.cfg2_rows(np.arange(300))
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"])
+    dev = run_plan(plan, g)
+    gh = torch.from_numpy(g).pin_memory()
+    fh = torch.empty((300, c["L"]), dtype=torch.float32).pin_memory()
+    plan.execute_host(gh, fh)
+    assert np.array_equal(fh.numpy(), dev.astype(np.float32))
