@@ -140,6 +140,19 @@ template <int DIR, typename V> __device__ __forceinline__ V twid(const V *__rest
     return w;
 }
 
+// Block-wide max (NT threads, red = NT/32 scratch slots).  All threads get the result.
+template <int NT, typename T> __device__ __forceinline__ T block_max(T v, T *red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    T r = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) r = fmax(r, red[w]);
+    __syncthreads();
+    return r;
+}
+
 __host__ __device__ constexpr int ilog2c(int64_t n) { return n <= 1 ? 0 : 1 + ilog2c(n / 2); }
 // radix of the next pass for an n-point FFT after `done` points combined
 __host__ __device__ constexpr int next_radix(int64_t n, int64_t done) {

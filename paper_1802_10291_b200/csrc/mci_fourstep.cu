@@ -17,6 +17,9 @@
 // Residues mod N1 line up because N1 divides N and S: class q = k mod N and
 // FFT index k' = k mod S share k mod N1, so one FB CTA owns everything a
 // residue pair needs (including the mirror classes for real-signal unpacking).
+#include <algorithm>
+#include <type_traits>
+
 #include "mci_fft.cuh"
 #include "mci_internal.h"
 
@@ -48,34 +51,66 @@ template <typename T> struct FSArgs {
     Tw2<T> twS;  // e^{+2 pi i m/S}
     Tw2<T> twL;  // e^{+2 pi i m/L}
     int64_t sig0;  // first signal of this chunk (input/output offset)
+    typename std::conditional<sizeof(T) == 4, unsigned, unsigned long long>::type *cmax;  // [sig][M] |g| max bits
 };
+
+// exponent e with max|g_m| = f 2^e, f in [0.5, 1) (0 for an all-zero channel)
+template <typename T> __device__ __forceinline__ int chan_exp(const FSArgs<T> &a, int64_t sl, int m) {
+    if (m >= a.M) return 0;
+    T mx;
+    if constexpr (sizeof(T) == 4) mx = __uint_as_float(a.cmax[sl * a.M + m]);
+    else mx = __longlong_as_double((long long)a.cmax[sl * a.M + m]);
+    int e = 0;
+    if (mx > 0) frexp(mx, &e);
+    return e;
+}
+
+// ---- channel magnitude pre-pass (exact power-of-two scaling before channel packing) ----------
+static constexpr int MX_NT = 256, MX_BLK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(MX_NT) mci_fs_max(const FSArgs<T> a) {
+    const int blk = blockIdx.x % MX_BLK;
+    const int m = (blockIdx.x / MX_BLK) % a.M;
+    const int64_t sl = blockIdx.x / ((int64_t)MX_BLK * a.M);
+    const T *g0 = a.g + ((a.sig0 + sl) * a.M + m) * a.N;
+    T v = 0;
+    for (int64_t n = (int64_t)blk * MX_NT + threadIdx.x; n < a.N; n += (int64_t)MX_BLK * MX_NT) v = fmax(v, fabs(__ldg(g0 + n)));
+    __shared__ T red[MX_NT / 32];
+    v = block_max<MX_NT>(v, red);
+    if (threadIdx.x == 0) {
+        if constexpr (sizeof(T) == 4) atomicMax(a.cmax + sl * a.M + m, __float_as_uint(v));
+        else atomicMax(a.cmax + sl * a.M + m, (unsigned long long)__double_as_longlong(v));
+    }
+}
 
 // ---- FA ------------------------------------------------------------------------------------
 static constexpr int FA_TN2 = 8, FA_NT = 256;
 
-template <typename T>
+template <typename T, int TN2>
 __global__ void __launch_bounds__(FA_NT) mci_fs_fa(const FSArgs<T> a) {
     using V = cv<T>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     V *buf = reinterpret_cast<V *>(smem_raw);  // [FA_TN2][N1]
-    const int ntiles = (int)(a.N2 / FA_TN2);
+    const int ntiles = (int)(a.N2 / TN2);
     const int tile = blockIdx.x % ntiles;
     const int c = (blockIdx.x / ntiles) % a.npair;
     const int64_t sl = blockIdx.x / ((int64_t)ntiles * a.npair);  // signal within chunk
     const T *g0 = a.g + (a.sig0 + sl) * (int64_t)a.M * a.N;
-    for (int idx = threadIdx.x; idx < FA_TN2 * N1; idx += FA_NT) {
-        const int n1 = idx / FA_TN2, t = idx % FA_TN2;
-        const int64_t n = (int64_t)n1 * a.N2 + tile * FA_TN2 + t;
+    const int e0 = chan_exp(a, sl, 2 * c), e1 = chan_exp(a, sl, 2 * c + 1);
+    for (int idx = threadIdx.x; idx < TN2 * N1; idx += FA_NT) {
+        const int n1 = idx / TN2, t = idx % TN2;
+        const int64_t n = (int64_t)n1 * a.N2 + tile * TN2 + t;
         T re = __ldg(g0 + (int64_t)(2 * c) * a.N + n);
         T im = (2 * c + 1 < a.M) ? __ldg(g0 + (int64_t)(2 * c + 1) * a.N + n) : T(0);
-        buf[t * N1 + n1] = V{re, im};
+        buf[t * N1 + n1] = V{ldexp(re, -e0), ldexp(im, -e1)};
     }
     __syncthreads();
-    block_fft_ct<T, N1, 1, -1, FA_NT, FA_TN2>(buf, N1, a.twF, a.TW);
+    block_fft_ct<T, N1, 1, -1, FA_NT, TN2>(buf, N1, a.twF, a.TW);
     V *out = a.Tw + (sl * a.npair + c) * (int64_t)N1 * a.N2;
-    for (int idx = threadIdx.x; idx < FA_TN2 * N1; idx += FA_NT) {
-        const int q1 = idx / FA_TN2, t = idx % FA_TN2;
-        const int64_t n2 = (int64_t)tile * FA_TN2 + t;
+    for (int idx = threadIdx.x; idx < TN2 * N1; idx += FA_NT) {
+        const int q1 = idx / TN2, t = idx % TN2;
+        const int64_t n2 = (int64_t)tile * TN2 + t;
         out[(int64_t)q1 * a.N2 + n2] = cmul(buf[t * N1 + q1], a.twN(n2 * q1));
     }
 }
@@ -127,6 +162,8 @@ __global__ void __launch_bounds__(FB_NT) mci_fs_fb(const FSArgs<T> a) {
             V zc = Z[((int64_t)r * npair + c) * N2 + q2], zm = cconj(Z[((int64_t)rm * npair + c) * N2 + q2m]);
             V gm = (m & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}
                            : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};
+            const int em = chan_exp(a, sl, m);
+            gm = V{ldexp(gm.x, em), ldexp(gm.y, em)};
             const V *qrow = a.Qt + (q * M + m) * M;
             for (int l = 0; l < M && l < 8; ++l) v[l] = cadd(v[l], cmul(gm, __ldg(qrow + l)));
         }
@@ -243,7 +280,7 @@ static size_t vsize(const Axis1D &ax) { return ax.dtype == MCI_F64 ? 16 : 8; }
 
 size_t fourstep_ws_bytes_per_signal(const Axis1D &ax) {
     const int64_t npair = (ax.M + 1) / 2, npi = ax.R / 2;
-    return (size_t)(npair * ax.N + npi * ax.S) * vsize(ax);
+    return (size_t)(npair * ax.N + npi * ax.S) * vsize(ax) + 8 * (size_t)ax.M;
 }
 
 static size_t fb_smem(const Axis1D &ax) {
@@ -256,7 +293,7 @@ bool fourstep_supported(const Axis1D &ax) {
     if (ax.analytic || ax.M > 8) return false;
     if (ax.N < 2 * N1 || ax.S < 2 * N1 || ax.N % N1 || ax.S % N1) return false;
     if (ax.R != 2 && ax.R != 4) return false;      // npi in {1,2}
-    if ((ax.N / N1) % FA_TN2 || (ax.S / N1) % IC_TU) return false;
+    if ((ax.S / N1) % IC_TU) return false;
     return fb_smem(ax) <= 200 * 1024;
 }
 
@@ -269,6 +306,7 @@ static cudaError_t fs_launch_t(const Axis1D &ax, int64_t batch, const void *g, v
     a.g = (const T *)g; a.f = (T *)f;
     a.Tw = (cv<T> *)ws;
     a.Uw = a.Tw + ws_sig * a.npair * ax.N;
+    a.cmax = (decltype(a.cmax))(a.Uw + ws_sig * a.npi * ax.S);
     a.Qt = (const cv<T> *)ax.Qt; a.twF = (const cv<T> *)ax.twF; a.TW = ax.TW;
     const cv<T> *const *ext = (const cv<T> *const *)nullptr;
     (void)ext;
@@ -284,20 +322,24 @@ static cudaError_t fs_launch_t(const Axis1D &ax, int64_t batch, const void *g, v
     a.twS = Tw2<T>{sb, sb + ax.S / LO, lob, ax.S - 1};
 
     const size_t vs = vsize(ax);
-    const size_t fa_sm = (size_t)FA_TN2 * N1 * vs;
+    const int tn2 = (int)std::min<int64_t>(FA_TN2, a.N2);
+    const size_t fa_sm = (size_t)tn2 * N1 * vs;
+    auto fa = tn2 == 8 ? mci_fs_fa<T, 8> : (tn2 == 4 ? mci_fs_fa<T, 4> : mci_fs_fa<T, 2>);
     const size_t fb_sm = fb_smem(ax);
     const size_t ic_sm = (size_t)a.npi * IC_TU * N1 * vs;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(mci_fs_fa<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
+    if ((e = cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fs_fb<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fs_ic<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ic_sm))) return e;
     for (int64_t s0 = 0; s0 < batch; s0 += ws_sig) {
         const int64_t ns = (batch - s0 < ws_sig) ? batch - s0 : ws_sig;
         a.sig0 = s0;
-        mci_fs_fa<T><<<(unsigned)(ns * a.npair * (a.N2 / FA_TN2)), FA_NT, fa_sm, st>>>(a);
+        if ((e = cudaMemsetAsync(a.cmax, 0, sizeof(*a.cmax) * ns * a.M, st))) return e;
+        mci_fs_max<T><<<(unsigned)(ns * a.M * MX_BLK), MX_NT, 0, st>>>(a);
+        fa<<<(unsigned)(ns * a.npair * (a.N2 / tn2)), FA_NT, fa_sm, st>>>(a);
         mci_fs_fb<T><<<(unsigned)(ns * (N1 / 2 + 1)), FB_NT, fb_sm, st>>>(a);
         mci_fs_ic<T><<<(unsigned)(ns * (a.S2 / IC_TU)), IC_NT, ic_sm, st>>>(a);
-        if (nl) *nl += 3;
+        if (nl) *nl += 4;
         if ((e = cudaGetLastError())) return e;
     }
     return cudaSuccess;

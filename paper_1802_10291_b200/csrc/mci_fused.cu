@@ -73,16 +73,41 @@ __global__ void __launch_bounds__(NT) mci_fused_kernel(const FusedArgs<T> a) {
     V *zB = slots + npair * N;
     const int ns = a.analytic ? a.G : (R > 1 ? R / 2 : 1);
     const int tid = threadIdx.x;
+    __shared__ T red[NT / 32];
+    __shared__ int escale[8];
 
     for (int64_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
         // ---- 1. load channel rows as complex pairs z_c = g_{2c} + i g_{2c+1}
         const RowAddr &ra = a.ra;
         const int64_t base = (row / (ra.D0 * ra.D1)) * ra.s2 + ((row / ra.D0) % ra.D1) * ra.s1 + (row % ra.D0) * ra.s0;
+        // Two real channels share one complex FFT; channels of very different
+        // magnitude (f vs f'' ~ K^2 f) would leak rounding error into each other,
+        // so each channel is first scaled by an exact power of two to unit range
+        // and the scale is undone after unpacking (no rounding is introduced).
+        for (int c = 0; c < npair; ++c) {
+            T m0 = 0, m1 = 0;
+            for (int n = tid; n < N; n += NT) {
+                T re = __ldg(a.g + base + (int64_t)(2 * c) * ra.cs + (int64_t)n * ra.ss);
+                T im = (2 * c + 1 < M) ? __ldg(a.g + base + (int64_t)(2 * c + 1) * ra.cs + (int64_t)n * ra.ss) : T(0);
+                zA[c * N + n] = V{re, im};
+                m0 = fmax(m0, fabs(re));
+                m1 = fmax(m1, fabs(im));
+            }
+            m0 = block_max<NT>(m0, red);
+            m1 = block_max<NT>(m1, red);
+            if (tid == 0) {
+                int e0 = 0, e1 = 0;
+                if (m0 > 0) frexp(m0, &e0);
+                if (m1 > 0) frexp(m1, &e1);
+                escale[2 * c] = e0;
+                escale[2 * c + 1] = e1;
+            }
+        }
+        __syncthreads();
         for (int idx = tid; idx < npair * N; idx += NT) {
-            int c = idx / N, n = idx - c * N;
-            T re = __ldg(a.g + base + (int64_t)(2 * c) * ra.cs + (int64_t)n * ra.ss);
-            T im = (2 * c + 1 < M) ? __ldg(a.g + base + (int64_t)(2 * c + 1) * ra.cs + (int64_t)n * ra.ss) : T(0);
-            zA[idx] = V{re, im};
+            const int c = idx / N;
+            V z = zA[idx];
+            zA[idx] = V{ldexp(z.x, -escale[2 * c]), ldexp(z.y, -escale[2 * c + 1])};
         }
         __syncthreads();
         // ---- 2. forward DFT of every pair, G_c[q] = sum_n z_c[n] e^{-2 pi i q n/N}
@@ -98,6 +123,7 @@ __global__ void __launch_bounds__(NT) mci_fused_kernel(const FusedArgs<T> a) {
                 V zc = Z[(m >> 1) * N + q], zm = cconj(Z[(m >> 1) * N + qm]);
                 V gm = (m & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}   // (zc - zm)/(2i)
                                : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};   // (zc + zm)/2
+                gm = V{ldexp(gm.x, escale[m]), ldexp(gm.y, escale[m])};
                 const V *qrow = a.Qt + ((int64_t)q * M + m) * M;
                 for (int l = 0; l < M && l < 8; ++l) v[l] = cadd(v[l], cmul(gm, __ldg(qrow + l)));
             }

@@ -486,7 +486,7 @@ int64_t mci_plan_launches(mci_plan p, int64_t batch) {
     if (!p || batch <= 0) return 0;
     if (p->path == mci::PATH_FUSED) return 1;
     const int64_t chunks = (batch + p->ws_units - 1) / p->ws_units;
-    return p->path == mci::PATH_FOURSTEP ? 3 * chunks : 2 * chunks;
+    return p->path == mci::PATH_FOURSTEP ? 4 * chunks : 2 * chunks;
 }
 
 const char *mci_status_str(mci_status s) {
