@@ -24,6 +24,7 @@ struct Axis1D {
     void *twLhi = nullptr;  // [L/LO] complex e^{+2 pi i (h*LO) / L}
     void *twLlo = nullptr;  // [LO]   complex e^{+2 pi i l / L}
     int64_t LO = 0;
+    const void *rowtab = nullptr;  // tables of the specialised row kernel (mci_row.cu), or null
 };
 
 enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2 };
@@ -40,6 +41,10 @@ cudaError_t launch_fused(const Axis1D &ax, const RowAddr &ra, int64_t rows, cons
                          void *hf, cudaStream_t st, int *n_launches);
 size_t fused_smem_bytes(const Axis1D &ax);
 bool fused_supported(const Axis1D &ax);
+
+bool row_supported(const Axis1D &ax);
+cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const void *g, void *f, cudaStream_t st,
+                       int *n_launches);
 
 cudaError_t launch_fourstep(const Axis1D &ax, int64_t batch, const void *g, void *f, void *ws,
                             int64_t ws_signals, cudaStream_t st, int *n_launches);

@@ -14,7 +14,9 @@
 #include <complex>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
+#include <type_traits>
 #include <vector>
 
 #include "mci_internal.h"
@@ -200,6 +202,18 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
     offs.push_back(blob.size());
     push_roots(blob, L, L / ax.LO, ax.LO, +1);
     push_roots(blob, L, ax.LO, 1, +1);
+    if (!fourstep && !getenv("MCI_DISABLE_ROW") && std::is_same<T, float>::value) {
+        ax.dtype = MCI_F32;
+        if (mci::row_supported(ax)) {
+            // specialised row kernel tables: [wp: K+1][ft2: 8x8][ft3: 16x64][it2: 16x16][it3: 4x256]
+            offs.push_back(blob.size());
+            push_roots(blob, L, K + 1, 1, +1);
+            for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
+            for (int j = 0; j < 16; ++j) push_roots(blob, 1024, 64, j, -1);
+            for (int j = 0; j < 16; ++j) push_roots(blob, 256, 16, j, +1);
+            for (int e = 0; e < 4; ++e) push_roots(blob, 4096, 256, 1 << e, +1);
+        }
+    }
     if (fourstep) {
         push_roots(blob, N, N / ax.LO, ax.LO, -1);
         push_roots(blob, N, ax.LO, 1, -1);
@@ -227,6 +241,7 @@ void set_ptrs(mci::Axis1D &ax, void *base, const std::vector<size_t> &offs, size
     ax.twF = b + offs[1] * elem;
     ax.twLhi = b + offs[2] * elem;
     ax.twLlo = b + (offs[2] + 2 * (ax.L / ax.LO)) * elem;
+    ax.rowtab = offs.size() > 3 ? (const void *)(b + offs[3] * elem) : nullptr;
 }
 
 template <typename T>
@@ -297,6 +312,8 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
 mci_status from_cuda(cudaError_t e) { return e == cudaSuccess ? MCI_OK : MCI_E_CUDA; }
 
 mci_status exec_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf, cudaStream_t st, int *nl) {
+    if (p->path == mci::PATH_FUSED && p->ax.rowtab)
+        return from_cuda(mci::launch_row(p->ax, p->ax.rowtab, batch, g, f, st, nl));
     if (p->path == mci::PATH_FUSED) {
         mci::RowAddr ra;
         ra.s2 = (int64_t)p->ax.M * p->ax.N;

@@ -249,3 +249,28 @@ def test_host_execute_matches_device():
     fh = torch.empty((300, c["L"]), dtype=torch.float32).pin_memory()
     plan.execute_host(gh, fh)
     assert np.array_equal(fh.numpy(), dev.astype(np.float32))
+
+
+# -------------------------------------------------------------------------- specialised row kernel
+@pytest.mark.parametrize("L,rows", [(16384, 301), (8192, 37), (16384, 1)])
+def test_row_kernel_vs_oracle_and_generic(L, rows, monkeypatch):
+    """The specialised config-2 kernel (mci_row.cu) on ragged batches (group
+    tails) and the R = 2 variant; bit-for-bit independent of batch size, and
+    within tolerance of both the oracle and the generic fused kernel."""
+    m = mci()
+    c = synth.CONFIGS[2]
+    g = synth.cfg2_rows(np.arange(rows))
+    # non-bandlimited rows too (class q* averaging on odd M)
+    g[::2] = np.random.default_rng(7).standard_normal(g[::2].shape).astype(np.float32) * g[::2].std(axis=2, keepdims=True)
+    plan = m.Plan(3, 1024, L, c["bank"])
+    out = run_plan(plan, g)
+    P = oracle.OraclePlan(3, 1024, L, c["bank"])
+    pick = sorted({0, rows // 2, rows - 1} | ({1} if rows > 1 else set()))
+    assert row_rel(out[pick], P.eval(g[pick])).max() < F32_TOL
+    monkeypatch.setenv("MCI_DISABLE_ROW", "1")
+    generic = m.Plan(3, 1024, L, c["bank"])
+    out_g = run_plan(generic, g)
+    assert row_rel(out, out_g).max() < F32_TOL
+    # a single row computed alone gives the same bits
+    one = run_plan(plan, g[-1:])
+    assert np.array_equal(one[0], out[-1])
