@@ -260,3 +260,76 @@ __device__ cv<T> *block_fft_rt(cv<T> *a, cv<T> *b, int n, int batch, int bstride
 }
 
 }  // namespace mci
+
+// ---------------------------------------------------------------------------------------
+// Compile-time two-stage codelets (radix 32 = 4 x 8, radix 64 = 8 x 8) with constant
+// twiddles from a 64th-root table (exact zeros/ones at the quadrant points).
+namespace mci {
+namespace cl {
+// cos(2 pi e / 64), e = 0..16 (rounded from long double)
+constexpr double C64[17] = {
+    1.0, 0.99518472667219688624, 0.98078528040323044913, 0.95694033573220886494, 0.92387953251128675613,
+    0.88192126434835502971, 0.83146961230254523708, 0.77301045336273696081, 0.70710678118654752440,
+    0.63439328416364549822, 0.55557023301960222474, 0.47139673682599764856, 0.38268343236508977173,
+    0.29028467725446236764, 0.19509032201612826785, 0.09801714032956060199, 0.0};
+constexpr double cos64(int e) {
+    e = ((e % 64) + 64) % 64;
+    return e <= 16 ? C64[e] : (e <= 32 ? -C64[32 - e] : (e <= 48 ? -C64[e - 32] : C64[64 - e]));
+}
+constexpr double sin64(int e) { return cos64(e - 16); }
+
+template <int B, int E, typename F> __device__ __forceinline__ void static_for(F &&f) {
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+// v * e^{DIR 2 pi i E / R}, R | 64, E compile-time
+template <int R, int E, int DIR, typename V> __device__ __forceinline__ V twc(V v) {
+    using S = decltype(v.x);
+    constexpr int e64 = (((E % R) + R) % R) * (64 / R);
+    if constexpr (e64 == 0) return v;
+    else if constexpr (e64 == 16) return rot<DIR>(v);
+    else if constexpr (e64 == 32) return V{-v.x, -v.y};
+    else if constexpr (e64 == 48) return rot<-DIR>(v);
+    else {
+        constexpr S c = (S)cos64(e64);
+        constexpr S s = (S)(DIR * sin64(e64));
+        return V{v.x * c - v.y * s, v.x * s + v.y * c};
+    }
+}
+
+// DFT of size R1*R2 on x[n1 + R1 n2] -> natural order x[k], k = k2 + R2 k1.
+template <int R1, int R2, int DIR, typename V> __device__ __forceinline__ void dft2s(V *x) {
+    constexpr int R = R1 * R2;
+    V y[R];
+    static_for<0, R1>([&](auto n1c) {
+        constexpr int n1 = decltype(n1c)::value;
+        V t[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2) t[n2] = x[n1 + R1 * n2];
+        dft<R2, DIR>(t);
+        static_for<0, R2>([&](auto k2c) {
+            constexpr int k2 = decltype(k2c)::value;
+            y[n1 + R1 * k2] = twc<R, n1 * k2, DIR>(t[k2]);
+        });
+    });
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) {
+        V t[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) t[n1] = y[n1 + R1 * k2];
+        dft<R1, DIR>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) x[k2 + R2 * k1] = t[k1];
+    }
+}
+
+template <int R, int DIR, typename V> __device__ __forceinline__ void dft_big(V *x) {
+    if constexpr (R == 32) dft2s<4, 8, DIR>(x);
+    else if constexpr (R == 64) dft2s<8, 8, DIR>(x);
+    else dft<R, DIR>(x);
+}
+}  // namespace cl
+}  // namespace mci

@@ -25,6 +25,7 @@ struct Axis1D {
     void *twLlo = nullptr;  // [LO]   complex e^{+2 pi i l / L}
     int64_t LO = 0;
     const void *rowtab = nullptr;  // tables of the specialised row kernel (mci_row.cu), or null
+    int bank_deriv012 = 0;         // bank is exactly (1, ik, -k^2): closed-form inverse available
 };
 
 enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2 };

@@ -205,13 +205,18 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
     if (!fourstep && !getenv("MCI_DISABLE_ROW") && std::is_same<T, float>::value) {
         ax.dtype = MCI_F32;
         if (mci::row_supported(ax)) {
-            // specialised row kernel tables: [wp: K+1][ft2: 8x8][ft3: 16x64][it2: 16x16][it3: 4x256]
+            // Example 2 bank (f, f', f'') with no null bins: the row kernel evaluates the
+            // paper's closed-form H^{-1} instead of reading the table
+            ax.bank_deriv012 = (M == 3 && n_null == 0 && sys[0].kind == MCI_SYS_IDENTITY &&
+                                sys[1].kind == MCI_SYS_DERIVATIVE && sys[1].order == 1 &&
+                                sys[2].kind == MCI_SYS_DERIVATIVE && sys[2].order == 2 && !getenv("MCI_ROW_QTAB"))
+                                   ? 1 : 0;
+            // specialised row kernel tables: [wp: K+1][fw2: 32x32][it1: 8x64][it2: 8x64]
             offs.push_back(blob.size());
             push_roots(blob, L, K + 1, 1, +1);
-            for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
-            for (int j = 0; j < 16; ++j) push_roots(blob, 1024, 64, j, -1);
-            for (int j = 0; j < 16; ++j) push_roots(blob, 256, 16, j, +1);
-            for (int e = 0; e < 4; ++e) push_roots(blob, 4096, 256, 1 << e, +1);
+            for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, -1);
+            for (int j = 0; j < 8; ++j) push_roots(blob, 4096, 64, j, +1);
+            for (int j = 0; j < 8; ++j) push_roots(blob, 4096, 64, 8 * j, +1);
         }
     }
     if (fourstep) {

@@ -1,34 +1,41 @@
 // Specialised fused MCI row kernel for the batched real-output shape
-// (BASELINE.json configs[1]: M = 3 channels f, f', f'', N = 1024, L = 16384).
+// (BASELINE.json configs[1]: M = 3 channels, N = 1024, L = 16384, fp32).
 //
 // Same mathematics as mci_fused.cu (Lemma 1 forward DFT PAPER.md:180-233,
 // per-class solve a = D H^{-1} Eq. matrixeqn1, Hermitian-part
-// assembly, zero-padded inverse of Eq. DFTexpression), laid
-// out for B200:
-//   * CTA = G independent row groups of 256 threads (named barriers), sharing
-//     one shared-memory copy of the per-class inverse tables Q~;
-//   * input rows arrive by TMA bulk copy (cp.async.bulk + mbarrier), the next
-//     row is prefetched while the current one is transformed;
-//   * forward: two complex 1024-point FFTs (channel pairs), radix 8/8/16;
-//   * the solve writes the pre-twiddled inputs of both inverse FFTs directly
-//     (Zin_c(k) = Y(k) T_c(k), T_c = w^{2ck} + i w^{(2c+1)k}, w = e^{2 pi i/L});
-//   * inverse: two 4096-point FFTs, three register radix-16 passes, 16 points
-//     per thread, padded shared-memory exchanges (conflict-free);
-//   * the last pass hands results straight to 128-bit streaming stores:
-//     thread t owns p2 = t + 256 j and writes f[4 p2 .. 4 p2 + 3].
+// assembly, zero-padded inverse of Eq. DFTexpression).
+// B200 layout (the binding resource is the shared-memory/L1 data pipe, so the
+// design minimises shared-memory round trips):
+//   * CTA = G row groups of 128 threads (4 warps) with named barriers; input
+//     rows arrive by TMA bulk copy (cp.async.bulk + mbarrier), the next row is
+//     prefetched while the current one is transformed;
+//   * forward: two complex 1024-point FFTs (channel pairs (g0,g1), (g2,0)) as
+//     two register radix-32 passes (one shared-memory exchange);
+//   * per-class solve: Q from a shared table, or -- for the (f, f', f'') bank --
+//     the paper's closed-form inverse of Example 2, exact in
+//     fp32 (integer numerators over powers of two);
+//   * the solve writes the pre-twiddled inputs of the two inverse FFTs
+//     (A: p1 = 0,1 and B: p1 = 2,3; Zin(k) = Y(k)(w^{2ck} + i w^{(2c+1)k}));
+//   * inverse: two 4096-point FFTs as two register radix-64 passes; lanes 0-15
+//     of every warp run FFT A and lanes 16-31 FFT B on the same butterfly
+//     index, so one warp-wide 64-bit store writes 256 contiguous output bytes
+//     (A: f[4p2], f[4p2+1]; B: f[4p2+2], f[4p2+3]);
+//   * shared buffers use XOR swizzles (conflict-free for both access strides);
+//   * all complex arithmetic runs on packed FP32x2 instructions (FADD2/FFMA2/
+//     FMUL2, mci_pk.cuh): same FLOP rate as scalar FFMA, half the issue slots.
 #include <cstdint>
 
 #include "mci_fft.cuh"
 #include "mci_internal.h"
+#include "mci_pk.cuh"
 
 namespace mci {
 
 namespace rowk {
 
-constexpr int NT = 256;
+constexpr int NT = 128;  // threads per row group
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -53,347 +60,311 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "r"(a), "r"(parity)
             : "memory");
 }
-__device__ __forceinline__ void group_bar(int id) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory");
+__device__ __forceinline__ void tma_store_1d(void *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ __forceinline__ void tma_store_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory"); }
 
-__device__ __forceinline__ int pad16(int a) { return a + (a >> 4); }
-__device__ __forceinline__ int pad8(int a) { return a + (a >> 3); }
+// swizzles (8-byte elements; bank pair = low 4 bits): conflict-free for contiguous
+// runs and for the radix-R transposed stores (stride R)
+__device__ __forceinline__ int swz32(int a) { return a ^ ((a >> 5) & 15); }
+__device__ __forceinline__ int swz64(int a) { return a ^ ((a >> 6) & 15); }
+
+// 2^e as an exact float (|e| <= 100)
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 
 }  // namespace rowk
 
-// Device tables built by the plan (fp64-rounded), see mci_plan.cpp build_row_tables().
+// Device tables built by the plan (fp64-rounded), see mci_plan.cpp.
 struct RowTables {
-    const float2 *Qt;   // [(N/2+1)][M][M]  H^{-1}/N per class
-    const float2 *wp;   // [K+1]  e^{+2 pi i p / L}
-    const float2 *ft2;  // [8][8]    e^{-2 pi i j k / 64}
-    const float2 *ft3;  // [16][64]  e^{-2 pi i j k / 1024}
-    const float2 *it2;  // [16][16]  e^{+2 pi i j k / 256}
-    const float2 *it3;  // [4][256]  e^{+2 pi i 2^e t / 4096}, e = 0..3
+    const float2 *Qt;   // [(N/2+1)][M][M]  H^{-1}/N per class (table mode)
+    const float2 *wp;   // [K+1]      e^{+2 pi i p / L}
+    const float2 *fw2;  // [32][32]   e^{-2 pi i j k / 1024}     (forward pass 2)
+    const float2 *it1;  // [8][64]    e^{+2 pi i j1 t / 4096}    (inverse pass 2, j1 = 0..7)
+    const float2 *it2;  // [8][64]    e^{+2 pi i 8 j2 t / 4096}  (j2 = 0..7)
+    int deriv;          // 1: bank is (1, ik, -k^2) -> closed-form Q (Example 2)
 };
 
-template <int M, int N, int S, int NPI, int G>
+template <int G, bool QTAB>
 struct RowCfg {
-    static constexpr int K = M * N / 2;
-    static constexpr int L = 2 * NPI * S;
-    static constexpr int NPAIR = (M + 1) / 2;
+    static constexpr int M = 3, N = 1024, S = 4096, K = 1536, L = 16384;
     static constexpr int NQ = N / 2 + 1;
-    static constexpr int FWD_STRIDE = N + N / 8;        // padded forward buffer per pair
-    static constexpr int INV_STRIDE = S + S / 16;       // padded inverse buffer
-    static constexpr int STAGE_BYTES = M * N * 4;
-    // per-group shared layout (bytes)
-    static constexpr int OFF_STAGE = 0;
-    static constexpr int OFF_BUF = STAGE_BYTES;                       // NPI... inverse buffers (8B each)
-    static constexpr int NBUF = NPI < 2 ? 2 : NPI;                    // forward aliases buffer 1
-    static constexpr int GROUP_BYTES = STAGE_BYTES + NBUF * INV_STRIDE * 8;
-    static constexpr int Q_BYTES = NQ * M * M * 8;
-    static constexpr int TAB_BYTES = (8 * 8 + 16 * 64 + 16 * 16) * 8;
+    static constexpr int STAGE_BYTES = M * N * 4;          // 12 KB
+    static constexpr int BUF_BYTES = S * 8;                 // 32 KB per inverse buffer
+    static constexpr int GROUP_BYTES = STAGE_BYTES + 2 * BUF_BYTES + 64;  // B offset by 64 B from A
+    static constexpr int Q_BYTES = QTAB ? NQ * M * M * 8 : 0;
+    static constexpr int TAB_BYTES = (32 * 32 + 2 * 8 * 64 + K + 2) * 8;
     static constexpr int SMEM = G * GROUP_BYTES + Q_BYTES + TAB_BYTES;
-    static_assert(N == 1024 && S == 4096, "specialised for N=1024, S=4096");
-    static_assert(NPAIR == 2, "two channel pairs (M = 3 or 4)");
-    static_assert(S > 2 * K, "no alias bin at K");
-    static_assert(2 * FWD_STRIDE <= INV_STRIDE, "forward buffers alias one inverse buffer");
 };
 
-template <int M, int N, int S, int NPI, int G>
+template <int G, bool QTAB>
 __global__ void __launch_bounds__(G * rowk::NT, 1)
     mci_row_kernel(const float *__restrict__ g, float *__restrict__ f, int64_t rows, RowTables tb) {
     using namespace rowk;
-    using C = RowCfg<M, N, S, NPI, G>;
-    constexpr int K = C::K, L = C::L;
+    using C = RowCfg<G, QTAB>;
+    constexpr int M = C::M, N = C::N, S = C::S, K = C::K, L = C::L;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar[G];
-    __shared__ float red[G][NT / 32][4];
+    __shared__ float ssup[G][4];
 
     const int grp = threadIdx.x / NT;
-    const int t = threadIdx.x % NT;
+    const int tid = threadIdx.x % NT;
+    const int warp = tid >> 5, lane = tid & 31;
     const int barid = 1 + grp;
     unsigned char *gbase = smem + grp * C::GROUP_BYTES;
-    float *stage = reinterpret_cast<float *>(gbase + C::OFF_STAGE);
-    float2 *bufA = reinterpret_cast<float2 *>(gbase + C::OFF_BUF);
-    float2 *bufB = bufA + C::INV_STRIDE;
-    float2 *fwd = bufB;  // forward spectra alias buffer B
+    float *stage = reinterpret_cast<float *>(gbase);
+    float2 *bufA = reinterpret_cast<float2 *>(gbase + C::STAGE_BYTES);
+    float2 *bufB = bufA + S + 8;  // +64 B: A and B lanes of a half-warp hit different banks
+    float2 *fwd = bufB;  // forward spectra (2 x 1024) alias buffer B
     float2 *Qs = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES);
-    float2 *ft2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
-    float2 *ft3 = ft2 + 64;
-    float2 *it2 = ft3 + 16 * 64;
+    float2 *fw2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
+    float2 *it1 = fw2 + 32 * 32;
+    float2 *it2 = it1 + 8 * 64;
+    float2 *wps = it2 + 8 * 64;  // e^{+2 pi i p / L}, p = 0..K
 
-    // ---- one-time setup: shared tables, per-thread pass-3 twiddle bases, barriers
-    for (int i = threadIdx.x; i < C::NQ * M * M; i += G * NT) Qs[i] = tb.Qt[i];
-    for (int i = threadIdx.x; i < 64; i += G * NT) ft2[i] = tb.ft2[i];
-    for (int i = threadIdx.x; i < 16 * 64; i += G * NT) ft3[i] = tb.ft3[i];
-    for (int i = threadIdx.x; i < 16 * 16; i += G * NT) it2[i] = tb.it2[i];
-    const float2 b1 = tb.it3[t], b2 = tb.it3[256 + t], b4 = tb.it3[512 + t], b8 = tb.it3[768 + t];
-    if (t == 0) mbar_init(&mbar[grp], 1);
+    // ---- one-time setup
+    if constexpr (QTAB)
+        for (int i = threadIdx.x; i < C::NQ * M * M; i += G * NT) Qs[i] = tb.Qt[i];
+    for (int i = threadIdx.x; i < 32 * 32; i += G * NT) fw2[i] = tb.fw2[i];
+    for (int i = threadIdx.x; i < 8 * 64; i += G * NT) {
+        it1[i] = tb.it1[i];
+        it2[i] = tb.it2[i];
+    }
+    for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
+    if (tid == 0) mbar_init(&mbar[grp], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
     const int64_t gid = (int64_t)blockIdx.x * G + grp;
     const int64_t gstride = (int64_t)gridDim.x * G;
     uint32_t phase = 0;
-    if (t == 0 && gid < rows) {
+    if (tid == 0 && gid < rows) {
         mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
         tma_load_1d(stage, g + gid * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
     }
 
+    // forward FFTs run on two warps per group; group 0 uses warps 0-1 and group 1
+    // warps 2-3 so the two groups' forward phases land on different SM sub-partitions
+    const int fw = warp - 2 * (grp & 1);  // 0 / 1 for the forward warps
+    const bool fwd_warp = fw == 0 || fw == 1;
+    // inverse FFT lane mapping: even lanes FFT A, odd lanes FFT B, same butterfly t,
+    // so every half-warp output store covers 128 contiguous bytes
+    const int h = lane & 1;
+    const int t = 16 * warp + (lane >> 1);
+
     for (int64_t row = gid; row < rows; row += gstride) {
+        using namespace pkx;
         mbar_wait(&mbar[grp], phase);
         phase ^= 1;
 
-        // ---- per-channel max |g| -> exact power-of-two scale (see mci_fused.cu)
+        // ---- forward: two register radix-32 passes; FFT c = fw on the channel pair
+        //      (g_{2c}, g_{2c+1}); channels scaled to unit range by exact powers of two
+        //      (avoids cross-channel rounding leakage when |f''| >> |f|)
         {
-            float mx[4] = {0.f, 0.f, 0.f, 0.f};
+            const int c = fw, i = lane;
+            float2 *F = fwd + (c & 1) * N;
+            pk x[32];
+            if (fwd_warp) {  // pass 1: radix 32, Ls = 1, from the staged rows
+                const float *g0 = stage + (2 * c) * N;
+                const float *g1 = stage + (2 * c + 1) * N;
+                float m0 = 0.f, m1 = 0.f;
 #pragma unroll
-            for (int m = 0; m < M; ++m) {
-                const float4 v = reinterpret_cast<const float4 *>(stage + m * N)[t];
-                mx[m] = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+                for (int j = 0; j < 32; ++j) {
+                    const float re = g0[i + 32 * j];
+                    const float im = c == 0 ? g1[i + 32 * j] : 0.f;
+                    x[j] = mk(re, im);
+                    m0 = fmaxf(m0, fabsf(re));
+                    m1 = fmaxf(m1, fabsf(im));
+                }
 #pragma unroll
-                for (int o = 16; o; o >>= 1) mx[m] = fmaxf(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+                for (int o = 16; o; o >>= 1) {
+                    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+                    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+                }
+                const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
+                const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
+                const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
+                const pk sc = mk(pow2f(-e0), pow2f(-e1));
+                if (lane == 0) {
+                    ssup[grp][2 * c] = pow2f(e0);
+                    ssup[grp][2 * c + 1] = pow2f(e1);
+                }
+#pragma unroll
+                for (int j = 0; j < 32; ++j) x[j] = pkx::mul(x[j], sc);
+                pkx::dft<32, -1>(x);
             }
-            if ((t & 31) == 0)
+            group_bar(barid);  // previous row's reads of buffers A/B are complete
+            if (fwd_warp) {
 #pragma unroll
-                for (int m = 0; m < M; ++m) red[grp][t >> 5][m] = mx[m];
-        }
-        group_bar(barid);  // also: previous row's reads of bufA/bufB are complete
-        // exact power-of-two scales: max|g_m| = f 2^e, f in [0.5, 1); multiply by 2^-e before
-        // packing, by 2^e after unpacking (bit-built powers of two, no rounding)
-        float sdn[4], sup[4];
-#pragma unroll
-        for (int m = 0; m < 4; ++m) {
-            float v = 0.f;
-            if (m < M)
-#pragma unroll
-                for (int w = 0; w < NT / 32; ++w) v = fmaxf(v, red[grp][w][m]);
-            const int E = (__float_as_int(v) >> 23) & 0xff;
-            const int e = E == 0 ? 0 : max(-100, min(100, E - 126));
-            sdn[m] = __int_as_float((127 - e) << 23);
-            sup[m] = __int_as_float((127 + e) << 23);
-        }
-
-        // ---- forward pass F1: radix 8, Ls = 1 (reads the staged rows, applies the scales)
-        {
-            const int c = t >> 7, i = t & 127;
-            const float *g0 = stage + (2 * c) * N;
-            const float *g1 = stage + (2 * c + 1) * N;
-            const float s0 = c ? sdn[2] : sdn[0], s1 = c ? sdn[3] : sdn[1];
-            float2 x[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float re = g0[i + 128 * j];
-                const float im = (2 * c + 1 < M) ? g1[i + 128 * j] : 0.f;
-                x[j] = make_float2(re * s0, im * s1);
+                for (int j = 0; j < 32; ++j) F[swz32(32 * i + j)] = f2(x[j]);
             }
-            dft<8, -1>(x);
-            float2 *F = fwd + c * C::FWD_STRIDE;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) F[pad8(8 * i + j)] = x[j];
-        }
-        group_bar(barid);
-        // the staged input has been consumed: prefetch the next row
-        if (t == 0 && row + gstride < rows) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
-            tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
-        }
-        // ---- F2: radix 8, Ls = 8
-        {
-            const int c = t >> 7, i = t & 127, k = i & 7;
-            float2 *F = fwd + c * C::FWD_STRIDE;
-            float2 x[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[j] = F[pad8(i + 128 * j)];
             group_bar(barid);
+            if (tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
+                tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
+            }
+            if (fwd_warp) {  // pass 2: radix 32, Ls = 32, in place on own positions
 #pragma unroll
-            for (int j = 1; j < 8; ++j) x[j] = cmul(x[j], ft2[j * 8 + k]);
-            dft<8, -1>(x);
+                for (int j = 0; j < 32; ++j) x[j] = mk(F[swz32(i + 32 * j)]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) F[pad8((i - k) * 8 + k + 8 * j)] = x[j];
+                for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], mk(fw2[j * 32 + i]));
+                pkx::dft<32, -1>(x);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) F[swz32(i + 32 * j)] = f2(x[j]);
+            }
+            group_bar(barid);
         }
-        group_bar(barid);
-        // ---- F3: radix 16, Ls = 64 (in place on own positions)
-        if (t < 128) {
-            const int c = t >> 6, i = t & 63;
-            float2 *F = fwd + c * C::FWD_STRIDE;
-            float2 x[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) x[j] = F[pad8(i + 64 * j)];
-#pragma unroll
-            for (int j = 1; j < 16; ++j) x[j] = cmul(x[j], ft3[j * 64 + i]);
-            dft<16, -1>(x);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) F[pad8(i + 64 * j)] = x[j];
-        }
-        group_bar(barid);
 
-        // ---- solve (M = 3: j_q = q - N for 0 < q < N/2, elements q - N, q, q + N).
-        // Thread t owns classes t and t + 256; thread 0 also the two self-mirror
-        // classes q = 0 and q* = N/2 (Hermitian-part averaging).
-        static_assert(M == 3, "solve specialised for M = 3");
-        float2 zq[3][2], zm[3][2];
+        // ---- solve.  M = 3: for 0 < q < N/2 the class is j_q = q - N with elements
+        //      q - N, q, q + N; the self-mirror classes q = 0 and q* = N/2 are done by
+        //      thread 0 with the Hermitian-part averaging.
+        pk zq[5][2], zm[5][2];
 #pragma unroll
-        for (int u = 0; u < 3; ++u) {
-            const int q = (u < 2) ? t + 256 * u : N / 2;
+        for (int u = 0; u < 5; ++u) {
+            const int q = u < 4 ? tid + 128 * u : N / 2;
             const int qm = (N - q) & (N - 1);
-            if (u < 2 || t == 0) {
+            if (u < 4 || tid == 0) {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    zq[u][c] = fwd[c * C::FWD_STRIDE + pad8(q)];
-                    zm[u][c] = fwd[c * C::FWD_STRIDE + pad8(qm)];
+                    zq[u][c] = mk(fwd[c * N + swz32(q)]);
+                    zm[u][c] = mk(fwd[c * N + swz32(qm)]);
                 }
             }
         }
+        float hs[3];  // 2^e_m / 2 (the 1/2 of the channel-pair unpacking folded in)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) hs[m] = 0.5f * ssup[grp][m];
         group_bar(barid);  // forward spectra read: buffer B may now be overwritten
 
-        // write the pre-twiddled inputs of both inverse FFTs for position p with
-        // value X = X[p]:  Zin_A(k) = X (1 + i w^k), Zin_B(k) = X (w^2k + i w^3k),
-        // and the mirrored k' = S - p with conj(X) (Hermitian spectrum).
-        auto emit = [&](int p, float2 X) {
-            const float2 a = __ldg(tb.wp + p);
-            const float2 P1 = cmul(X, a);
-            bufA[pad16(p)] = make_float2(X.x - P1.y, X.y + P1.x);
-            if (p > 0) bufA[pad16(S - p)] = make_float2(X.x + P1.y, -X.y + P1.x);
-            if constexpr (NPI == 2) {
-                const float2 P2 = cmul(P1, a);
-                const float2 P3 = cmul(P2, a);
-                bufB[pad16(p)] = make_float2(P2.x - P3.y, P2.y + P3.x);
-                if (p > 0) bufB[pad16(S - p)] = make_float2(P2.x + P3.y, -P2.y + P3.x);
+        auto emit = [&](int p, pk X) {
+            const pk a = mk(wps[p]);
+            const pk P1 = pkx::cmul(X, a);
+            const pk P2 = pkx::cmul(P1, a);
+            const pk P3 = pkx::cmul(P2, a);
+            bufA[swz64(p)] = f2(add_rot<1>(X, P1));  // X + i P1
+            bufB[swz64(p)] = f2(add_rot<1>(P2, P3));
+            if (p > 0) {  // k' = S - p: conj(X) + i conj(P1)
+                bufA[swz64(S - p)] = f2(add_rot<1>(pkx::conj(X), pkx::conj(P1)));
+                bufB[swz64(S - p)] = f2(add_rot<1>(pkx::conj(P2), pkx::conj(P3)));
             }
         };
-        auto solve = [&](int u, int q, float2 *v) {
-            float2 gm[3];
+        auto solve = [&](const pk *zqu, const pk *zmu, int q, pk *v) {
+            // channel-pair unpacking: G_{2c} = (Z[q] + conj Z[-q])/2, G_{2c+1} = (Z[q] - conj Z[-q])/(2i)
+            const pk g0 = pkx::mul(add(zqu[0], pkx::conj(zmu[0])), bc(hs[0]));
+            const pk g1 = pkx::mul(rot<-1>(sub(zqu[0], pkx::conj(zmu[0]))), bc(hs[1]));
+            const pk g2 = pkx::mul(add(zqu[1], pkx::conj(zmu[1])), bc(hs[2]));
+            if constexpr (QTAB) {
+                const float2 *Qq = Qs + q * 9;
 #pragma unroll
-            for (int m = 0; m < 3; ++m) {
-                const float2 a = zq[u][m >> 1], b = cconj(zm[u][m >> 1]);
-                const float2 w = (m & 1) ? make_float2(0.5f * (a.y - b.y), -0.5f * (a.x - b.x))
-                                         : make_float2(0.5f * (a.x + b.x), 0.5f * (a.y + b.y));
-                gm[m] = make_float2(w.x * sup[m], w.y * sup[m]);
-            }
-            const float2 *Qq = Qs + q * 9;
-#pragma unroll
-            for (int l = 0; l < 3; ++l) {
-                float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int m = 0; m < 3; ++m) {
-                    const float2 qv = Qq[m * 3 + l];
-                    acc.x = fmaf(gm[m].x, qv.x, fmaf(-gm[m].y, qv.y, acc.x));
-                    acc.y = fmaf(gm[m].x, qv.y, fmaf(gm[m].y, qv.x, acc.y));
+                for (int l = 0; l < 3; ++l) {
+                    pk acc = pkx::cmul(g0, mk(Qq[l]));
+                    acc = add(acc, pkx::cmul(g1, mk(Qq[3 + l])));
+                    v[l] = add(acc, pkx::cmul(g2, mk(Qq[6 + l])));
                 }
-                v[l] = acc;
+            } else {
+                // Example 2, paper's L = N, n = j_q; divided by N (d = G/N).
+                // Every numerator is an integer < 2^24 and every denominator a power of
+                // two, so these entries are exact in fp32.
+                const float n = (float)(-K + ((q + K) % N));
+                const float Nf = (float)N;
+                const float d2 = 1.f / (2.f * Nf * Nf * Nf), d1 = 1.f / (Nf * Nf * Nf);
+                const float r0[3] = {(2.f * Nf * Nf + 3.f * Nf * n + n * n) * d2, -(n * (2.f * Nf + n)) * d1,
+                                     (n * (Nf + n)) * d2};
+                const float r1[3] = {(3.f * Nf + 2.f * n) * d2, -2.f * (Nf + n) * d1, (Nf + 2.f * n) * d2};
+                const float r2[3] = {-d2, d1, -d2};
+                const pk ig1 = rot<1>(g1);  // i G1
+#pragma unroll
+                for (int l = 0; l < 3; ++l)  // v = G0 r0 + i G1 r1 + G2 r2
+                    v[l] = pkx::fma(g2, bc(r2[l]), pkx::fma(ig1, bc(r1[l]), pkx::mul(g0, bc(r0[l]))));
             }
         };
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int q = t + 256 * u;
-            float2 v[3];
-            solve(u, q, v);
+        for (int u = 0; u < 4; ++u) {
+            const int q = tid + 128 * u;
+            pk v[3];
+            solve(zq[u], zm[u], q, v);
             if (q != 0) {
-                emit(N - q, cconj(v[0]));
+                emit(N - q, pkx::conj(v[0]));
                 emit(q, v[1]);
                 emit(q + N, v[2]);
-            } else {  // q = 0: elements -N, 0, N
-                emit(0, make_float2(v[1].x, 0.f));
-                emit(N, make_float2(0.5f * (v[2].x + v[0].x), 0.5f * (v[2].y - v[0].y)));
+            } else {  // q = 0: elements -N, 0, N; X[0] = Re a(0), X[N] = (a(N) + conj a(-N))/2
+                emit(0, mk(f2(v[1]).x, 0.f));
+                emit(N, pkx::mul(add(v[2], pkx::conj(v[0])), bc(0.5f)));
             }
         }
-        if (t == 0) {  // q* = N/2: elements -3N/2 = -K, -N/2, N/2
-            float2 v[3];
-            solve(2, N / 2, v);
-            emit(K, make_float2(0.5f * v[0].x, -0.5f * v[0].y));
-            emit(N / 2, make_float2(0.5f * (v[2].x + v[1].x), 0.5f * (v[2].y - v[1].y)));
+        if (tid == 0) {  // q* = N/2: elements -3N/2 = -K, -N/2, N/2
+            pk v[3];
+            solve(zq[4], zm[4], N / 2, v);
+            emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)));
+            emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)));
         }
         group_bar(barid);
 
-        // ---- inverse FFTs: three radix-16 passes, A and B interleaved around barriers
-        float2 xa[16], xb[16];
-        // I1 loads (Ls = 1): zero-padding positions (K, S-K) are not read
+        // ---- inverse pass 1: radix 64, Ls = 1.  Lane pair (2s, 2s+1) runs FFTs A and B
+        //      on butterfly t; zero-padding inputs k' in (K, S-K) are not read.
+        float2 *buf = h ? bufB : bufA;
+        pk x[64];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int kp = t + 256 * j;
-            const bool nz = (kp <= K) || (kp >= S - K);
-            xa[j] = nz ? bufA[pad16(kp)] : make_float2(0.f, 0.f);
+        for (int j = 0; j < 64; ++j) {
+            const int kp = t + 64 * j;
+            if (j < 24 || j >= 40) x[j] = mk(buf[swz64(kp)]);
+            else if (j == 24) x[j] = (t == 0) ? mk(buf[swz64(kp)]) : mk(0.f, 0.f);
+            else x[j] = mk(0.f, 0.f);
         }
         group_bar(barid);
-        dft<16, 1>(xa);
+        pkx::dft<64, 1>(x);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) bufA[pad16(16 * t + j)] = xa[j];
-        if constexpr (NPI == 2) {
+        for (int j = 0; j < 64; ++j) buf[swz64(64 * t + j)] = f2(x[j]);
+        group_bar(barid);
+        // ---- inverse pass 2: radix 64, Ls = 64; twiddles w4096^{j t} = it1[j&7] * it2[j>>3]
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const int kp = t + 256 * j;
-                const bool nz = (kp <= K) || (kp >= S - K);
-                xb[j] = nz ? bufB[pad16(kp)] : make_float2(0.f, 0.f);
+        for (int j = 0; j < 64; ++j) x[j] = mk(buf[swz64(t + 64 * j)]);
+        {
+            pk a[8], b[8];
+#pragma unroll
+            for (int e = 1; e < 8; ++e) {
+                a[e] = mk(it1[e * 64 + t]);
+                b[e] = mk(it2[e * 64 + t]);
+            }
+#pragma unroll
+            for (int j = 1; j < 64; ++j) {
+                const int j1 = j & 7, j2 = j >> 3;
+                pk w;
+                if (j2 == 0) w = a[j1];
+                else if (j1 == 0) w = b[j2];
+                else w = pkx::cmul(a[j1], b[j2]);
+                x[j] = pkx::cmul(x[j], w);
             }
         }
-        group_bar(barid);
-        // I2 (Ls = 16): twiddles w256^{j k}, k = t & 15
-        const int k2 = t & 15;
-        if constexpr (NPI == 2) {
-            dft<16, 1>(xb);
+        pkx::dft<64, 1>(x);
+        // outputs p2 = t + 64 j: A -> f[4p2], f[4p2+1]; B -> f[4p2+2], f[4p2+3]
+        // (each half-warp store covers 128 contiguous bytes)
+        float2 *fo = reinterpret_cast<float2 *>(f + row * (int64_t)L);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) bufB[pad16(16 * t + j)] = xb[j];
-        }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) xa[j] = bufA[pad16(t + 256 * j)];
-        group_bar(barid);
-#pragma unroll
-        for (int j = 1; j < 16; ++j) xa[j] = cmul(xa[j], it2[j * 16 + k2]);
-        dft<16, 1>(xa);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) bufA[pad16((t - k2) * 16 + k2 + 16 * j)] = xa[j];
-        if constexpr (NPI == 2) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) xb[j] = bufB[pad16(t + 256 * j)];
-        }
-        group_bar(barid);
-        if constexpr (NPI == 2) {
-#pragma unroll
-            for (int j = 1; j < 16; ++j) xb[j] = cmul(xb[j], it2[j * 16 + k2]);
-            dft<16, 1>(xb);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) bufB[pad16((t - k2) * 16 + k2 + 16 * j)] = xb[j];
-        }
-        // I3 (Ls = 256): twiddles w4096^{j t} from the per-thread bases b1, b2, b4, b8
-        float2 tw[16];
-        tw[1] = b1; tw[2] = b2; tw[4] = b4; tw[8] = b8;
-        tw[3] = cmul(b2, b1);
-        tw[5] = cmul(b4, b1); tw[6] = cmul(b4, b2); tw[7] = cmul(b4, tw[3]);
-#pragma unroll
-        for (int j = 1; j < 8; ++j) tw[8 + j] = cmul(b8, tw[j]);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) xa[j] = bufA[pad16(t + 256 * j)];
-#pragma unroll
-        for (int j = 1; j < 16; ++j) xa[j] = cmul(xa[j], tw[j]);
-        dft<16, 1>(xa);
-        float *frow = f + row * (int64_t)L;
-        if constexpr (NPI == 2) {
-            group_bar(barid);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) xb[j] = bufB[pad16(t + 256 * j)];
-#pragma unroll
-            for (int j = 1; j < 16; ++j) xb[j] = cmul(xb[j], tw[j]);
-            dft<16, 1>(xb);
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                __stcs(reinterpret_cast<float4 *>(frow) + (t + 256 * j), make_float4(xa[j].x, xa[j].y, xb[j].x, xb[j].y));
-        } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-                __stcs(reinterpret_cast<float2 *>(frow) + (t + 256 * j), xa[j]);
-        }
+        for (int j = 0; j < 64; ++j) __stcs(fo + 2 * (t + 64 * j) + h, f2(x[j]));
     }
 }
 
 // ---------------------------------------------------------------------------------------
-template <int M, int NPI, int G>
+template <int G, bool QTAB>
 static cudaError_t row_launch_t(const RowTables &tb, int64_t rows, const float *g, float *f, cudaStream_t st) {
-    using C = RowCfg<M, 1024, 4096, NPI, G>;
-    auto kern = mci_row_kernel<M, 1024, 4096, NPI, G>;
+    using C = RowCfg<G, QTAB>;
+    auto kern = mci_row_kernel<G, QTAB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 148;
+    int dev = 0, nsm = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int64_t grid = nsm;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G * rowk::NT, C::SMEM);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + G - 1) / G;
     if (grid > need) grid = need;
     kern<<<(unsigned)grid, G * rowk::NT, C::SMEM, st>>>(g, f, rows, tb);
@@ -401,8 +372,7 @@ static cudaError_t row_launch_t(const RowTables &tb, int64_t rows, const float *
 }
 
 bool row_supported(const Axis1D &ax) {
-    return ax.dtype == MCI_F32 && !ax.analytic && ax.N == 1024 && ax.S == 4096 && ax.M == 3 &&
-           (ax.R == 2 || ax.R == 4) && ax.S > 2 * ax.K;
+    return ax.dtype == MCI_F32 && !ax.analytic && ax.M == 3 && ax.N == 1024 && ax.S == 4096 && ax.R == 4;
 }
 
 cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const void *g, void *f, cudaStream_t st,
@@ -411,16 +381,16 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     const float2 *base = (const float2 *)rowtab;
     RowTables tb;
     tb.Qt = (const float2 *)ax.Qt;
-    // layout written by mci_plan.cpp: [wp: K+1][ft2: 64][ft3: 1024][it2: 256][it3: 1024]
+    // layout written by mci_plan.cpp: [wp: K+1][fw2: 32x32][it1: 8x64][it2: 8x64]
+    tb.deriv = ax.bank_deriv012;
     tb.wp = base;
-    tb.ft2 = tb.wp + (ax.K + 1);
-    tb.ft3 = tb.ft2 + 64;
-    tb.it2 = tb.ft3 + 1024;
-    tb.it3 = tb.it2 + 256;
+    tb.fw2 = tb.wp + (ax.K + 1);
+    tb.it1 = tb.fw2 + 32 * 32;
+    tb.it2 = tb.it1 + 8 * 64;
     if (n_launches) *n_launches += 1;
     const float *gg = (const float *)g;
     float *ff = (float *)f;
-    return ax.R == 4 ? row_launch_t<3, 2, 2>(tb, rows, gg, ff, st) : row_launch_t<3, 1, 2>(tb, rows, gg, ff, st);
+    return tb.deriv ? row_launch_t<2, false>(tb, rows, gg, ff, st) : row_launch_t<2, true>(tb, rows, gg, ff, st);
 }
 
 }  // namespace mci

@@ -252,16 +252,20 @@ def test_host_execute_matches_device():
 
 
 # -------------------------------------------------------------------------- specialised row kernel
-@pytest.mark.parametrize("L,rows", [(16384, 301), (8192, 37), (16384, 1)])
-def test_row_kernel_vs_oracle_and_generic(L, rows, monkeypatch):
-    """The specialised config-2 kernel (mci_row.cu) on ragged batches (group
-    tails) and the R = 2 variant; bit-for-bit independent of batch size, and
-    within tolerance of both the oracle and the generic fused kernel."""
+@pytest.mark.parametrize("L,rows,qtab", [(16384, 301, False), (16384, 301, True), (8192, 37, False),
+                                         (16384, 1, False), (16384, 297, True)])
+def test_row_kernel_vs_oracle_and_generic(L, rows, qtab, monkeypatch):
+    """The specialised config-2 kernel (mci_row.cu; closed-form Example-2 inverse or
+    the Q table) on ragged batches (group tails); L = 8192 exercises the generic
+    kernel.  Within tolerance of the oracle and of the generic fused kernel, and
+    bit-for-bit independent of batch size."""
     m = mci()
     c = synth.CONFIGS[2]
     g = synth.cfg2_rows(np.arange(rows))
     # non-bandlimited rows too (class q* averaging on odd M)
     g[::2] = np.random.default_rng(7).standard_normal(g[::2].shape).astype(np.float32) * g[::2].std(axis=2, keepdims=True)
+    if qtab:
+        monkeypatch.setenv("MCI_ROW_QTAB", "1")
     plan = m.Plan(3, 1024, L, c["bank"])
     out = run_plan(plan, g)
     P = oracle.OraclePlan(3, 1024, L, c["bank"])
