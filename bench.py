@@ -77,6 +77,14 @@ def make_inputs(cfg, rank):
     return np.ascontiguousarray(np.tile(g, (reps, 1, 1, 1, 1)))
 
 
+def max_over_ranks(x: float, dist, device) -> float:
+    """Max of a per-rank scalar over all ranks (the step time of a weak-scaling run)."""
+    import torch
+    t = torch.tensor([x], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def make_plan(cfg):
     import paper_1802_10291_b200 as mci
     c = synth.CONFIGS[cfg]
@@ -338,9 +346,7 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dist, "cuda")
     ms_step = ms / args.steps
     total_samples = units * w["outs_per_unit"] * world
     value = total_samples / (ms_step / 1e3)
@@ -378,9 +384,7 @@ def main():
             estep()
         et = (time.perf_counter() - t0) / e_steps
         if world > 1:
-            t = torch.tensor([et], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            et = float(t.item())
+            et = max_over_ranks(et, dist, "cuda")
         e2e = {"value": total_samples / et, "unit": UNIT,
                "h2d_bytes_per_step": int(gh.numel() * esz),
                "d2h_bytes_per_step": int(oh.numel() * esz * (2 if hilbert else 1)),

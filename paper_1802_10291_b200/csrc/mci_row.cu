@@ -24,6 +24,7 @@
 //   * all complex arithmetic runs on packed FP32x2 instructions (FADD2/FFMA2/
 //     FMUL2, mci_pk.cuh): same FLOP rate as scalar FFMA, half the issue slots.
 #include <cstdint>
+#include <cstdlib>
 
 #include "mci_fft.cuh"
 #include "mci_internal.h"
@@ -95,7 +96,8 @@ template <int G, bool QTAB>
 struct RowCfg {
     static constexpr int M = 3, N = 1024, S = 4096, K = 1536, L = 16384;
     static constexpr int NQ = N / 2 + 1;
-    static constexpr int STAGE_BYTES = M * N * 4;          // 12 KB
+    static constexpr bool STAGED = G < 3;                   // TMA-staged input rows (G <= 2)
+    static constexpr int STAGE_BYTES = STAGED ? M * N * 4 : 0;  // 12 KB
     static constexpr int BUF_BYTES = S * 8;                 // 32 KB per inverse buffer
     static constexpr int GROUP_BYTES = STAGE_BYTES + 2 * BUF_BYTES + 64;  // B offset by 64 B from A
     static constexpr int Q_BYTES = QTAB ? NQ * M * M * 8 : 0;
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     const int64_t gid = (int64_t)blockIdx.x * G + grp;
     const int64_t gstride = (int64_t)gridDim.x * G;
     uint32_t phase = 0;
-    if (tid == 0 && gid < rows) {
+    if (C::STAGED && tid == 0 && gid < rows) {
         mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
         tma_load_1d(stage, g + gid * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
     }
@@ -160,8 +162,10 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
 
     for (int64_t row = gid; row < rows; row += gstride) {
         using namespace pkx;
-        mbar_wait(&mbar[grp], phase);
-        phase ^= 1;
+        if constexpr (C::STAGED) {
+            mbar_wait(&mbar[grp], phase);
+            phase ^= 1;
+        }
 
         // ---- forward: two register radix-32 passes; FFT c = fw on the channel pair
         //      (g_{2c}, g_{2c+1}); channels scaled to unit range by exact powers of two
@@ -171,8 +175,9 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             float2 *F = fwd + (c & 1) * N;
             pk x[32];
             if (fwd_warp) {  // pass 1: radix 32, Ls = 1, from the staged rows
-                const float *g0 = stage + (2 * c) * N;
-                const float *g1 = stage + (2 * c + 1) * N;
+                const float *src = C::STAGED ? stage : g + row * (int64_t)(M * N);
+                const float *g0 = src + (2 * c) * N;
+                const float *g1 = src + (2 * c + 1) * N;
                 float m0 = 0.f, m1 = 0.f;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
@@ -205,7 +210,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
                 for (int j = 0; j < 32; ++j) F[swz32(32 * i + j)] = f2(x[j]);
             }
             group_bar(barid);
-            if (tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch
+            if (C::STAGED && tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
                 tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
@@ -390,6 +395,8 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     if (n_launches) *n_launches += 1;
     const float *gg = (const float *)g;
     float *ff = (float *)f;
+    static const int groups = getenv("MCI_ROW_GROUPS") ? atoi(getenv("MCI_ROW_GROUPS")) : 2;
+    if (tb.deriv && groups == 3) return row_launch_t<3, false>(tb, rows, gg, ff, st);
     return tb.deriv ? row_launch_t<2, false>(tb, rows, gg, ff, st) : row_launch_t<2, true>(tb, rows, gg, ff, st);
 }
 
