@@ -12,7 +12,9 @@
 // butterfly are zero-padding).  In real mode two p1 share one complex FFT
 // (f_{p1a} + i f_{p1b}); in analytic mode z = f + i Hf at one p1.
 // All arithmetic in T (float or double); twiddles from fp64-rounded tables.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "mci_fft.cuh"
 #include "mci_internal.h"
@@ -259,6 +261,15 @@ static cudaError_t launch_t(const Axis1D &ax, const RowAddr &ra, int64_t rows, c
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
     if (occ < 1) occ = 1;
+    // Analytic (f + i Hf) rows write f[R p2 + p1] in partial 32-byte sectors that are
+    // completed by later p1 groups of the same row; bound the rows in flight so the
+    // partially written output (rows x 8 L bytes) stays L2-resident (126 MB).
+    if (ax.analytic) {
+        const int64_t row_bytes = 8 * ax.L;
+        const int64_t max_rows = (64ll << 20) / row_bytes;
+        if ((int64_t)nsm * occ > max_rows) occ = (int)std::max<int64_t>(1, max_rows / nsm);
+    }
+    if (const char *e = getenv("MCI_FUSED_CTAS_PER_SM")) occ = std::max(1, atoi(e));
     int64_t grid = (int64_t)nsm * occ;
     if (grid > rows) grid = rows;
     kern<<<(unsigned)grid, NT, smem, st>>>(a);

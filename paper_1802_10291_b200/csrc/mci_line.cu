@@ -1,0 +1,236 @@
+// Warp-per-line MCI kernel for short real-output lines (the 2D passes of
+// BASELINE.json configs[4]: M = 2 channels, N = 512 samples, L = 2048 outputs).
+//
+// Same mathematics as mci_fused.cu (Lemma 1 forward DFT PAPER.md:180-233,
+// per-class solve Eq. matrixeqn1, Hermitian-part assembly,
+// zero-padded inverse of Eq. DFTexpression).  One warp owns
+// one line at a time, so there are no block barriers, only __syncwarp:
+//   * forward: one complex 512-point FFT of (g0 + i g1) (channels scaled to unit
+//     range by exact powers of two), three radix-8 passes, 2 butterflies/lane;
+//   * solve: 257 classes (j_q = q - N, elements q - N and q; self-mirror
+//     classes q = 0 and N/2), Q~ from shared memory;
+//   * inverse: S = 1024 = 2K (the window [-K, K] aliases only at k' = K),
+//     R = 2: one complex FFT gives f[2 p2] + i f[2 p2 + 1]; two radix-32
+//     passes; lane i writes float2 at p2 = i + 32 j (256 contiguous bytes);
+//   * packed FP32x2 arithmetic (mci_pk.cuh), XOR-swizzled warp-private buffers.
+// Lines are addressed with RowAddr, so the same kernel serves 1D batches and
+// both passes of the separable 2D transform (strided samples).
+#include <cstdint>
+
+#include "mci_internal.h"
+#include "mci_pk.cuh"
+
+namespace mci {
+
+namespace linek {
+constexpr int N = 512, S = 1024, L = 2048, K = 512, NQ = N / 2 + 1;
+__device__ __forceinline__ int sw3(int a) { return a ^ ((a >> 3) & 15); }
+__device__ __forceinline__ int sw5(int a) { return a ^ ((a >> 5) & 15); }
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+}  // namespace linek
+
+struct LineTables {
+    const float2 *Qt;   // [NQ][2][2] H^{-1}/N per class
+    const float2 *wp;   // [K+1] e^{+2 pi i p / L}
+    const float2 *fw2;  // [8][8]   e^{-2 pi i j k / 64}
+    const float2 *fw3;  // [8][64]  e^{-2 pi i j k / 512}
+    const float2 *iw;   // [32][32] e^{+2 pi i j k / 1024}
+};
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
+                                                              int64_t lines, RowAddr ra, LineTables tb) {
+    using namespace linek;
+    using namespace pkx;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float2 *Qs = reinterpret_cast<float2 *>(smem);  // NQ*4
+    float2 *wps = Qs + NQ * 4;                      // K+1 (+1 pad)
+    float2 *fw2 = wps + K + 2;                      // 64
+    float2 *fw3 = fw2 + 64;                         // 512
+    float2 *iw = fw3 + 512;                         // 1024
+    float2 *bufs = iw + 1024;                       // WARPS x S
+    for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
+    for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
+    for (int i = threadIdx.x; i < 64; i += WARPS * 32) fw2[i] = tb.fw2[i];
+    for (int i = threadIdx.x; i < 512; i += WARPS * 32) fw3[i] = tb.fw3[i];
+    for (int i = threadIdx.x; i < 1024; i += WARPS * 32) iw[i] = tb.iw[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float2 *buf = bufs + warp * S;
+
+    for (int64_t line = (int64_t)blockIdx.x * WARPS + warp; line < lines; line += (int64_t)gridDim.x * WARPS) {
+        const int64_t base =
+            (line / (ra.D0 * ra.D1)) * ra.s2 + ((line / ra.D0) % ra.D1) * ra.s1 + (line % ra.D0) * ra.s0;
+        const float *g0 = g + base, *g1 = g + base + ra.cs;
+        __syncwarp();  // previous line's reads of buf are complete
+
+        // ---- forward pass 1 (radix 8, Ls = 1), butterflies b = lane, lane + 32
+        pk x[2][8];
+        float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t n = lane + 32 * h + 64 * j;
+                const float a = __ldg(g0 + n * ra.ss), b = __ldg(g1 + n * ra.ss);
+                m0 = fmaxf(m0, fabsf(a));
+                m1 = fmaxf(m1, fabsf(b));
+                x[h][j] = mk(a, b);
+            }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        }
+        const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
+        const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
+        const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
+        {
+            const pk sc = mk(pow2f(-e0), pow2f(-e1));
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) x[h][j] = mul(x[h][j], sc);
+                dft<8, -1>(x[h]);
+                const int b = lane + 32 * h;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) buf[sw3(8 * b + j)] = f2(x[h][j]);
+            }
+        }
+        __syncwarp();
+        // ---- pass 2 (Ls = 8)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int b = lane + 32 * h;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[h][j] = mk(buf[sw3(b + 64 * j)]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int b = lane + 32 * h, k = b & 7;
+#pragma unroll
+            for (int j = 1; j < 8; ++j) x[h][j] = pkx::cmul(x[h][j], mk(fw2[j * 8 + k]));
+            dft<8, -1>(x[h]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) buf[sw3((b - k) * 8 + k + 8 * j)] = f2(x[h][j]);
+        }
+        __syncwarp();
+        // ---- pass 3 (Ls = 64), in place on own positions
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int b = lane + 32 * h;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) x[h][j] = mk(buf[sw3(b + 64 * j)]);
+#pragma unroll
+            for (int j = 1; j < 8; ++j) x[h][j] = pkx::cmul(x[h][j], mk(fw3[j * 64 + b]));
+            dft<8, -1>(x[h]);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) buf[sw3(b + 64 * j)] = f2(x[h][j]);
+        }
+        __syncwarp();
+
+        // ---- solve: classes q = lane + 32 u (u < 8) and q = N/2 (lane 0)
+        pk zq[9], zm[9];
+#pragma unroll
+        for (int u = 0; u < 9; ++u) {
+            const int q = u < 8 ? lane + 32 * u : N / 2;
+            if (u < 8 || lane == 0) {
+                zq[u] = mk(buf[sw3(q)]);
+                zm[u] = mk(buf[sw3((N - q) & (N - 1))]);
+            }
+        }
+        __syncwarp();  // forward spectrum read: buf becomes the inverse input
+        const float h0 = 0.5f * pow2f(e0), h1 = 0.5f * pow2f(e1);
+        auto solve = [&](int u, int q, pk &v0, pk &v1) {
+            const pk G0 = mul(add(zq[u], pkx::conj(zm[u])), bc(h0));
+            const pk G1 = mul(rot<-1>(sub(zq[u], pkx::conj(zm[u]))), bc(h1));
+            const float2 *Qq = Qs + q * 4;  // [m][l]
+            v0 = add(pkx::cmul(G0, mk(Qq[0])), pkx::cmul(G1, mk(Qq[2])));
+            v1 = add(pkx::cmul(G0, mk(Qq[1])), pkx::cmul(G1, mk(Qq[3])));
+        };
+        // inverse input (p1 = 0, 1 share one FFT): Zin(k) = Y(k)(1 + i w^k), w = e^{2 pi i/L}
+        auto emit = [&](int p, pk X) {
+            const pk P = pkx::cmul(X, mk(wps[p]));
+            buf[sw5(p)] = f2(add_rot<1>(X, P));
+            buf[sw5(S - p)] = f2(add_rot<1>(pkx::conj(X), pkx::conj(P)));
+        };
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int q = lane + 32 * u;
+            pk v0, v1;
+            solve(u, q, v0, v1);
+            if (q != 0) {  // elements q - N (-> X[N - q] = conj v0) and q (-> X[q] = v1)
+                emit(N - q, pkx::conj(v0));
+                emit(q, v1);
+            } else {  // q = 0: X[0] = Re a(0); position K = N aliases +-K at k' = K
+                const float2 a0 = f2(v1);
+                buf[sw5(0)] = make_float2(a0.x, a0.x);  // X + iX, X real
+                const pk XK = mul(pkx::conj(v0), bc(0.5f));  // X[K] = conj a(-K)/2
+                const pk P = pkx::cmul(XK, mk(wps[K]));
+                buf[sw5(K)] = f2(add(add_rot<1>(XK, P), add_rot<1>(pkx::conj(XK), pkx::conj(P))));
+            }
+        }
+        if (lane == 0) {  // q = N/2: elements -N/2, N/2 -> X[N/2] = (a(N/2) + conj a(-N/2))/2
+            pk v0, v1;
+            solve(8, N / 2, v0, v1);
+            emit(N / 2, mul(add(v1, pkx::conj(v0)), bc(0.5f)));
+        }
+        __syncwarp();
+
+        // ---- inverse pass 1 (radix 32, Ls = 1)
+        pk y[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
+        __syncwarp();
+        dft<32, 1>(y);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) buf[sw5(32 * lane + j)] = f2(y[j]);
+        __syncwarp();
+        // ---- pass 2 (Ls = 32)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
+#pragma unroll
+        for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(iw[j * 32 + lane]));
+        dft<32, 1>(y);
+        float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) __stcs(fo + lane + 32 * j, f2(y[j]));
+    }
+}
+
+bool line_supported(const Axis1D &ax) {
+    return ax.dtype == MCI_F32 && !ax.analytic && ax.M == 2 && ax.N == 512 && ax.L == 2048 && ax.S == 1024;
+}
+
+size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 64 + 512 + 1024; }
+
+cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
+                        int *n_launches) {
+    if (lines <= 0) return cudaSuccess;
+    constexpr int WARPS = 8;
+    LineTables tb;
+    tb.Qt = (const float2 *)ax.Qt;
+    const float2 *base = (const float2 *)ax.rowtab;  // [wp K+1][fw2 64][fw3 512][iw 1024]
+    tb.wp = base;
+    tb.fw2 = tb.wp + (ax.K + 1);
+    tb.fw3 = tb.fw2 + 64;
+    tb.iw = tb.fw3 + 512;
+    const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 64 + 512 + 1024 + WARPS * linek::S) * 8;
+    auto kern = mci_line_kernel<WARPS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
+    if (occ < 1) occ = 1;
+    int64_t grid = (int64_t)nsm * occ;
+    const int64_t need = (lines + WARPS - 1) / WARPS;
+    if (grid > need) grid = need;
+    if (n_launches) *n_launches += 1;
+    kern<<<(unsigned)grid, WARPS * 32, smem, st>>>((const float *)g, (float *)f, lines, ra, tb);
+    return cudaGetLastError();
+}
+
+}  // namespace mci

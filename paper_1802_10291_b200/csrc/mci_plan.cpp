@@ -217,6 +217,15 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, -1);
             for (int j = 0; j < 8; ++j) push_roots(blob, 4096, 64, j, +1);
             for (int j = 0; j < 8; ++j) push_roots(blob, 4096, 64, 8 * j, +1);
+            ax.special = 1;
+        } else if (mci::line_supported(ax)) {
+            // line kernel tables: [wp: K+1][fw2: 8x8][fw3: 8x64][iw: 32x32]
+            offs.push_back(blob.size());
+            push_roots(blob, L, K + 1, 1, +1);
+            for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
+            for (int j = 0; j < 8; ++j) push_roots(blob, 512, 64, j, -1);
+            for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, +1);
+            ax.special = 2;
         }
     }
     if (fourstep) {
@@ -317,14 +326,12 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
 mci_status from_cuda(cudaError_t e) { return e == cudaSuccess ? MCI_OK : MCI_E_CUDA; }
 
 mci_status exec_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf, cudaStream_t st, int *nl) {
-    if (p->path == mci::PATH_FUSED && p->ax.rowtab)
-        return from_cuda(mci::launch_row(p->ax, p->ax.rowtab, batch, g, f, st, nl));
     if (p->path == mci::PATH_FUSED) {
         mci::RowAddr ra;
         ra.s2 = (int64_t)p->ax.M * p->ax.N;
         ra.cs = p->ax.N;
         ra.ss = 1;
-        return from_cuda(mci::launch_fused(p->ax, ra, batch, g, f, hf, st, nl));
+        return from_cuda(mci::launch_axis(p->ax, ra, batch, g, f, hf, st, nl));
     }
     return from_cuda(mci::launch_fourstep(p->ax, batch, g, f, p->ws, p->ws_units, st, nl));
 }
@@ -341,19 +348,29 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
         mci::RowAddr rc;
         rc.D0 = Nx; rc.D1 = Mx; rc.s0 = 1; rc.s1 = Ny * Nx; rc.s2 = My * Mx * Ny * Nx;
         rc.cs = Mx * Ny * Nx; rc.ss = Nx;
-        cudaError_t e = mci::launch_fused(p->ay, rc, ni * Mx * Nx, gi, p->ws, nullptr, st, nl);
+        cudaError_t e = mci::launch_axis(p->ay, rc, ni * Mx * Nx, gi, p->ws, nullptr, st, nl);
         if (e != cudaSuccess) return MCI_E_CUDA;
         // row pass (along x, channels mx) on ws -> out[img][py][Lx]
         mci::RowAddr rr;
         rr.D0 = Ly; rr.D1 = 1; rr.s0 = 1; rr.s1 = 0; rr.s2 = Mx * Nx * Ly;
         rr.cs = Nx * Ly; rr.ss = Ly;
-        e = mci::launch_fused(p->ax, rr, ni * Ly, p->ws, oi, nullptr, st, nl);
+        e = mci::launch_axis(p->ax, rr, ni * Ly, p->ws, oi, nullptr, st, nl);
         if (e != cudaSuccess) return MCI_E_CUDA;
     }
     return MCI_OK;
 }
 
 }  // namespace
+
+namespace mci {
+cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
+                        cudaStream_t st, int *nl) {
+    if (ax.special == 1 && ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N)
+        return launch_row(ax, ax.rowtab, rows, g, f, st, nl);
+    if (ax.special == 2) return launch_line(ax, ra, rows, g, f, st, nl);
+    return launch_fused(ax, ra, rows, g, f, hf, st, nl);
+}
+}  // namespace mci
 
 extern "C" {
 
