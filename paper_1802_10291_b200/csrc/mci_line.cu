@@ -37,7 +37,7 @@ struct LineTables {
     const float2 *iw;   // [32][32] e^{+2 pi i j k / 1024}
 };
 
-template <int WARPS>
+template <int WARPS, bool TILED>
 __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
                                                               int64_t lines, RowAddr ra, LineTables tb) {
     using namespace linek;
@@ -58,25 +58,60 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2 *buf = bufs + warp * S;
 
-    for (int64_t line = (int64_t)blockIdx.x * WARPS + warp; line < lines; line += (int64_t)gridDim.x * WARPS) {
+    // TILED (2D passes): WARPS consecutive lines are adjacent in memory (s0 = 1) while
+    // samples are strided; the CTA loads the tile [2][WARPS][N] with coalesced 16-byte
+    // loads (transposed on the way into shared memory, aliasing the warp buffers).
+    float *tile = reinterpret_cast<float *>(bufs);
+    const int64_t ntiles = (lines + WARPS - 1) / WARPS;
+    for (int64_t tl = blockIdx.x; tl < (TILED ? ntiles : (lines + WARPS - 1) / WARPS); tl += gridDim.x) {
+        const int64_t line = tl * WARPS + warp;
         const int64_t base =
             (line / (ra.D0 * ra.D1)) * ra.s2 + ((line / ra.D0) % ra.D1) * ra.s1 + (line % ra.D0) * ra.s0;
         const float *g0 = g + base, *g1 = g + base + ra.cs;
-        __syncwarp();  // previous line's reads of buf are complete
-
-        // ---- forward pass 1 (radix 8, Ls = 1), butterflies b = lane, lane + 32
         pk x[2][8];
         float m0 = 0.f, m1 = 0.f;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int64_t n = lane + 32 * h + 64 * j;
-                const float a = __ldg(g0 + n * ra.ss), b = __ldg(g1 + n * ra.ss);
-                m0 = fmaxf(m0, fabsf(a));
-                m1 = fmaxf(m1, fabsf(b));
-                x[h][j] = mk(a, b);
+        if constexpr (TILED) {
+            __syncthreads();  // every warp is done with its buffer (tile aliases them)
+            const int64_t l0 = tl * WARPS;
+            const int64_t tb0 = (l0 / (ra.D0 * ra.D1)) * ra.s2 + ((l0 / ra.D0) % ra.D1) * ra.s1 + (l0 % ra.D0) * ra.s0;
+            for (int idx = threadIdx.x; idx < 2 * N * (WARPS / 4); idx += WARPS * 32) {
+                const int q4 = idx % (WARPS / 4), n = (idx / (WARPS / 4)) % N, m = idx / (N * (WARPS / 4));
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(g + tb0 + m * ra.cs + (int64_t)n * ra.ss) + q4);
+                float *tr = tile + (m * WARPS + 4 * q4) * N + n;
+                tr[0] = v.x;
+                tr[N] = v.y;
+                tr[2 * N] = v.z;
+                tr[3 * N] = v.w;
             }
+            __syncthreads();
+            if (line < lines) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int n = lane + 32 * h + 64 * j;
+                        const float a = tile[warp * N + n], b = tile[(WARPS + warp) * N + n];
+                        m0 = fmaxf(m0, fabsf(a));
+                        m1 = fmaxf(m1, fabsf(b));
+                        x[h][j] = mk(a, b);
+                    }
+            }
+            __syncthreads();  // tile consumed: warp buffers are free
+            if (line >= lines) continue;
+        } else {
+            if (line >= lines) continue;
+            __syncwarp();  // previous line's reads of buf are complete
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int64_t n = lane + 32 * h + 64 * j;
+                    const float a = __ldg(g0 + n * ra.ss), b = __ldg(g1 + n * ra.ss);
+                    m0 = fmaxf(m0, fabsf(a));
+                    m1 = fmaxf(m1, fabsf(b));
+                    x[h][j] = mk(a, b);
+                }
+        }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
             m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
@@ -217,7 +252,10 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     tb.fw3 = tb.fw2 + 64;
     tb.iw = tb.fw3 + 512;
     const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 64 + 512 + 1024 + WARPS * linek::S) * 8;
-    auto kern = mci_line_kernel<WARPS>;
+    const bool tiled = ra.s0 == 1 && ra.ss != 1 && ra.D0 % WARPS == 0 &&
+                       (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 && ra.s1 % 4 == 0 &&
+                       ra.s2 % 4 == 0;
+    auto kern = tiled ? mci_line_kernel<WARPS, true> : mci_line_kernel<WARPS, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;

@@ -316,7 +316,8 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
     p->Mx = Mx; p->My = My; p->Nx = Nx; p->Ny = Ny; p->Lx = ax.L; p->Ly = ay.L;
     p->path = mci::PATH_2D;
     const size_t per = (size_t)Mx * Nx * ay.L * sizeof(T);  // column-pass intermediate per image
-    int64_t units = std::max<int64_t>(1, (int64_t)((64u << 20) / per));
+    // chunk of images whose intermediate (32 MB) stays L2-resident between the two passes
+    int64_t units = std::max<int64_t>(1, (int64_t)((32u << 20) / per));
     p->ws_units = units;
     p->ws_bytes = per * units;
     if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
