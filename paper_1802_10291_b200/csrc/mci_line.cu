@@ -6,7 +6,7 @@
 // zero-padded inverse of Eq. DFTexpression).  One warp owns
 // one line at a time, so there are no block barriers, only __syncwarp:
 //   * forward: one complex 512-point FFT of (g0 + i g1) (channels scaled to unit
-//     range by exact powers of two), three radix-8 passes, 2 butterflies/lane;
+//     range by exact powers of two), radix 16 (all lanes) then radix 32 (16 lanes);
 //   * solve: 257 classes (j_q = q - N, elements q - N and q; self-mirror
 //     classes q = 0 and N/2), Q~ from shared memory;
 //   * inverse: S = 1024 = 2K (the window [-K, K] aliases only at k' = K),
@@ -24,16 +24,17 @@ namespace mci {
 
 namespace linek {
 constexpr int N = 512, S = 1024, L = 2048, K = 512, NQ = N / 2 + 1;
-__device__ __forceinline__ int sw3(int a) { return a ^ ((a >> 3) & 15); }
-__device__ __forceinline__ int sw5(int a) { return a ^ ((a >> 5) & 15); }
+// paddings (conflict-free for the access strides used, constant offsets per index)
+__device__ __forceinline__ int sw3(int a) { return a + (a >> 4); }  // forward 512 -> 544
+__device__ __forceinline__ int sw5(int a) { return a + (a >> 5); }  // inverse 1024 -> 1056
+constexpr int BUF = S + S / 32;
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 }  // namespace linek
 
 struct LineTables {
     const float2 *Qt;   // [NQ][2][2] H^{-1}/N per class
     const float2 *wp;   // [K+1] e^{+2 pi i p / L}
-    const float2 *fw2;  // [8][8]   e^{-2 pi i j k / 64}
-    const float2 *fw3;  // [8][64]  e^{-2 pi i j k / 512}
+    const float2 *fwt;  // [32][16] e^{-2 pi i j k / 512}
     const float2 *iw;   // [32][32] e^{+2 pi i j k / 1024}
 };
 
@@ -45,18 +46,16 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
     extern __shared__ __align__(16) unsigned char smem[];
     float2 *Qs = reinterpret_cast<float2 *>(smem);  // NQ*4
     float2 *wps = Qs + NQ * 4;                      // K+1 (+1 pad)
-    float2 *fw2 = wps + K + 2;                      // 64
-    float2 *fw3 = fw2 + 64;                         // 512
-    float2 *iw = fw3 + 512;                         // 1024
-    float2 *bufs = iw + 1024;                       // WARPS x S
+    float2 *fwt = wps + K + 2;                      // 512
+    float2 *iw = fwt + 512;                         // 1024
+    float2 *bufs = iw + 1024;                       // WARPS x BUF
     for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
     for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
-    for (int i = threadIdx.x; i < 64; i += WARPS * 32) fw2[i] = tb.fw2[i];
-    for (int i = threadIdx.x; i < 512; i += WARPS * 32) fw3[i] = tb.fw3[i];
+    for (int i = threadIdx.x; i < 512; i += WARPS * 32) fwt[i] = tb.fwt[i];
     for (int i = threadIdx.x; i < 1024; i += WARPS * 32) iw[i] = tb.iw[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float2 *buf = bufs + warp * S;
+    float2 *buf = bufs + warp * BUF;
 
     // TILED (2D passes): WARPS consecutive lines are adjacent in memory (s0 = 1) while
     // samples are strided; the CTA loads the tile [2][WARPS][N] with coalesced 16-byte
@@ -68,7 +67,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
         const int64_t base =
             (line / (ra.D0 * ra.D1)) * ra.s2 + ((line / ra.D0) % ra.D1) * ra.s1 + (line % ra.D0) * ra.s0;
         const float *g0 = g + base, *g1 = g + base + ra.cs;
-        pk x[2][8];
+        pk x[16];
         float m0 = 0.f, m1 = 0.f;
         if constexpr (TILED) {
             __syncthreads();  // every warp is done with its buffer (tile aliases them)
@@ -86,15 +85,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
             __syncthreads();
             if (line < lines) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int n = lane + 32 * h + 64 * j;
-                        const float a = tile[warp * N + n], b = tile[(WARPS + warp) * N + n];
-                        m0 = fmaxf(m0, fabsf(a));
-                        m1 = fmaxf(m1, fabsf(b));
-                        x[h][j] = mk(a, b);
-                    }
+                for (int j = 0; j < 16; ++j) {
+                    const int n = lane + 32 * j;
+                    const float a = tile[warp * N + n], b = tile[(WARPS + warp) * N + n];
+                    m0 = fmaxf(m0, fabsf(a));
+                    m1 = fmaxf(m1, fabsf(b));
+                    x[j] = mk(a, b);
+                }
             }
             __syncthreads();  // tile consumed: warp buffers are free
             if (line >= lines) continue;
@@ -102,15 +99,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
             if (line >= lines) continue;
             __syncwarp();  // previous line's reads of buf are complete
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int64_t n = lane + 32 * h + 64 * j;
-                    const float a = __ldg(g0 + n * ra.ss), b = __ldg(g1 + n * ra.ss);
-                    m0 = fmaxf(m0, fabsf(a));
-                    m1 = fmaxf(m1, fabsf(b));
-                    x[h][j] = mk(a, b);
-                }
+            for (int j = 0; j < 16; ++j) {
+                const int64_t n = lane + 32 * j;
+                const float a = __ldg(g0 + n * ra.ss), b = __ldg(g1 + n * ra.ss);
+                m0 = fmaxf(m0, fabsf(a));
+                m1 = fmaxf(m1, fabsf(b));
+                x[j] = mk(a, b);
+            }
         }
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
@@ -120,48 +115,24 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
         const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
         const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
         const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
-        {
+        {  // ---- forward pass 1 (radix 16, Ls = 1): butterfly i = lane, inputs n = i + 32 j
             const pk sc = mk(pow2f(-e0), pow2f(-e1));
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int j = 0; j < 16; ++j) x[j] = mul(x[j], sc);
+            dft<16, -1>(x);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) x[h][j] = mul(x[h][j], sc);
-                dft<8, -1>(x[h]);
-                const int b = lane + 32 * h;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) buf[sw3(8 * b + j)] = f2(x[h][j]);
-            }
+            for (int j = 0; j < 16; ++j) buf[sw3(16 * lane + j)] = f2(x[j]);
         }
         __syncwarp();
-        // ---- pass 2 (Ls = 8)
+        pk y[32];
+        if (lane < 16) {  // ---- pass 2 (radix 32, Ls = 16): butterfly i = lane < 16, in place
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int b = lane + 32 * h;
+            for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw3(lane + 16 * j)]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) x[h][j] = mk(buf[sw3(b + 64 * j)]);
-        }
-        __syncwarp();
+            for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(fwt[j * 16 + lane]));
+            dft<32, -1>(y);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int b = lane + 32 * h, k = b & 7;
-#pragma unroll
-            for (int j = 1; j < 8; ++j) x[h][j] = pkx::cmul(x[h][j], mk(fw2[j * 8 + k]));
-            dft<8, -1>(x[h]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) buf[sw3((b - k) * 8 + k + 8 * j)] = f2(x[h][j]);
-        }
-        __syncwarp();
-        // ---- pass 3 (Ls = 64), in place on own positions
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int b = lane + 32 * h;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) x[h][j] = mk(buf[sw3(b + 64 * j)]);
-#pragma unroll
-            for (int j = 1; j < 8; ++j) x[h][j] = pkx::cmul(x[h][j], mk(fw3[j * 64 + b]));
-            dft<8, -1>(x[h]);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) buf[sw3(b + 64 * j)] = f2(x[h][j]);
+            for (int j = 0; j < 32; ++j) buf[sw3(lane + 16 * j)] = f2(y[j]);
         }
         __syncwarp();
 
@@ -214,7 +185,6 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
         __syncwarp();
 
         // ---- inverse pass 1 (radix 32, Ls = 1)
-        pk y[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
         __syncwarp();
@@ -238,7 +208,7 @@ bool line_supported(const Axis1D &ax) {
     return ax.dtype == MCI_F32 && !ax.analytic && ax.M == 2 && ax.N == 512 && ax.L == 2048 && ax.S == 1024;
 }
 
-size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 64 + 512 + 1024; }
+size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 512 + 1024; }
 
 cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
                         int *n_launches) {
@@ -246,12 +216,11 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     constexpr int WARPS = 8;
     LineTables tb;
     tb.Qt = (const float2 *)ax.Qt;
-    const float2 *base = (const float2 *)ax.rowtab;  // [wp K+1][fw2 64][fw3 512][iw 1024]
+    const float2 *base = (const float2 *)ax.rowtab;  // [wp K+1][fwt 32x16][iw 32x32]
     tb.wp = base;
-    tb.fw2 = tb.wp + (ax.K + 1);
-    tb.fw3 = tb.fw2 + 64;
-    tb.iw = tb.fw3 + 512;
-    const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 64 + 512 + 1024 + WARPS * linek::S) * 8;
+    tb.fwt = tb.wp + (ax.K + 1);
+    tb.iw = tb.fwt + 512;
+    const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8;
     const bool tiled = ra.s0 == 1 && ra.ss != 1 && ra.D0 % WARPS == 0 &&
                        (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 && ra.s1 % 4 == 0 &&
                        ra.s2 % 4 == 0;

@@ -219,11 +219,10 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             for (int j = 0; j < 8; ++j) push_roots(blob, 4096, 64, 8 * j, +1);
             ax.special = 1;
         } else if (mci::line_supported(ax)) {
-            // line kernel tables: [wp: K+1][fw2: 8x8][fw3: 8x64][iw: 32x32]
+            // line kernel tables: [wp: K+1][fwt: 32x16][iw: 32x32]
             offs.push_back(blob.size());
             push_roots(blob, L, K + 1, 1, +1);
-            for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
-            for (int j = 0; j < 8; ++j) push_roots(blob, 512, 64, j, -1);
+            for (int j = 0; j < 32; ++j) push_roots(blob, 512, 16, j, -1);
             for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, +1);
             ax.special = 2;
         }

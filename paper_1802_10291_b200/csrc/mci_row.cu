@@ -72,10 +72,11 @@ __device__ __forceinline__ void tma_store_wait_read() {
 }
 __device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(NT) : "memory"); }
 
-// swizzles (8-byte elements; bank pair = low 4 bits): conflict-free for contiguous
-// runs and for the radix-R transposed stores (stride R)
-__device__ __forceinline__ int swz32(int a) { return a ^ ((a >> 5) & 15); }
-__device__ __forceinline__ int swz64(int a) { return a ^ ((a >> 6) & 15); }
+// paddings (8-byte elements; bank pair = low 4 bits): conflict-free for contiguous
+// runs and for the radix-R transposed stores (stride R), and -- unlike XOR
+// swizzles -- a constant offset per unrolled index, so no address arithmetic
+__device__ __forceinline__ int swz32(int a) { return a + (a >> 5); }  // forward, 1024 -> 1056
+__device__ __forceinline__ int swz64(int a) { return a + (a >> 6); }  // inverse, 4096 -> 4160
 
 // 2^e as an exact float (|e| <= 100)
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
@@ -98,8 +99,9 @@ struct RowCfg {
     static constexpr int NQ = N / 2 + 1;
     static constexpr bool STAGED = G < 3;                   // TMA-staged input rows (G <= 2)
     static constexpr int STAGE_BYTES = STAGED ? M * N * 4 : 0;  // 12 KB
-    static constexpr int BUF_BYTES = S * 8;                 // 32 KB per inverse buffer
-    static constexpr int GROUP_BYTES = STAGE_BYTES + 2 * BUF_BYTES + 64;  // B offset by 64 B from A
+    static constexpr int BUF_ELEMS = S + S / 64;             // padded inverse buffer (4160)
+    static constexpr int FWD_ELEMS = N + N / 32;             // padded forward buffer (1056)
+    static constexpr int GROUP_BYTES = STAGE_BYTES + (2 * BUF_ELEMS + 8) * 8;  // B offset by 8 elements
     static constexpr int Q_BYTES = QTAB ? NQ * M * M * 8 : 0;
     static constexpr int TAB_BYTES = (32 * 32 + 2 * 8 * 64 + K + 2) * 8;
     static constexpr int SMEM = G * GROUP_BYTES + Q_BYTES + TAB_BYTES;
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     unsigned char *gbase = smem + grp * C::GROUP_BYTES;
     float *stage = reinterpret_cast<float *>(gbase);
     float2 *bufA = reinterpret_cast<float2 *>(gbase + C::STAGE_BYTES);
-    float2 *bufB = bufA + S + 8;  // +64 B: A and B lanes of a half-warp hit different banks
+    float2 *bufB = bufA + C::BUF_ELEMS + 8;  // +8 elements: A and B lanes of a half-warp hit different banks
     float2 *fwd = bufB;  // forward spectra (2 x 1024) alias buffer B
     float2 *Qs = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES);
     float2 *fw2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
         //      (avoids cross-channel rounding leakage when |f''| >> |f|)
         {
             const int c = fw, i = lane;
-            float2 *F = fwd + (c & 1) * N;
+            float2 *F = fwd + (c & 1) * C::FWD_ELEMS;
             pk x[32];
             if (fwd_warp) {  // pass 1: radix 32, Ls = 1, from the staged rows
                 const float *src = C::STAGED ? stage : g + row * (int64_t)(M * N);
@@ -238,8 +240,8 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             if (u < 4 || tid == 0) {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    zq[u][c] = mk(fwd[c * N + swz32(q)]);
-                    zm[u][c] = mk(fwd[c * N + swz32(qm)]);
+                    zq[u][c] = mk(fwd[c * C::FWD_ELEMS + swz32(q)]);
+                    zm[u][c] = mk(fwd[c * C::FWD_ELEMS + swz32(qm)]);
                 }
             }
         }
