@@ -11,7 +11,7 @@
 //     prefetched while the current one is transformed;
 //   * forward: two complex 1024-point FFTs (channel pairs (g0,g1), (g2,0)) as
 //     two register radix-32 passes (one shared-memory exchange);
-//   * per-class solve: Q from a shared table, or -- for the (f, f', f'') bank --
+//   * per-class solve: Q~ from the plan's table (through L1), or -- for the (f, f', f'') bank --
 //     the paper's closed-form inverse of Example 2, exact in
 //     fp32 (integer numerators over powers of two);
 //   * the solve writes the pre-twiddled inputs of the two inverse FFTs
@@ -88,8 +88,7 @@ struct RowTables {
     const float2 *Qt;   // [(N/2+1)][M][M]  H^{-1}/N per class (table mode)
     const float2 *wp;   // [K+1]      e^{+2 pi i p / L}
     const float2 *fw2;  // [32][32]   e^{-2 pi i j k / 1024}     (forward pass 2)
-    const float2 *it1;  // [8][64]    e^{+2 pi i j1 t / 4096}    (inverse pass 2, j1 = 0..7)
-    const float2 *it2;  // [8][64]    e^{+2 pi i 8 j2 t / 4096}  (j2 = 0..7)
+    const float2 *itw;  // [64][64]   e^{+2 pi i j t / 4096}     (inverse pass 2)
     int deriv;          // 1: bank is (1, ik, -k^2) -> closed-form Q (Example 2)
 };
 
@@ -102,8 +101,8 @@ struct RowCfg {
     static constexpr int BUF_ELEMS = S + S / 64;             // padded inverse buffer (4160)
     static constexpr int FWD_ELEMS = N + N / 32;             // padded forward buffer (1056)
     static constexpr int GROUP_BYTES = STAGE_BYTES + (2 * BUF_ELEMS + 8) * 8;  // B offset by 8 elements
-    static constexpr int Q_BYTES = QTAB ? NQ * M * M * 8 : 0;
-    static constexpr int TAB_BYTES = (32 * 32 + 2 * 8 * 64 + K + 2) * 8;
+    static constexpr int Q_BYTES = 0;  // table-mode Q~ is read through L1 (__ldg)
+    static constexpr int TAB_BYTES = (32 * 32 + 64 * 64 + K + 2) * 8;
     static constexpr int SMEM = G * GROUP_BYTES + Q_BYTES + TAB_BYTES;
 };
 
@@ -126,20 +125,13 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     float2 *bufA = reinterpret_cast<float2 *>(gbase + C::STAGE_BYTES);
     float2 *bufB = bufA + C::BUF_ELEMS + 8;  // +8 elements: A and B lanes of a half-warp hit different banks
     float2 *fwd = bufB;  // forward spectra (2 x 1024) alias buffer B
-    float2 *Qs = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES);
     float2 *fw2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
-    float2 *it1 = fw2 + 32 * 32;
-    float2 *it2 = it1 + 8 * 64;
-    float2 *wps = it2 + 8 * 64;  // e^{+2 pi i p / L}, p = 0..K
+    float2 *itw = fw2 + 32 * 32;  // [64][64] e^{+2 pi i j t / 4096}
+    float2 *wps = itw + 64 * 64;  // e^{+2 pi i p / L}, p = 0..K
 
     // ---- one-time setup
-    if constexpr (QTAB)
-        for (int i = threadIdx.x; i < C::NQ * M * M; i += G * NT) Qs[i] = tb.Qt[i];
     for (int i = threadIdx.x; i < 32 * 32; i += G * NT) fw2[i] = tb.fw2[i];
-    for (int i = threadIdx.x; i < 8 * 64; i += G * NT) {
-        it1[i] = tb.it1[i];
-        it2[i] = tb.it2[i];
-    }
+    for (int i = threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
     for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
     if (tid == 0) mbar_init(&mbar[grp], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -268,12 +260,12 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             const pk g1 = pkx::mul(rot<-1>(sub(zqu[0], pkx::conj(zmu[0]))), bc(hs[1]));
             const pk g2 = pkx::mul(add(zqu[1], pkx::conj(zmu[1])), bc(hs[2]));
             if constexpr (QTAB) {
-                const float2 *Qq = Qs + q * 9;
+                const float2 *Qq = tb.Qt + q * 9;
 #pragma unroll
                 for (int l = 0; l < 3; ++l) {
-                    pk acc = pkx::cmul(g0, mk(Qq[l]));
-                    acc = add(acc, pkx::cmul(g1, mk(Qq[3 + l])));
-                    v[l] = add(acc, pkx::cmul(g2, mk(Qq[6 + l])));
+                    pk acc = pkx::cmul(g0, mk(__ldg(Qq + l)));
+                    acc = add(acc, pkx::cmul(g1, mk(__ldg(Qq + 3 + l))));
+                    v[l] = add(acc, pkx::cmul(g2, mk(__ldg(Qq + 6 + l))));
                 }
             } else {
                 // Example 2, paper's L = N, n = j_q; divided by N (d = G/N).
@@ -333,23 +325,8 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
         // ---- inverse pass 2: radix 64, Ls = 64; twiddles w4096^{j t} = it1[j&7] * it2[j>>3]
 #pragma unroll
         for (int j = 0; j < 64; ++j) x[j] = mk(buf[swz64(t + 64 * j)]);
-        {
-            pk a[8], b[8];
 #pragma unroll
-            for (int e = 1; e < 8; ++e) {
-                a[e] = mk(it1[e * 64 + t]);
-                b[e] = mk(it2[e * 64 + t]);
-            }
-#pragma unroll
-            for (int j = 1; j < 64; ++j) {
-                const int j1 = j & 7, j2 = j >> 3;
-                pk w;
-                if (j2 == 0) w = a[j1];
-                else if (j1 == 0) w = b[j2];
-                else w = pkx::cmul(a[j1], b[j2]);
-                x[j] = pkx::cmul(x[j], w);
-            }
-        }
+        for (int j = 1; j < 64; ++j) x[j] = pkx::cmul(x[j], mk(itw[j * 64 + t]));
         pkx::dft<64, 1>(x);
         // outputs p2 = t + 64 j: A -> f[4p2], f[4p2+1]; B -> f[4p2+2], f[4p2+3]
         // (each half-warp store covers 128 contiguous bytes)
@@ -388,12 +365,11 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     const float2 *base = (const float2 *)rowtab;
     RowTables tb;
     tb.Qt = (const float2 *)ax.Qt;
-    // layout written by mci_plan.cpp: [wp: K+1][fw2: 32x32][it1: 8x64][it2: 8x64]
+    // layout written by mci_plan.cpp: [wp: K+1][fw2: 32x32][itw: 64x64]
     tb.deriv = ax.bank_deriv012;
     tb.wp = base;
     tb.fw2 = tb.wp + (ax.K + 1);
-    tb.it1 = tb.fw2 + 32 * 32;
-    tb.it2 = tb.it1 + 8 * 64;
+    tb.itw = tb.fw2 + 32 * 32;
     if (n_launches) *n_launches += 1;
     const float *gg = (const float *)g;
     float *ff = (float *)f;
