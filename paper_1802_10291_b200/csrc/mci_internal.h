@@ -26,7 +26,7 @@ struct Axis1D {
     int64_t LO = 0;
     const void *rowtab = nullptr;  // tables of the specialised row kernel (mci_row.cu), or null
     int bank_deriv012 = 0;         // bank is exactly (1, ik, -k^2): closed-form inverse available
-    int special = 0;               // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu)
+    int special = 0;  // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu), 3 Hilbert (mci_hilbert.cu)
 };
 
 enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2 };
@@ -46,6 +46,9 @@ bool fused_supported(const Axis1D &ax);
 
 bool row_supported(const Axis1D &ax);
 bool line_supported(const Axis1D &ax);
+bool hilbert_supported(const Axis1D &ax);
+cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *f, void *hf, cudaStream_t st,
+                           int *n_launches);
 cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
                         int *n_launches);
 // dispatch a fused-path axis to its kernel (specialised when available)

@@ -224,6 +224,13 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             for (int j = 0; j < 32; ++j) push_roots(blob, 512, 16, j, -1);
             for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, +1);
             ax.special = 2;
+        } else if (mci::hilbert_supported(ax)) {
+            // Hilbert kernel tables: [whi: 256][wlo: 256][itw: 64x64]
+            offs.push_back(blob.size());
+            push_roots(blob, L, 256, 256, +1);
+            push_roots(blob, L, 256, 1, +1);
+            for (int j = 0; j < 64; ++j) push_roots(blob, 4096, 64, j, +1);
+            ax.special = 3;
         }
     }
     if (fourstep) {
@@ -367,6 +374,8 @@ cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const
     if (ax.special == 1 && ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N)
         return launch_row(ax, ax.rowtab, rows, g, f, st, nl);
     if (ax.special == 2) return launch_line(ax, ra, rows, g, f, st, nl);
+    if (ax.special == 3 && ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N)
+        return launch_hilbert(ax, rows, g, f, hf, st, nl);
     return launch_fused(ax, ra, rows, g, f, hf, st, nl);
 }
 }  // namespace mci
