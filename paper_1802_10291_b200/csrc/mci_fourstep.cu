@@ -18,52 +18,12 @@
 // FFT index k' = k mod S share k mod N1, so one FB CTA owns everything a
 // residue pair needs (including the mirror classes for real-signal unpacking).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
-#include "mci_fft.cuh"
-#include "mci_internal.h"
+#include "mci_fourstep.cuh"
 
 namespace mci {
-
-static constexpr int N1 = 1024;  // shared residue modulus / step-1 length
-
-template <typename T> struct Tw2 {
-    const cv<T> *hi, *lo;
-    int lob;
-    int64_t mask;  // size - 1
-    __device__ __forceinline__ cv<T> operator()(int64_t m) const {
-        m &= mask;
-        return cmul(__ldg(hi + (m >> lob)), __ldg(lo + (m & ((1 << lob) - 1))));
-    }
-};
-
-template <typename T> struct FSArgs {
-    int M, npair, npi;
-    int64_t N, N2, S, S2, L, K, R;
-    const T *g;
-    T *f;
-    cv<T> *Tw;  // workspace T   [sig][npair][N1][N2]
-    cv<T> *Uw;  // workspace U   [sig][npi][N1][S2]
-    const cv<T> *Qt;
-    const cv<T> *twF;  // e^{-2 pi i m/TW} (TW >= max(N1, N2, S2))
-    int64_t TW;
-    Tw2<T> twN;  // e^{-2 pi i m/N}
-    Tw2<T> twS;  // e^{+2 pi i m/S}
-    Tw2<T> twL;  // e^{+2 pi i m/L}
-    int64_t sig0;  // first signal of this chunk (input/output offset)
-    typename std::conditional<sizeof(T) == 4, unsigned, unsigned long long>::type *cmax;  // [sig][M] |g| max bits
-};
-
-// exponent e with max|g_m| = f 2^e, f in [0.5, 1) (0 for an all-zero channel)
-template <typename T> __device__ __forceinline__ int chan_exp(const FSArgs<T> &a, int64_t sl, int m) {
-    if (m >= a.M) return 0;
-    T mx;
-    if constexpr (sizeof(T) == 4) mx = __uint_as_float(a.cmax[sl * a.M + m]);
-    else mx = __longlong_as_double((long long)a.cmax[sl * a.M + m]);
-    int e = 0;
-    if (mx > 0) frexp(mx, &e);
-    return e;
-}
 
 // ---- channel magnitude pre-pass (exact power-of-two scaling before channel packing) ----------
 static constexpr int MX_NT = 256, MX_BLK = 16;
@@ -331,11 +291,19 @@ static cudaError_t fs_launch_t(const Axis1D &ax, int64_t batch, const void *g, v
     if ((e = cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fs_fb<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fs_ic<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ic_sm))) return e;
+    const bool fast = fourstep_fast_ok(ax) && !getenv("MCI_FOURSTEP_GENERIC");
     for (int64_t s0 = 0; s0 < batch; s0 += ws_sig) {
         const int64_t ns = (batch - s0 < ws_sig) ? batch - s0 : ws_sig;
         a.sig0 = s0;
         if ((e = cudaMemsetAsync(a.cmax, 0, sizeof(*a.cmax) * ns * a.M, st))) return e;
         mci_fs_max<T><<<(unsigned)(ns * a.M * MX_BLK), MX_NT, 0, st>>>(a);
+        if constexpr (std::is_same<T, float>::value) {
+            if (fast) {
+                if ((e = fourstep_fast_chunk(a, ns, st))) return e;
+                if (nl) *nl += 4;
+                continue;
+            }
+        }
         fa<<<(unsigned)(ns * a.npair * (a.N2 / tn2)), FA_NT, fa_sm, st>>>(a);
         mci_fs_fb<T><<<(unsigned)(ns * (N1 / 2 + 1)), FB_NT, fb_sm, st>>>(a);
         mci_fs_ic<T><<<(unsigned)(ns * (a.S2 / IC_TU)), IC_NT, ic_sm, st>>>(a);

@@ -1,0 +1,296 @@
+// Packed-FP32x2 four-step kernels for the config-4 shape (N = N1 * N2 with
+// N1 = 1024, N2 = 256; S = N1 * S2 with S2 = 1024; M in {3, 4}; R = 4).
+// Same decomposition and workspace layout as mci_fourstep.cu (FA / FB / IC;
+// see the header comment there), with register radix-32 / radix-16 two-pass
+// FFTs (packed complex arithmetic, mci_pk.cuh), padded shared buffers and
+// coalesced 32-64 byte global runs.  Selected by launch_fourstep when the
+// shape matches; the generic kernels remain the fallback.
+#include "mci_fourstep.cuh"
+#include "mci_pk.cuh"
+
+namespace mci {
+
+namespace fsf {
+constexpr int N2 = 256, S2 = 1024;  // N1 = 1024 from mci_fourstep.cuh
+__device__ __forceinline__ int pad5(int a) { return a + (a >> 5); }
+__device__ __forceinline__ int pad4(int a) { return a + (a >> 4); }
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+}  // namespace fsf
+
+using pkx::pk;
+
+// ---- FA: 8 FFTs of length N1 over n1 for 8 consecutive residues n2 -------------------------
+// lane = 8 il + t2: FFT t2 (n2 = tile*8 + t2), butterfly i = 4 warp + il
+__global__ void __launch_bounds__(256) mci_fsf_fa(const FSArgs<float> a) {
+    using namespace fsf;
+    using namespace pkx;
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int BS = 1056 + 2;  // per-FFT stride (== 2 mod 16: conflict-free)
+    float2 *bufs = reinterpret_cast<float2 *>(smem);
+    float2 *tw = bufs + 8 * BS;  // [32][32] e^{-2 pi i j i / 1024}
+    for (int q = threadIdx.x; q < 1024; q += 256) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    __syncthreads();
+    const int ntiles = N2 / 8;
+    const int tile = blockIdx.x % ntiles;
+    const int c = (blockIdx.x / ntiles) % a.npair;
+    const int64_t sl = blockIdx.x / ((int64_t)ntiles * a.npair);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t2 = lane & 7, i = 4 * warp + (lane >> 3);
+    const int n2 = tile * 8 + t2;
+    const float *g0 = a.g + (a.sig0 + sl) * (int64_t)a.M * a.N + (int64_t)(2 * c) * a.N;
+    const float *g1 = g0 + a.N;
+    const bool has1 = 2 * c + 1 < a.M;
+    const pk sc = mk(pow2f(-chan_exp(a, sl, 2 * c)), pow2f(-chan_exp(a, sl, 2 * c + 1)));
+    float2 *buf = bufs + t2 * BS;
+    pk x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int64_t n = (int64_t)(i + 32 * j) * N2 + n2;
+        x[j] = mul(mk(__ldg(g0 + n), has1 ? __ldg(g1 + n) : 0.f), sc);
+    }
+    dft<32, -1>(x);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) buf[pad5(32 * i + j)] = f2(x[j]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
+#pragma unroll
+    for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], mk(tw[j * 32 + i]));
+    dft<32, -1>(x);
+    float2 *out = reinterpret_cast<float2 *>(a.Tw + (sl * a.npair + c) * (int64_t)N1 * N2);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int q1 = i + 32 * j;
+        out[(int64_t)q1 * N2 + n2] = f2(pkx::cmul(x[j], mk(a.twN((int64_t)n2 * q1))));
+    }
+}
+
+// ---- FB: forward step 2 + solve + assembly + inverse step 1 for the residue pair --------------
+__global__ void __launch_bounds__(256) mci_fsf_fb(const FSArgs<float> a) {
+    using namespace fsf;
+    using namespace pkx;
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int GB = 272 + 1;   // forward buffer stride (4 FFTs of 256, pad4)
+    constexpr int IB = 1056 + 4;  // inverse buffer stride (4 FFTs of 1024, pad5); == 4 mod 16
+    const int64_t xl = a.K / N1 + 2;
+    float2 *fb = reinterpret_cast<float2 *>(smem);  // 4 x GB
+    float2 *G = fb + 4 * GB;                         // [4][256] natural order
+    float2 *Xl = G + 4 * 256;                        // [2][xl]
+    float2 *ib = Xl + 2 * xl;                        // 4 x IB
+    float2 *tw16 = ib + 4 * IB;                      // [16][16] e^{-2 pi i j b/256}
+    float2 *tw32 = tw16 + 256;                       // [32][32] e^{-2 pi i j i/1024}
+    for (int q = threadIdx.x; q < 256; q += 256) tw16[q] = __ldg(a.twF + ((4 * (q >> 4) * (q & 15)) & 1023));
+    for (int q = threadIdx.x; q < 1024; q += 256) tw32[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    const int q1 = blockIdx.x % (N1 / 2 + 1);
+    const int64_t sl = blockIdx.x / (N1 / 2 + 1);
+    const int nres = (q1 == 0 || q1 == N1 / 2) ? 1 : 2;
+    const int res[2] = {q1, N1 - q1};
+    const int64_t N = a.N, K = a.K;
+    const int M = a.M, npair = a.npair, tid = threadIdx.x;
+    __syncthreads();
+    // -- A: 4 forward FFTs of length 256 (residue r, pair c): radix 16 x 16 on 64 threads
+    if (tid < 64) {
+        const int fi = tid >> 4, b = tid & 15, r = fi >> 1, c = fi & 1;
+        if (r < nres) {
+            const float2 *trow = reinterpret_cast<const float2 *>(a.Tw) + ((sl * npair + c) * N1 + res[r]) * (int64_t)N2;
+            float2 *buf = fb + fi * GB;
+            pk x[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = mk(trow[b + 16 * j]);
+            dft<16, -1>(x);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) buf[pad4(16 * b + j)] = f2(x[j]);
+            __syncwarp();
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = mk(buf[pad4(b + 16 * j)]);
+#pragma unroll
+            for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(tw16[j * 16 + b]));
+            dft<16, -1>(x);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) G[fi * 256 + b + 16 * j] = f2(x[j]);
+        } else {
+            asm volatile("bar.sync 1, 64;" ::: "memory");
+        }
+    }
+    __syncthreads();
+    // -- B: solve classes q = res_r + N1 q2 <= N/2 and assemble X at p = +-res mod N1
+    float sup[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) sup[m] = 0.5f * pow2f(chan_exp(a, sl, m));
+    for (int idx = tid; idx < nres * N2; idx += 256) {
+        const int r = idx / N2, q2 = idx % N2;
+        const int64_t q = res[r] + (int64_t)N1 * q2;
+        if (q > N / 2) continue;
+        const int rm = (nres == 1) ? 0 : 1 - r;
+        const int q2m = (res[r] == 0) ? ((N2 - q2) % N2) : (N2 - 1 - q2);
+        const int64_t jq = -K + (((q + K) % N) + N) % N;
+        pk gm[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            if (m < M) {
+                const int c = m >> 1;
+                const pk zc = mk(G[(r * 2 + c) * 256 + q2]), zm = pkx::conj(mk(G[(rm * 2 + c) * 256 + q2m]));
+                gm[m] = (m & 1) ? mul(rot<-1>(sub(zc, zm)), bc(sup[m])) : mul(add(zc, zm), bc(sup[m]));
+            } else {
+                gm[m] = mk(0.f, 0.f);
+            }
+        }
+        pk v[4];
+        const float2 *Qq = reinterpret_cast<const float2 *>(a.Qt) + q * M * M;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            pk acc = mk(0.f, 0.f);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+                if (m < M && l < M) acc = add(acc, pkx::cmul(gm[m], mk(__ldg(Qq + m * M + l))));
+            v[l] = acc;
+        }
+        const bool selfm = (q == 0) || (2 * q == N);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            if (l >= M) break;
+            const int64_t k = jq + (int64_t)l * N;
+            int64_t p = -1;
+            float2 val;
+            if (!selfm) {
+                p = k > 0 ? k : -k;
+                val = k > 0 ? f2(v[l]) : f2(pkx::conj(v[l]));
+            } else {
+                const int64_t lm = -k - jq;
+                const bool neg_in = (lm >= 0) && (lm % N == 0) && (lm / N < M);
+                if (k >= 0 || !neg_in) {
+                    p = k >= 0 ? k : -k;
+                    pk ap = mk(0.f, 0.f), an = mk(0.f, 0.f);
+                    const int64_t lp = p - jq, ln = -p - jq;
+#pragma unroll
+                    for (int l2 = 0; l2 < 4; ++l2) {
+                        if (l2 < M && lp == (int64_t)l2 * N) ap = v[l2];
+                        if (l2 < M && ln == (int64_t)l2 * N) an = v[l2];
+                    }
+                    val = f2(mul(add(ap, pkx::conj(an)), bc(0.5f)));
+                }
+            }
+            if (p >= 0) Xl[((int)(p % N1) == res[0] ? 0 : 1) * xl + p / N1] = val;
+        }
+    }
+    __syncthreads();
+    // -- C: inverse step 1, 4 FFTs (residue r, pair ip) of length S2 over k1: radix 32 x 32 on 128 threads
+    if (tid < 128) {
+        const int fi = tid >> 5, i = tid & 31, r = fi >> 1, ip = fi & 1;
+        float2 *buf = ib + fi * IB;
+        const bool act = r < nres;
+        pk x[32];
+        if (act) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int64_t kp = res[r] + (int64_t)N1 * (i + 32 * j);
+                pk acc = mk(0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < 2; ++w) {
+                    const int64_t k = w == 0 ? kp : kp - a.S;
+                    if (k > K || k < -K) continue;
+                    const int64_t ak = k >= 0 ? k : -k;
+                    const int slot = ((int)(ak % N1) == res[0]) ? 0 : 1;
+                    pk y = mk(Xl[slot * xl + ak / N1]);
+                    const pk w1 = mk(a.twL(ak));  // e^{2 pi i |k| / L}
+                    pk ta, tb;
+                    if (ip == 0) {
+                        ta = mk(1.f, 0.f);
+                        tb = w1;
+                    } else {
+                        ta = pkx::cmul(w1, w1);
+                        tb = pkx::cmul(ta, w1);
+                    }
+                    if (k < 0) {
+                        y = pkx::conj(y);
+                        ta = pkx::conj(ta);
+                        tb = pkx::conj(tb);
+                    }
+                    acc = add(acc, add_rot<1>(pkx::cmul(y, ta), pkx::cmul(y, tb)));  // y ta + i y tb
+                }
+                x[j] = acc;
+            }
+            dft<32, 1>(x);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) buf[pad5(32 * i + j)] = f2(x[j]);
+        }
+        asm volatile("bar.sync 2, 128;" ::: "memory");
+        if (act) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
+#pragma unroll
+            for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(tw32[j * 32 + i])));
+            dft<32, 1>(x);
+            float2 *urow = reinterpret_cast<float2 *>(a.Uw) + ((sl * a.npi + ip) * N1 + res[r]) * (int64_t)S2;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const int u = i + 32 * j;
+                urow[u] = f2(pkx::cmul(x[j], mk(a.twS((int64_t)res[r] * u))));
+            }
+        }
+    }
+}
+
+// ---- IC: 16 FFTs (pair ip, 8 consecutive u) of length N1 over k2; output runs of 128 B ----------
+// lane = 16 il + 8 ip + t: butterfly i = 2 warp + il
+__global__ void __launch_bounds__(512) mci_fsf_ic(const FSArgs<float> a) {
+    using namespace fsf;
+    using namespace pkx;
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int BS = 1056 + 1;  // == 1 mod 16: conflict-free for the 16 FFTs of a half-warp
+    float2 *bufs = reinterpret_cast<float2 *>(smem);
+    float2 *tw = bufs + 16 * BS;  // [32][32] e^{-2 pi i j i/1024}
+    for (int q = threadIdx.x; q < 1024; q += 512) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    __syncthreads();
+    const int ntiles = S2 / 8;
+    const int tile = blockIdx.x % ntiles;
+    const int64_t sl = blockIdx.x / ntiles;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = lane & 7, ip = (lane >> 3) & 1, i = 2 * warp + (lane >> 4);
+    const int u = tile * 8 + t;
+    float2 *buf = bufs + (ip * 8 + t) * BS;
+    const float2 *ucol = reinterpret_cast<const float2 *>(a.Uw) + (sl * a.npi + ip) * (int64_t)N1 * S2 + u;
+    pk x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = mk(ucol[(int64_t)(i + 32 * j) * S2]);
+    dft<32, 1>(x);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) buf[pad5(32 * i + j)] = f2(x[j]);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
+#pragma unroll
+    for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(tw[j * 32 + i])));
+    dft<32, 1>(x);
+    // y[u + S2 v] = f[4 p2 + 2 ip + {0,1}], p2 = u + S2 v, v = i + 32 j
+    float2 *fo = reinterpret_cast<float2 *>(a.f + (a.sig0 + sl) * a.L);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        const int64_t p2 = u + (int64_t)S2 * (i + 32 * j);
+        __stcs(fo + 2 * p2 + ip, f2(x[j]));
+    }
+}
+
+bool fourstep_fast_ok(const Axis1D &ax) {
+    return ax.dtype == MCI_F32 && ax.N / 1024 == fsf::N2 && ax.S / 1024 == fsf::S2 && (ax.M == 3 || ax.M == 4) &&
+           ax.R == 4;
+}
+
+cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t st) {
+    using namespace fsf;
+    const size_t fa_sm = (size_t)(8 * (1056 + 2) + 1024) * 8;
+    const int64_t xl = a.K / N1 + 2;
+    const size_t fb_sm = (size_t)(4 * 273 + 4 * 256 + 2 * xl + 4 * 1060 + 256 + 1024) * 8;
+    const size_t ic_sm = (size_t)(16 * 1057 + 1024) * 8;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_ic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ic_sm))) return e;
+    mci_fsf_fa<<<(unsigned)(ns * a.npair * (N2 / 8)), 256, fa_sm, st>>>(a);
+    mci_fsf_fb<<<(unsigned)(ns * (N1 / 2 + 1)), 256, fb_sm, st>>>(a);
+    mci_fsf_ic<<<(unsigned)(ns * (S2 / 8)), 512, ic_sm, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace mci
