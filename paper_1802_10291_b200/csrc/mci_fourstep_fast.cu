@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(256) mci_fsf_fa(const FSArgs<float> a) {
 }
 
 // ---- FB: forward step 2 + solve + assembly + inverse step 1 for the residue pair --------------
-__global__ void __launch_bounds__(256) mci_fsf_fb(const FSArgs<float> a) {
+__global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
     using namespace fsf;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -79,9 +79,19 @@ __global__ void __launch_bounds__(256) mci_fsf_fb(const FSArgs<float> a) {
     float2 *ib = Xl + 2 * xl;                        // 4 x IB
     float2 *tw16 = ib + 4 * IB;                      // [16][16] e^{-2 pi i j b/256}
     float2 *tw32 = tw16 + 256;                       // [32][32] e^{-2 pi i j i/1024}
-    for (int q = threadIdx.x; q < 256; q += 256) tw16[q] = __ldg(a.twF + ((4 * (q >> 4) * (q & 15)) & 1023));
-    for (int q = threadIdx.x; q < 1024; q += 256) tw32[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    float2 *tw128 = tw32 + 1024;                     // [3][32] e^{2 pi i e j / 128}, e = 1, 2, 3
+    float2 *twE = tw128 + 96;                        // [2][32] e^{2 pi i 32 res_r j / S}
+    for (int q = threadIdx.x; q < 256; q += 128) tw16[q] = __ldg(a.twF + ((4 * (q >> 4) * (q & 15)) & 1023));
+    for (int q = threadIdx.x; q < 1024; q += 128) tw32[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
     const int q1 = blockIdx.x % (N1 / 2 + 1);
+    for (int q = threadIdx.x; q < 96; q += 128) {  // e^{+2 pi i e j / 128} = conj(twF[8 e j])
+        const float2 v = __ldg(a.twF + ((8 * ((q >> 5) + 1) * (q & 31)) & 1023));
+        tw128[q] = make_float2(v.x, -v.y);
+    }
+    for (int q = threadIdx.x; q < 64; q += 128) {
+        const int rq = (q >> 5) == 0 ? q1 : N1 - q1;
+        twE[q] = a.twS((int64_t)32 * rq * (q & 31));
+    }
     const int64_t sl = blockIdx.x / (N1 / 2 + 1);
     const int nres = (q1 == 0 || q1 == N1 / 2) ? 1 : 2;
     const int res[2] = {q1, N1 - q1};
@@ -118,7 +128,7 @@ __global__ void __launch_bounds__(256) mci_fsf_fb(const FSArgs<float> a) {
     float sup[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) sup[m] = 0.5f * pow2f(chan_exp(a, sl, m));
-    for (int idx = tid; idx < nres * N2; idx += 256) {
+    for (int idx = tid; idx < nres * N2; idx += 128) {
         const int r = idx / N2, q2 = idx % N2;
         const int64_t q = res[r] + (int64_t)N1 * q2;
         if (q > N / 2) continue;
@@ -175,39 +185,54 @@ __global__ void __launch_bounds__(256) mci_fsf_fb(const FSArgs<float> a) {
         }
     }
     __syncthreads();
-    // -- C: inverse step 1, 4 FFTs (residue r, pair ip) of length S2 over k1: radix 32 x 32 on 128 threads
+    // -- C: inverse step 1, 4 FFTs (residue r, pair ip) of length S2 over k1: radix 32 x 32 on 128 threads.
+    //    k' = res + N1 k1, k1 = i + 32 j.  With S = 2K: k' < K (j < 16) is k = k' (positive);
+    //    k' > K (j >= 16) is k = k' - S (negative, Y = conj X[S - k'], w^k = -i w^k'); k' = K
+    //    (res = 0, k1 = 512) carries both.  w^{k'} = w^{res + N1 i} e^{2 pi i j / 128}.
+    //    Zin(k') = W_{pa}(k) + i W_{pb}(k), W_p(k) = Y(k) w^{k p}, (pa, pb) = (2 ip, 2 ip + 1).
     if (tid < 128) {
         const int fi = tid >> 5, i = tid & 31, r = fi >> 1, ip = fi & 1;
         float2 *buf = ib + fi * IB;
         const bool act = r < nres;
         pk x[32];
         if (act) {
+            const int rr = res[r];
+            const int ro = (rr == 0) ? 0 : ((nres == 1) ? 0 : 1 - r);  // slot of residue N1 - rr
+            const float2 *Xp = Xl + r * xl, *Xn = Xl + ro * xl;
+            const pk P1 = mk(a.twL((int64_t)rr + (int64_t)N1 * i));   // w^{res + N1 i}
+            const pk P2 = pkx::cmul(P1, P1), P3 = pkx::cmul(P2, P1);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const int64_t kp = res[r] + (int64_t)N1 * (i + 32 * j);
-                pk acc = mk(0.f, 0.f);
-#pragma unroll
-                for (int w = 0; w < 2; ++w) {
-                    const int64_t k = w == 0 ? kp : kp - a.S;
-                    if (k > K || k < -K) continue;
-                    const int64_t ak = k >= 0 ? k : -k;
-                    const int slot = ((int)(ak % N1) == res[0]) ? 0 : 1;
-                    pk y = mk(Xl[slot * xl + ak / N1]);
-                    const pk w1 = mk(a.twL(ak));  // e^{2 pi i |k| / L}
-                    pk ta, tb;
+                const int k1 = i + 32 * j;
+                const pk c1 = mk(tw128[j]);                            // e^{2 pi i j / 128}
+                const pk w1 = pkx::cmul(P1, c1);                         // w^{k'}
+                pk acc;
+                if (j < 16) {  // positive frequencies: Y = X[k1] (slot r)
+                    const pk X = mk(Xp[k1]);
                     if (ip == 0) {
-                        ta = mk(1.f, 0.f);
-                        tb = w1;
+                        acc = add_rot<1>(X, pkx::cmul(X, w1));  // X + i X w
                     } else {
-                        ta = pkx::cmul(w1, w1);
-                        tb = pkx::cmul(ta, w1);
+                        const pk w2 = pkx::cmul(P2, mk(tw128[32 + j])), w3 = pkx::cmul(P3, mk(tw128[64 + j]));
+                        acc = add_rot<1>(pkx::cmul(X, w2), pkx::cmul(X, w3));
                     }
-                    if (k < 0) {
-                        y = pkx::conj(y);
-                        ta = pkx::conj(ta);
-                        tb = pkx::conj(tb);
+                } else {  // negative frequencies: Y = conj X[S - k'] (slot ro)
+                    const int idx = (rr == 0) ? (N1 - k1) : (N1 - 1 - k1);
+                    const pk Xc = pkx::conj(mk(Xn[idx]));
+                    if (ip == 0) {
+                        acc = add(Xc, pkx::cmul(Xc, w1));  // conj X + i conj X (-i w)
+                    } else {
+                        const pk w2 = pkx::cmul(P2, mk(tw128[32 + j])), w3 = pkx::cmul(P3, mk(tw128[64 + j]));
+                        acc = mul(add(pkx::cmul(Xc, w2), pkx::cmul(Xc, w3)), bc(-1.f));
                     }
-                    acc = add(acc, add_rot<1>(pkx::cmul(y, ta), pkx::cmul(y, tb)));  // y ta + i y tb
+                    if (rr == 0 && k1 == 512) {  // k' = K: add the k = +K term, Y = X[K]
+                        const pk X = mk(Xp[512]);
+                        if (ip == 0) {
+                            acc = add(acc, add_rot<1>(X, pkx::cmul(X, w1)));
+                        } else {
+                            const pk w2 = pkx::cmul(P2, mk(tw128[32 + j])), w3 = pkx::cmul(P3, mk(tw128[64 + j]));
+                            acc = add(acc, add_rot<1>(pkx::cmul(X, w2), pkx::cmul(X, w3)));
+                        }
+                    }
                 }
                 x[j] = acc;
             }
@@ -215,19 +240,19 @@ __global__ void __launch_bounds__(256) mci_fsf_fb(const FSArgs<float> a) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[pad5(32 * i + j)] = f2(x[j]);
         }
-        asm volatile("bar.sync 2, 128;" ::: "memory");
+        __syncthreads();
         if (act) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
 #pragma unroll
             for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(tw32[j * 32 + i])));
             dft<32, 1>(x);
+            // twiddle e^{2 pi i res u / S}, u = i + 32 j: base(i) * E[j], E[j] = e^{2 pi i 32 res j / S}
+            const pk B = mk(a.twS((int64_t)res[r] * i));
+            const float2 *E = twE + r * 32;
             float2 *urow = reinterpret_cast<float2 *>(a.Uw) + ((sl * a.npi + ip) * N1 + res[r]) * (int64_t)S2;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const int u = i + 32 * j;
-                urow[u] = f2(pkx::cmul(x[j], mk(a.twS((int64_t)res[r] * u))));
-            }
+            for (int j = 0; j < 32; ++j) urow[i + 32 * j] = f2(pkx::cmul(x[j], pkx::cmul(B, mk(E[j]))));
         }
     }
 }
@@ -281,14 +306,14 @@ cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t
     using namespace fsf;
     const size_t fa_sm = (size_t)(8 * (1056 + 2) + 1024) * 8;
     const int64_t xl = a.K / N1 + 2;
-    const size_t fb_sm = (size_t)(4 * 273 + 4 * 256 + 2 * xl + 4 * 1060 + 256 + 1024) * 8;
+    const size_t fb_sm = (size_t)(4 * 273 + 4 * 256 + 2 * xl + 4 * 1060 + 256 + 1024 + 96 + 64) * 8;
     const size_t ic_sm = (size_t)(16 * 1057 + 1024) * 8;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fsf_ic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ic_sm))) return e;
     mci_fsf_fa<<<(unsigned)(ns * a.npair * (N2 / 8)), 256, fa_sm, st>>>(a);
-    mci_fsf_fb<<<(unsigned)(ns * (N1 / 2 + 1)), 256, fb_sm, st>>>(a);
+    mci_fsf_fb<<<(unsigned)(ns * (N1 / 2 + 1)), 128, fb_sm, st>>>(a);
     mci_fsf_ic<<<(unsigned)(ns * (S2 / 8)), 512, ic_sm, st>>>(a);
     return cudaGetLastError();
 }
