@@ -77,6 +77,19 @@ def make_inputs(cfg, rank):
     return np.ascontiguousarray(np.tile(g, (reps, 1, 1, 1, 1)))
 
 
+def algorithmic_flops(cfg):
+    """Algorithmic flops per unit (row / signal / image), SURVEY.md §8(d) counting."""
+    c = synth.CONFIGS[cfg]
+    lg = math.log2
+    if cfg == 5:
+        n, L = c["N"], c["N"] * c["scale"]
+        line = 2 * 2.5 * n * lg(n) + 8 * 4 * (n // 2 + 1) + 2.5 * L * lg(L)
+        return (2 * n + L) * line  # per image: column pass Mx*Nx = 2n lines, row pass Ly = L lines
+    M, N, L = c["M"], c["N"], c["L"]
+    inv = 5 * L * lg(L) if c.get("hilbert") else 2.5 * L * lg(L)
+    return M * 2.5 * N * lg(N) + 8 * M * M * (N // 2 + 1) + inv
+
+
 def max_over_ranks(x: float, dist, device) -> float:
     """Max of a per-rank scalar over all ranks (the step time of a weak-scaling run)."""
     import torch
@@ -362,6 +375,14 @@ def main():
             "traffic": load_traffic(w["name"]), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes if cfg in (1, 2, 3) else None,
             "algorithmic_bytes_per_step": alg_bytes}
+    # secondary ceiling: the FP32 pipe.  Algorithmic flops per unit =
+    # SURVEY.md §8(d) counts (2.5 n log2 n per real FFT, 5 n log2 n complex, 8 M^2 per class).
+    flops = algorithmic_flops(cfg) * units
+    sm_clock = (clk.summary().get("sm_mhz") or 1965.0) * 1e6
+    fp32_peak = 148 * 128 * 2 * sm_clock / 1e12
+    roof["fp32"] = {"achieved_tflops": flops / (ms_step / 1e3) / 1e12, "peak_tflops": fp32_peak,
+                    "frac": flops / (ms_step / 1e3) / 1e12 / fp32_peak,
+                    "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sampled SM clock"}
 
     # end-to-end through the host-buffer C-ABI call (H2D + compute + D2H inside)
     e2e = None
