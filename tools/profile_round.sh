@@ -12,7 +12,7 @@ for c in 2 3 4 5; do
       --log-file $OUT/launches_c$c.csv $CMD --config $c > $OUT/ncu_launch_c$c.log 2>&1
   echo "launches cfg$c rc=$?"
 done
-declare -A KREGEX=([2]="mci_row" [3]="mci_fused" [4]="mci_fs_fb" [5]="mci_fused")
+declare -A KREGEX=([2]="mci_row" [3]="mci_hilbert" [4]="mci_fsf_fb" [5]="mci_line")
 for c in 2 3 4 5; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX[$c]} -s 4 -c 1 \
       -o $OUT/full_c$c $CMD --config $c > $OUT/ncu_full_c$c.log 2>&1
