@@ -211,11 +211,13 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
                                 sys[1].kind == MCI_SYS_DERIVATIVE && sys[1].order == 1 &&
                                 sys[2].kind == MCI_SYS_DERIVATIVE && sys[2].order == 2 && !getenv("MCI_ROW_QTAB"))
                                    ? 1 : 0;
-            // specialised row kernel tables: [wp: K+1][fw2: 32x32][itw: 64x64]
+            // specialised row kernel tables: [wp: K+1][fw2: 32x32][itw: 64x64][fw3: 16x64][fw8: 8x8]
             offs.push_back(blob.size());
             push_roots(blob, L, K + 1, 1, +1);
             for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, -1);
             for (int j = 0; j < 64; ++j) push_roots(blob, 4096, 64, j, +1);
+            for (int j = 0; j < 16; ++j) push_roots(blob, 1024, 64, j, -1);
+            for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
             ax.special = 1;
         } else if (mci::line_supported(ax)) {
             // line kernel tables: [wp: K+1][fwt: 32x16][iw: 32x32]

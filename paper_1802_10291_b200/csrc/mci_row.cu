@@ -77,6 +77,9 @@ __device__ __forceinline__ void group_bar(int id) { asm volatile("bar.sync %0, %
 // swizzles -- a constant offset per unrolled index, so no address arithmetic
 __device__ __forceinline__ int swz32(int a) { return a + (a >> 5); }  // forward, 1024 -> 1056
 __device__ __forceinline__ int swz64(int a) { return a + (a >> 6); }  // inverse, 4096 -> 4160
+// 4-warp forward (radix 8 x 8 x 16): no padding is conflict-free for all its strides;
+// this XOR swizzle is (brute-force checked), and keeps each 1024-point FFT in 1024 slots
+__device__ __forceinline__ int sw3(int a) { return a ^ ((a >> 3) & 15); }
 
 // 2^e as an exact float (|e| <= 100)
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
@@ -89,10 +92,12 @@ struct RowTables {
     const float2 *wp;   // [K+1]      e^{+2 pi i p / L}
     const float2 *fw2;  // [32][32]   e^{-2 pi i j k / 1024}     (forward pass 2)
     const float2 *itw;  // [64][64]   e^{+2 pi i j t / 4096}     (inverse pass 2)
+    const float2 *fw3;  // [16][64]   e^{-2 pi i j b / 1024}     (4-warp forward pass 3)
+    const float2 *fw8;  // [8][8]     e^{-2 pi i j k / 64}       (4-warp forward pass 2)
     int deriv;          // 1: bank is (1, ik, -k^2) -> closed-form Q (Example 2)
 };
 
-template <int G, bool QTAB>
+template <int G, bool QTAB, bool FW4 = false>
 struct RowCfg {
     static constexpr int M = 3, N = 1024, S = 4096, K = 1536, L = 16384;
     static constexpr int NQ = N / 2 + 1;
@@ -102,19 +107,22 @@ struct RowCfg {
     static constexpr int FWD_ELEMS = N + N / 32;             // padded forward buffer (1056)
     static constexpr int GROUP_BYTES = STAGE_BYTES + (2 * BUF_ELEMS + 8) * 8;  // B offset by 8 elements
     static constexpr int Q_BYTES = 0;  // table-mode Q~ is read through L1 (__ldg)
-    static constexpr int TAB_BYTES = (32 * 32 + 64 * 64 + K + 2) * 8;
+    static constexpr int FW_TAB = FW4 ? 16 * 64 + 8 * 8 : 32 * 32;  // forward twiddles
+    static constexpr int TAB_BYTES = (FW_TAB + 64 * 64 + K + 2) * 8;
     static constexpr int SMEM = G * GROUP_BYTES + Q_BYTES + TAB_BYTES;
 };
 
-template <int G, bool QTAB>
+template <int G, bool QTAB, bool FW4>
 __global__ void __launch_bounds__(G * rowk::NT, 1)
     mci_row_kernel(const float *__restrict__ g, float *__restrict__ f, int64_t rows, RowTables tb) {
     using namespace rowk;
-    using C = RowCfg<G, QTAB>;
+    using C = RowCfg<G, QTAB, FW4>;
+    static_assert(!FW4 || C::STAGED, "4-warp forward reads the TMA-staged row");
     constexpr int M = C::M, N = C::N, S = C::S, K = C::K, L = C::L;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar[G];
     __shared__ float ssup[G][4];
+    __shared__ float smx[G][4][3];  // per-warp channel maxima (4-warp forward)
 
     const int grp = threadIdx.x / NT;
     const int tid = threadIdx.x % NT;
@@ -126,11 +134,17 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     float2 *bufB = bufA + C::BUF_ELEMS + 8;  // +8 elements: A and B lanes of a half-warp hit different banks
     float2 *fwd = bufB;  // forward spectra (2 x 1024) alias buffer B
     float2 *fw2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
-    float2 *itw = fw2 + 32 * 32;  // [64][64] e^{+2 pi i j t / 4096}
+    float2 *fw3 = fw2, *fw8 = fw2 + 16 * 64;  // 4-warp forward twiddles (alias fw2)
+    float2 *itw = fw2 + C::FW_TAB;  // [64][64] e^{+2 pi i j t / 4096}
     float2 *wps = itw + 64 * 64;  // e^{+2 pi i p / L}, p = 0..K
 
     // ---- one-time setup
-    for (int i = threadIdx.x; i < 32 * 32; i += G * NT) fw2[i] = tb.fw2[i];
+    if constexpr (FW4) {
+        for (int i = threadIdx.x; i < 16 * 64; i += G * NT) fw3[i] = tb.fw3[i];
+        for (int i = threadIdx.x; i < 8 * 8; i += G * NT) fw8[i] = tb.fw8[i];
+    } else {
+        for (int i = threadIdx.x; i < 32 * 32; i += G * NT) fw2[i] = tb.fw2[i];
+    }
     for (int i = threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
     for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
     if (tid == 0) mbar_init(&mbar[grp], 1);
@@ -161,64 +175,155 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             phase ^= 1;
         }
 
-        // ---- forward: two register radix-32 passes; FFT c = fw on the channel pair
-        //      (g_{2c}, g_{2c+1}); channels scaled to unit range by exact powers of two
-        //      (avoids cross-channel rounding leakage when |f''| >> |f|)
-        {
-            const int c = fw, i = lane;
-            float2 *F = fwd + (c & 1) * C::FWD_ELEMS;
-            pk x[32];
-            if (fwd_warp) {  // pass 1: radix 32, Ls = 1, from the staged rows
-                const float *src = C::STAGED ? stage : g + row * (int64_t)(M * N);
-                const float *g0 = src + (2 * c) * N;
-                const float *g1 = src + (2 * c + 1) * N;
-                float m0 = 0.f, m1 = 0.f;
+        // ---- forward, 4-warp variant: both 1024-point FFTs as radix 8 x 8 x 16 Stockham
+        //      passes over all 128 threads (half the serial work per thread of the 2-warp
+        //      variant); pass 1 reads the staged rows, 2 -> buffer A, 3 -> buffer B.
+        if constexpr (FW4) {
+            const int b = tid;
+            {  // pass 1: radix 8, Ls = 1, butterfly b of both FFTs
+                pk x0[8], x1[8];
+                float m0 = 0.f, m1 = 0.f, m2 = 0.f;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float re = g0[i + 32 * j];
-                    const float im = c == 0 ? g1[i + 32 * j] : 0.f;
-                    x[j] = mk(re, im);
-                    m0 = fmaxf(m0, fabsf(re));
-                    m1 = fmaxf(m1, fabsf(im));
+                for (int j = 0; j < 8; ++j) {
+                    const float a0 = stage[b + 128 * j], a1 = stage[N + b + 128 * j],
+                                a2 = stage[2 * N + b + 128 * j];
+                    x0[j] = mk(a0, a1);
+                    x1[j] = mk(a2, 0.f);
+                    m0 = fmaxf(m0, fabsf(a0));
+                    m1 = fmaxf(m1, fabsf(a1));
+                    m2 = fmaxf(m2, fabsf(a2));
                 }
 #pragma unroll
                 for (int o = 16; o; o >>= 1) {
                     m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
                     m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+                    m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
                 }
-                const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
-                const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
-                const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
-                const pk sc = mk(pow2f(-e0), pow2f(-e1));
                 if (lane == 0) {
-                    ssup[grp][2 * c] = pow2f(e0);
-                    ssup[grp][2 * c + 1] = pow2f(e1);
+                    smx[grp][warp][0] = m0;
+                    smx[grp][warp][1] = m1;
+                    smx[grp][warp][2] = m2;
                 }
+                group_bar(barid);  // maxima visible; previous row's reads of buffers A/B complete
+                int e[3];
 #pragma unroll
-                for (int j = 0; j < 32; ++j) x[j] = pkx::mul(x[j], sc);
-                pkx::dft<32, -1>(x);
-            }
-            group_bar(barid);  // previous row's reads of buffers A/B are complete
-            if (fwd_warp) {
+                for (int m = 0; m < 3; ++m) {
+                    const float mm = fmaxf(fmaxf(smx[grp][0][m], smx[grp][1][m]), fmaxf(smx[grp][2][m], smx[grp][3][m]));
+                    const int E = (__float_as_int(mm) >> 23) & 0xff;
+                    e[m] = E == 0 ? 0 : max(-100, min(100, E - 126));
+                }
+                if (tid == 0) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) F[swz32(32 * i + j)] = f2(x[j]);
+                    for (int m = 0; m < 3; ++m) ssup[grp][m] = pow2f(e[m]);
+                }
+                const pk sc0 = mk(pow2f(-e[0]), pow2f(-e[1]));
+                const float sc1 = pow2f(-e[2]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    x0[j] = pkx::mul(x0[j], sc0);
+                    x1[j] = pkx::mul(x1[j], bc(sc1));
+                }
+                pkx::dft<8, -1>(x0);
+                pkx::dft<8, -1>(x1);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    bufB[sw3(8 * b + j)] = f2(x0[j]);
+                    bufB[1024 + sw3(8 * b + j)] = f2(x1[j]);
+                }
             }
             group_bar(barid);
-            if (C::STAGED && tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch
+            if (tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch the next row
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
                 tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
             }
-            if (fwd_warp) {  // pass 2: radix 32, Ls = 32, in place on own positions
+            {  // pass 2: radix 8, Ls = 8, B -> A
+                const int k = b & 7;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) x[j] = mk(F[swz32(i + 32 * j)]);
+                for (int c = 0; c < 2; ++c) {
+                    pk x[8];
 #pragma unroll
-                for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], mk(fw2[j * 32 + i]));
-                pkx::dft<32, -1>(x);
+                    for (int j = 0; j < 8; ++j) x[j] = mk(bufB[c * 1024 + sw3(b + 128 * j)]);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) F[swz32(i + 32 * j)] = f2(x[j]);
+                    for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(fw8[j * 8 + k]));
+                    pkx::dft<8, -1>(x);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) bufA[c * 1024 + sw3(8 * (b - k) + k + 8 * j)] = f2(x[j]);
+                }
             }
             group_bar(barid);
+            {  // pass 3: radix 16, Ls = 64, A -> B; FFT c = tid / 64
+                const int c = tid >> 6, bb = tid & 63;
+                pk x[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) x[j] = mk(bufA[c * 1024 + sw3(bb + 64 * j)]);
+#pragma unroll
+                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(fw3[j * 64 + bb]));
+                pkx::dft<16, -1>(x);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) bufB[c * 1024 + sw3(bb + 64 * j)] = f2(x[j]);
+            }
+            group_bar(barid);
+        } else {
+            // ---- forward: two register radix-32 passes; FFT c = fw on the channel pair
+            //      (g_{2c}, g_{2c+1}); channels scaled to unit range by exact powers of two
+            //      (avoids cross-channel rounding leakage when |f''| >> |f|)
+            {
+                const int c = fw, i = lane;
+                float2 *F = fwd + (c & 1) * C::FWD_ELEMS;
+                pk x[32];
+                if (fwd_warp) {  // pass 1: radix 32, Ls = 1, from the staged rows
+                    const float *src = C::STAGED ? stage : g + row * (int64_t)(M * N);
+                    const float *g0 = src + (2 * c) * N;
+                    const float *g1 = src + (2 * c + 1) * N;
+                    float m0 = 0.f, m1 = 0.f;
+    #pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float re = g0[i + 32 * j];
+                        const float im = c == 0 ? g1[i + 32 * j] : 0.f;
+                        x[j] = mk(re, im);
+                        m0 = fmaxf(m0, fabsf(re));
+                        m1 = fmaxf(m1, fabsf(im));
+                    }
+    #pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+                        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+                    }
+                    const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
+                    const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
+                    const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
+                    const pk sc = mk(pow2f(-e0), pow2f(-e1));
+                    if (lane == 0) {
+                        ssup[grp][2 * c] = pow2f(e0);
+                        ssup[grp][2 * c + 1] = pow2f(e1);
+                    }
+    #pragma unroll
+                    for (int j = 0; j < 32; ++j) x[j] = pkx::mul(x[j], sc);
+                    pkx::dft<32, -1>(x);
+                }
+                group_bar(barid);  // previous row's reads of buffers A/B are complete
+                if (fwd_warp) {
+    #pragma unroll
+                    for (int j = 0; j < 32; ++j) F[swz32(32 * i + j)] = f2(x[j]);
+                }
+                group_bar(barid);
+                if (C::STAGED && tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
+                    tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
+                }
+                if (fwd_warp) {  // pass 2: radix 32, Ls = 32, in place on own positions
+    #pragma unroll
+                    for (int j = 0; j < 32; ++j) x[j] = mk(F[swz32(i + 32 * j)]);
+    #pragma unroll
+                    for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], mk(fw2[j * 32 + i]));
+                    pkx::dft<32, -1>(x);
+    #pragma unroll
+                    for (int j = 0; j < 32; ++j) F[swz32(i + 32 * j)] = f2(x[j]);
+                }
+                group_bar(barid);
+            }
         }
 
         // ---- solve.  M = 3: for 0 < q < N/2 the class is j_q = q - N with elements
@@ -232,8 +337,13 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             if (u < 4 || tid == 0) {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    zq[u][c] = mk(fwd[c * C::FWD_ELEMS + swz32(q)]);
-                    zm[u][c] = mk(fwd[c * C::FWD_ELEMS + swz32(qm)]);
+                    if constexpr (FW4) {
+                        zq[u][c] = mk(bufB[c * 1024 + sw3(q)]);
+                        zm[u][c] = mk(bufB[c * 1024 + sw3(qm)]);
+                    } else {
+                        zq[u][c] = mk(fwd[c * C::FWD_ELEMS + swz32(q)]);
+                        zm[u][c] = mk(fwd[c * C::FWD_ELEMS + swz32(qm)]);
+                    }
                 }
             }
         }
@@ -337,10 +447,10 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-template <int G, bool QTAB>
+template <int G, bool QTAB, bool FW4>
 static cudaError_t row_launch_t(const RowTables &tb, int64_t rows, const float *g, float *f, cudaStream_t st) {
-    using C = RowCfg<G, QTAB>;
-    auto kern = mci_row_kernel<G, QTAB>;
+    using C = RowCfg<G, QTAB, FW4>;
+    auto kern = mci_row_kernel<G, QTAB, FW4>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
@@ -370,12 +480,18 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     tb.wp = base;
     tb.fw2 = tb.wp + (ax.K + 1);
     tb.itw = tb.fw2 + 32 * 32;
+    tb.fw3 = tb.itw + 64 * 64;
+    tb.fw8 = tb.fw3 + 16 * 64;
     if (n_launches) *n_launches += 1;
     const float *gg = (const float *)g;
     float *ff = (float *)f;
     static const int groups = getenv("MCI_ROW_GROUPS") ? atoi(getenv("MCI_ROW_GROUPS")) : 2;
-    if (tb.deriv && groups == 3) return row_launch_t<3, false>(tb, rows, gg, ff, st);
-    return tb.deriv ? row_launch_t<2, false>(tb, rows, gg, ff, st) : row_launch_t<2, true>(tb, rows, gg, ff, st);
+    static const bool fw2warps = getenv("MCI_ROW_FWD2") != nullptr;  // A/B switch: 2-warp forward
+    if (tb.deriv && groups == 3) return row_launch_t<3, false, false>(tb, rows, gg, ff, st);
+    if (fw2warps)
+        return tb.deriv ? row_launch_t<2, false, false>(tb, rows, gg, ff, st)
+                        : row_launch_t<2, true, false>(tb, rows, gg, ff, st);
+    return tb.deriv ? row_launch_t<2, false, true>(tb, rows, gg, ff, st) : row_launch_t<2, true, true>(tb, rows, gg, ff, st);
 }
 
 }  // namespace mci
