@@ -218,6 +218,7 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             for (int j = 0; j < 64; ++j) push_roots(blob, 4096, 64, j, +1);
             for (int j = 0; j < 16; ++j) push_roots(blob, 1024, 64, j, -1);
             for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
+            ax.row_variant = getenv("MCI_ROW_VARIANT") ? atoi(getenv("MCI_ROW_VARIANT")) : 0;
             ax.special = 1;
         } else if (mci::line_supported(ax)) {
             // line kernel tables: [wp: K+1][fwt: 32x16][iw: 32x32]

@@ -24,7 +24,6 @@
 //   * all complex arithmetic runs on packed FP32x2 instructions (FADD2/FFMA2/
 //     FMUL2, mci_pk.cuh): same FLOP rate as scalar FFMA, half the issue slots.
 #include <cstdint>
-#include <cstdlib>
 
 #include "mci_fft.cuh"
 #include "mci_internal.h"
@@ -108,7 +107,10 @@ struct RowCfg {
     static constexpr int GROUP_BYTES = STAGE_BYTES + (2 * BUF_ELEMS + 8) * 8;  // B offset by 8 elements
     static constexpr int Q_BYTES = 0;  // table-mode Q~ is read through L1 (__ldg)
     static constexpr int FW_TAB = FW4 ? 16 * 64 + 8 * 8 : 32 * 32;  // forward twiddles
-    static constexpr int TAB_BYTES = (FW_TAB + 64 * 64 + K + 2) * 8;
+    // G = 3 (12 warps) fits 227 KB only with the inverse twiddles (rows j >= 1) alone in
+    // shared memory; the pre-twiddle and forward tables are then read through L1
+    static constexpr bool SMALL_TAB = G >= 3;
+    static constexpr int TAB_BYTES = SMALL_TAB ? 63 * 64 * 8 : (FW_TAB + 64 * 64 + K + 2) * 8;
     static constexpr int SMEM = G * GROUP_BYTES + Q_BYTES + TAB_BYTES;
 };
 
@@ -117,7 +119,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     mci_row_kernel(const float *__restrict__ g, float *__restrict__ f, int64_t rows, RowTables tb) {
     using namespace rowk;
     using C = RowCfg<G, QTAB, FW4>;
-    static_assert(!FW4 || C::STAGED, "4-warp forward reads the TMA-staged row");
+    static_assert(!C::SMALL_TAB || FW4, "G = 3 uses the 4-warp forward");
     constexpr int M = C::M, N = C::N, S = C::S, K = C::K, L = C::L;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar[G];
@@ -135,18 +137,26 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     float2 *fwd = bufB;  // forward spectra (2 x 1024) alias buffer B
     float2 *fw2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
     float2 *fw3 = fw2, *fw8 = fw2 + 16 * 64;  // 4-warp forward twiddles (alias fw2)
-    float2 *itw = fw2 + C::FW_TAB;  // [64][64] e^{+2 pi i j t / 4096}
+    float2 *itw = C::SMALL_TAB ? fw2 - 64 : fw2 + C::FW_TAB;  // [64][64] e^{+2 pi i j t / 4096} (j >= 1 used)
     float2 *wps = itw + 64 * 64;  // e^{+2 pi i p / L}, p = 0..K
+    // table reads: shared memory, or L1 (__ldg) in the G = 3 layout
+    auto ld_wp = [&](int p) { return C::SMALL_TAB ? __ldg(tb.wp + p) : wps[p]; };
+    auto ld_fw3 = [&](int i) { return C::SMALL_TAB ? __ldg(tb.fw3 + i) : fw3[i]; };
+    auto ld_fw8 = [&](int i) { return C::SMALL_TAB ? __ldg(tb.fw8 + i) : fw8[i]; };
 
     // ---- one-time setup
-    if constexpr (FW4) {
+    if constexpr (C::SMALL_TAB) {
+        for (int i = 64 + threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
+    } else if constexpr (FW4) {
         for (int i = threadIdx.x; i < 16 * 64; i += G * NT) fw3[i] = tb.fw3[i];
         for (int i = threadIdx.x; i < 8 * 8; i += G * NT) fw8[i] = tb.fw8[i];
     } else {
         for (int i = threadIdx.x; i < 32 * 32; i += G * NT) fw2[i] = tb.fw2[i];
     }
-    for (int i = threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
-    for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
+    if constexpr (!C::SMALL_TAB) {
+        for (int i = threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
+        for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
+    }
     if (tid == 0) mbar_init(&mbar[grp], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
@@ -185,8 +195,17 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
                 float m0 = 0.f, m1 = 0.f, m2 = 0.f;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const float a0 = stage[b + 128 * j], a1 = stage[N + b + 128 * j],
-                                a2 = stage[2 * N + b + 128 * j];
+                    float a0, a1, a2;
+                    if constexpr (C::STAGED) {
+                        a0 = stage[b + 128 * j];
+                        a1 = stage[N + b + 128 * j];
+                        a2 = stage[2 * N + b + 128 * j];
+                    } else {  // streaming loads (evict-first: keep L1 for the tables)
+                        const float *src = g + row * (int64_t)(M * N);
+                        a0 = __ldcs(src + b + 128 * j);
+                        a1 = __ldcs(src + N + b + 128 * j);
+                        a2 = __ldcs(src + 2 * N + b + 128 * j);
+                    }
                     x0[j] = mk(a0, a1);
                     x1[j] = mk(a2, 0.f);
                     m0 = fmaxf(m0, fabsf(a0));
@@ -232,7 +251,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
                 }
             }
             group_bar(barid);
-            if (tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch the next row
+            if (C::STAGED && tid == 0 && row + gstride < rows) {  // staged input consumed: prefetch the next row
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
                 tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
@@ -245,7 +264,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) x[j] = mk(bufB[c * 1024 + sw3(b + 128 * j)]);
 #pragma unroll
-                    for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(fw8[j * 8 + k]));
+                    for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(ld_fw8(j * 8 + k)));
                     pkx::dft<8, -1>(x);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) bufA[c * 1024 + sw3(8 * (b - k) + k + 8 * j)] = f2(x[j]);
@@ -258,7 +277,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) x[j] = mk(bufA[c * 1024 + sw3(bb + 64 * j)]);
 #pragma unroll
-                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(fw3[j * 64 + bb]));
+                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(ld_fw3(j * 64 + bb)));
                 pkx::dft<16, -1>(x);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) bufB[c * 1024 + sw3(bb + 64 * j)] = f2(x[j]);
@@ -353,7 +372,7 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
         group_bar(barid);  // forward spectra read: buffer B may now be overwritten
 
         auto emit = [&](int p, pk X) {
-            const pk a = mk(wps[p]);
+            const pk a = mk(ld_wp(p));
             const pk P1 = pkx::cmul(X, a);
             const pk P2 = pkx::cmul(P1, a);
             const pk P3 = pkx::cmul(P2, a);
@@ -485,13 +504,17 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     if (n_launches) *n_launches += 1;
     const float *gg = (const float *)g;
     float *ff = (float *)f;
-    static const int groups = getenv("MCI_ROW_GROUPS") ? atoi(getenv("MCI_ROW_GROUPS")) : 2;
-    static const bool fw2warps = getenv("MCI_ROW_FWD2") != nullptr;  // A/B switch: 2-warp forward
-    if (tb.deriv && groups == 3) return row_launch_t<3, false, false>(tb, rows, gg, ff, st);
-    if (fw2warps)
+    switch (ax.row_variant) {  // A/B variants (plan-time MCI_ROW_VARIANT); 0 is the tuned default
+    case 1:  // 2 groups (8 warps), 2-warp forward
         return tb.deriv ? row_launch_t<2, false, false>(tb, rows, gg, ff, st)
                         : row_launch_t<2, true, false>(tb, rows, gg, ff, st);
-    return tb.deriv ? row_launch_t<2, false, true>(tb, rows, gg, ff, st) : row_launch_t<2, true, true>(tb, rows, gg, ff, st);
+    case 2:  // 2 groups, 4-warp forward, all tables in shared memory
+        return tb.deriv ? row_launch_t<2, false, true>(tb, rows, gg, ff, st)
+                        : row_launch_t<2, true, true>(tb, rows, gg, ff, st);
+    default:  // 3 groups (12 warps), 4-warp forward, untiled inputs, inverse twiddles in shared memory
+        return tb.deriv ? row_launch_t<3, false, true>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true>(tb, rows, gg, ff, st);
+    }
 }
 
 }  // namespace mci

@@ -252,18 +252,22 @@ def test_host_execute_matches_device():
 
 
 # -------------------------------------------------------------------------- specialised row kernel
-@pytest.mark.parametrize("L,rows,qtab", [(16384, 301, False), (16384, 301, True), (8192, 37, False),
-                                         (16384, 1, False), (16384, 297, True)])
-def test_row_kernel_vs_oracle_and_generic(L, rows, qtab, monkeypatch):
+@pytest.mark.parametrize("L,rows,qtab,variant", [
+    (16384, 301, False, 0), (16384, 301, True, 0), (8192, 37, False, 0), (16384, 1, False, 0),
+    (16384, 297, True, 0), (16384, 5, False, 0), (16384, 301, False, 1), (16384, 298, True, 1),
+    (16384, 301, False, 2), (16384, 299, True, 2)])
+def test_row_kernel_vs_oracle_and_generic(L, rows, qtab, variant, monkeypatch):
     """The specialised config-2 kernel (mci_row.cu; closed-form Example-2 inverse or
-    the Q table) on ragged batches (group tails); L = 8192 exercises the generic
-    kernel.  Within tolerance of the oracle and of the generic fused kernel, and
-    bit-for-bit independent of batch size."""
+    the Q table; variant 0 = 3 row groups, 1/2 = the 2-group layouts) on ragged
+    batches (group tails); L = 8192 exercises the generic kernel.  Within tolerance
+    of the oracle and of the generic fused kernel, and bit-for-bit independent of
+    batch size."""
     m = mci()
     c = synth.CONFIGS[2]
     g = synth.cfg2_rows(np.arange(rows))
     # non-bandlimited rows too (class q* averaging on odd M)
     g[::2] = np.random.default_rng(7).standard_normal(g[::2].shape).astype(np.float32) * g[::2].std(axis=2, keepdims=True)
+    monkeypatch.setenv("MCI_ROW_VARIANT", str(variant))
     if qtab:
         monkeypatch.setenv("MCI_ROW_QTAB", "1")
     plan = m.Plan(3, 1024, L, c["bank"])
