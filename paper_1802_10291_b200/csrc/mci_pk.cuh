@@ -160,5 +160,89 @@ template <int R, int DIR> __device__ __forceinline__ void dft(pk *x) {
     }
 }
 
+// ---- DFTs with compile-time zero inputs (bit n of Z: x[n] == 0, never read).
+// Only the first stage of each sub-transform changes; supports at most one zero per
+// radix-4 / radix-2 group (asserted), which is all the row kernel needs.
+template <int R, int DIR, unsigned long long Z> __device__ __forceinline__ void dftz(pk *x);
+
+template <int DIR, unsigned Z> __device__ __forceinline__ void dft4z(pk &x0, pk &x1, pk &x2, pk &x3) {
+    static_assert((Z & 5) != 5 && (Z & 10) != 10, "at most one zero per butterfly pair");
+    pk t0, t1;  // x0 +- x2
+    if constexpr (Z & 4) { t0 = x0; t1 = x0; }
+    else if constexpr (Z & 1) { t0 = x2; t1 = mul(x2, bc(-1.f)); }
+    else { t0 = add(x0, x2); t1 = sub(x0, x2); }
+    if constexpr (Z & 8) {  // x3 = 0: x1 +- x3 = x1
+        const pk u = x1;
+        x0 = add(t0, u);
+        x2 = sub(t0, u);
+        x1 = add_rot<DIR>(t1, u);
+        x3 = sub_rot<DIR>(t1, u);
+    } else if constexpr (Z & 2) {  // x1 = 0: x1 + x3 = x3, x1 - x3 = -x3
+        const pk u = x3;
+        x0 = add(t0, u);
+        x2 = sub(t0, u);
+        x1 = sub_rot<DIR>(t1, u);
+        x3 = add_rot<DIR>(t1, u);
+    } else {
+        const pk t2 = add(x1, x3), t3 = sub(x1, x3);
+        x0 = add(t0, t2);
+        x2 = sub(t0, t2);
+        x1 = add_rot<DIR>(t1, t3);
+        x3 = sub_rot<DIR>(t1, t3);
+    }
+}
+
+template <unsigned long long Z, int n1, int R1, int R2> constexpr unsigned long long sub_mask() {
+    unsigned long long m = 0;
+    for (int n2 = 0; n2 < R2; ++n2)
+        if ((Z >> (n1 + R1 * n2)) & 1ull) m |= 1ull << n2;
+    return m;
+}
+
+template <int R1, int R2, int DIR, unsigned long long Z> __device__ __forceinline__ void dft2sz(pk *x) {
+    constexpr int R = R1 * R2;
+    pk y[R];
+    cl::static_for<0, R1>([&](auto n1c) {
+        constexpr int n1 = decltype(n1c)::value;
+        constexpr unsigned long long zm = sub_mask<Z, n1, R1, R2>();
+        pk t[R2];
+#pragma unroll
+        for (int n2 = 0; n2 < R2; ++n2)
+            if (!((zm >> n2) & 1ull)) t[n2] = x[n1 + R1 * n2];
+        dftz<R2, DIR, zm>(t);
+        cl::static_for<0, R2>([&](auto k2c) {
+            constexpr int k2 = decltype(k2c)::value;
+            y[n1 + R1 * k2] = twc<R, n1 * k2, DIR>(t[k2]);
+        });
+    });
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) {
+        pk t[R1];
+#pragma unroll
+        for (int n1 = 0; n1 < R1; ++n1) t[n1] = y[n1 + R1 * k2];
+        dft<R1, DIR>(t);
+#pragma unroll
+        for (int k1 = 0; k1 < R1; ++k1) x[k2 + R2 * k1] = t[k1];
+    }
+}
+
+template <int R, int DIR, unsigned long long Z> __device__ __forceinline__ void dftz(pk *x) {
+    if constexpr (Z == 0) {
+        dft<R, DIR>(x);
+    } else if constexpr (R == 4) {
+        dft4z<DIR, (unsigned)Z>(x[0], x[1], x[2], x[3]);
+    } else if constexpr (R == 8) {
+        dft2sz<2, 4, DIR, Z>(x);
+    } else if constexpr (R == 16) {
+        dft2sz<4, 4, DIR, Z>(x);
+    } else if constexpr (R == 32) {
+        dft2sz<4, 8, DIR, Z>(x);
+    } else if constexpr (R == 64) {
+        dft2sz<8, 8, DIR, Z>(x);
+    } else {
+        static_assert(R == 4, "dftz radix");
+    }
+}
+
 }  // namespace pkx
 }  // namespace mci

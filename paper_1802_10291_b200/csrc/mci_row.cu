@@ -447,7 +447,8 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             else x[j] = mk(0.f, 0.f);
         }
         group_bar(barid);
-        pkx::dft<64, 1>(x);
+        // inputs j = 25..39 (k' in (K, S-K)) are structurally zero: pruned from the first stage
+        pkx::dftz<64, 1, ((1ull << 40) - 1) & ~((1ull << 25) - 1)>(x);
 #pragma unroll
         for (int j = 0; j < 64; ++j) buf[swz64(64 * t + j)] = f2(x[j]);
         group_bar(barid);
