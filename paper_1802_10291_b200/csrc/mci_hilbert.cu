@@ -6,19 +6,22 @@
 // Hilbert twin through the one-sided analytic spectrum Z(0) = X(0),
 // Z(k) = 2 X(k) (Example 4; multiplier -i sgn k,
 // PAPER.md:107-116): one complex inverse DFT gives z = f + i Hf.
-// Layout: L = R S with S = 4096 = K and R = 16: output phase p1 of p = 16 p2 + p1
-// is a 4096-point inverse DFT of Z(k) e^{2 pi i k p1 / L} (k' = k mod S; k' = 0
-// also receives k = K).  One CTA (256 threads, 8 warps) per SM owns a row:
-//   * forward: one complex 4096-point FFT of (g0 + i g1) on warps 0-1 (radix 64 x 64),
-//     channels scaled by exact powers of two;
-//   * solve: 2049 classes -> Z[0..K] in shared memory;
-//   * two CTAs per row, 2 rounds of 4 FFTs each: lanes 4*tl + c run phase p1 on butterfly
-//     t = 8 warp + tl; the pre-twiddle is fused into the first pass's loads;
-//     two register radix-64 passes (packed FP32x2), padded buffers;
-//   * each quad of lanes writes 16 contiguous bytes of f and of Hf; the two CTAs
-//     of a row write the two halves of every 32-byte sector at the same time, so
-//     partial sectors merge in L2 instead of being read back from HBM.
+//
+// Inverse layout: L = R S with S = 2048, R = 32.  Output phase p1 of p = 32 p2 + p1
+// is the 2048-point inverse DFT over k' = k mod S of
+//     Zin(k') = sum_{k = k' (mod S), 0 <= k <= K} Z(k) e^{2 pi i k p1 / L}
+//             = w^{k' p1} (Z(k') + u Z(k' + S) [+ u^2 Z(2S) at k' = 0]),  u = e^{2 pi i p1 / 32}.
+// One CTA (256 threads, 8 warps) owns a row (persistent over rows):
+//   * forward: one complex 4096-point FFT of (g0 + i g1), channels scaled by exact
+//     powers of two, as three radix-16 passes over all 256 threads;
+//   * solve: 2049 classes -> Z[0..K] in shared memory; for the (1, ik) bank the
+//     closed-form inverse a(j) = ((j+N) G0 + i G1)/N^2, a(j+N) = (-j G0 - i G1)/N^2
+//     (exact in fp32), else the plan's Q table;
+//   * 4 rounds of 8 consecutive phases p1 = 8 r + c: lanes c = lane & 7 run phase c on
+//     butterfly tid >> 3, so every warp store writes 4 whole 32-byte sectors of f (and of Hf);
+//     pass 1 radix 64 with the pre-twiddle fused into its loads, pass 2 radix 32 x 2.
 #include <cstdint>
+#include <cstdlib>
 
 #include "mci_internal.h"
 #include "mci_pk.cuh"
@@ -26,18 +29,23 @@
 namespace mci {
 
 namespace hilk {
-constexpr int M = 2, N = 4096, S = 4096, K = 4096, L = 65536, R = 16, NT = 256;
-constexpr int BUF = S + S / 64 + 4;  // padded FFT buffer (pad6); +4 spreads the 4 FFTs of a half-warp over banks
+constexpr int M = 2, N = 4096, K = 4096, L = 65536, S = 2048, R = 32, NT = 256;
+constexpr int BUF = 2082;               // padded 2048-point buffer (pad6 -> 2079 used); = 2 (mod 16)
+constexpr int NBUF = 8;                 // one per phase of a round
+constexpr int ZLEN = K + 2;             // Z[0..K] (+1 pad)
+constexpr int ITW_LD = 65;              // row stride of the [32][65] twiddle table
 __device__ __forceinline__ int pad6(int a) { return a + (a >> 6); }
+__device__ __forceinline__ int pad4(int a) { return a + (a >> 4); }  // forward 4096-point buffer
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 __device__ __forceinline__ void bar() { __syncthreads(); }
 }  // namespace hilk
 
 struct HilbertTables {
-    const float2 *Qt;   // [N/2+1][2][2]   H^{-1}/N per class
+    const float2 *Qt;   // [N/2+1][2][2]   H^{-1}/N per class (table mode)
     const float2 *whi;  // [256]  e^{+2 pi i 256 h / L}
     const float2 *wlo;  // [256]  e^{+2 pi i l / L}
-    const float2 *itw;  // [64][64] e^{+2 pi i j t / 4096}  (inverse pass 2; conj for the forward)
+    const float2 *itw;  // [32][65] e^{+2 pi i j t / 2048}
+    int deriv;          // 1: bank is (1, ik) -> closed-form inverse
 };
 
 __global__ void __launch_bounds__(hilk::NT, 1)
@@ -46,41 +54,37 @@ __global__ void __launch_bounds__(hilk::NT, 1)
     using namespace hilk;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
-    float2 *Z = reinterpret_cast<float2 *>(smem);  // K+1 (+pad)
-    float2 *bufs = Z + (K + 2);                     // 4 x BUF
-    float2 *whi = bufs + 4 * BUF;                   // 256
+    float2 *Z = reinterpret_cast<float2 *>(smem);  // [ZLEN]
+    float2 *bufs = Z + ZLEN;                        // NBUF x BUF; the forward aliases bufs[0 .. 4352)
+    float2 *whi = bufs + NBUF * BUF;                // 256
     float2 *wlo = whi + 256;                        // 256
-    float2 *itw = wlo + 256;                        // 4096
-    __shared__ float ssc[4];
+    float2 *itw = wlo + 256;                        // 32 x 65
+    float2 *F = bufs;                               // forward spectrum, pad4 layout (4352 slots)
+    __shared__ float smx[8][2];
+    __shared__ float ssc[2];
     for (int i = threadIdx.x; i < 256; i += NT) {
         whi[i] = tb.whi[i];
         wlo[i] = tb.wlo[i];
     }
-    for (int i = threadIdx.x; i < 4096; i += NT) itw[i] = tb.itw[i];
+    for (int i = threadIdx.x; i < 32 * ITW_LD; i += NT) itw[i] = tb.itw[i];
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-    const int c = lane & 3;                 // FFT (phase) within the round
-    const int t = 8 * warp + (lane >> 2);   // butterfly index 0..63
-    float2 *buf = bufs + c * BUF;
+    // w = e^{+2 pi i m / L}, m in [0, L)
+    auto wL = [&](int m) { return pkx::cmul(mk(whi[m >> 8]), mk(wlo[m & 255])); };
 
-    // Two CTAs (adjacent blockIdx, co-scheduled) share a row: half hh runs phases
-    // p1 = 4 hh + c (round 0) and 8 + 4 hh + c (round 1), so every 32-byte sector of
-    // f / Hf (8 consecutive phases) is completed by two concurrent rounds.
-    const int hh = blockIdx.x & 1;
-    for (int64_t row = blockIdx.x >> 1; row < rows; row += gridDim.x >> 1) {
+    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
         const float *g0 = g + row * (int64_t)(M * N), *g1 = g0 + N;
-        bar();  // previous row done with all buffers
-        // ---- forward (warps 0-1): 4096-point FFT of (g0 + i g1), radix 64 x 64, in buffer 0
-        if (warp < 2) {
-            const int i = tid;  // butterfly 0..63
-            pk x[64];
+        // ---- forward: 4096-point FFT of (g0 + i g1), radix 16 x 16 x 16 (Stockham), all threads
+        {
+            const int b = tid;
+            pk x[16];
             float m0 = 0.f, m1 = 0.f;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const float a = __ldg(g0 + i + 64 * j), b = __ldg(g1 + i + 64 * j);
-                m0 = fmaxf(m0, fabsf(a));
-                m1 = fmaxf(m1, fabsf(b));
-                x[j] = mk(a, b);
+            for (int j = 0; j < 16; ++j) {
+                const float a0 = __ldcs(g0 + b + 256 * j), a1 = __ldcs(g1 + b + 256 * j);
+                m0 = fmaxf(m0, fabsf(a0));
+                m1 = fmaxf(m1, fabsf(a1));
+                x[j] = mk(a0, a1);
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) {
@@ -88,45 +92,74 @@ __global__ void __launch_bounds__(hilk::NT, 1)
                 m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
             }
             if (lane == 0) {
-                ssc[2 * warp] = m0;
-                ssc[2 * warp + 1] = m1;
+                smx[warp][0] = m0;
+                smx[warp][1] = m1;
             }
-            asm volatile("bar.sync 1, 64;" ::: "memory");
-            m0 = fmaxf(ssc[0], ssc[2]);
-            m1 = fmaxf(ssc[1], ssc[3]);
+            bar();  // maxima visible; previous row's last reads of the buffers are complete
+            m0 = smx[0][0];
+            m1 = smx[0][1];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) {
+                m0 = fmaxf(m0, smx[w][0]);
+                m1 = fmaxf(m1, smx[w][1]);
+            }
             const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
             const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
             const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
             const pk sc = mk(pow2f(-e0), pow2f(-e1));
 #pragma unroll
-            for (int j = 0; j < 64; ++j) x[j] = mul(x[j], sc);
-            dft<64, -1>(x);
+            for (int j = 0; j < 16; ++j) x[j] = mul(x[j], sc);
+            // pass 1: Ls = 1
+            dft<16, -1>(x);
 #pragma unroll
-            for (int j = 0; j < 64; ++j) bufs[pad6(64 * i + j)] = f2(x[j]);
-            asm volatile("bar.sync 1, 64;" ::: "memory");
+            for (int j = 0; j < 16; ++j) F[pad4(16 * b + j)] = f2(x[j]);
+            bar();
+            // pass 2: Ls = 16, twiddle e^{-2 pi i j k / 256} = conj(whi[j k])
+            {
+                const int k = b & 15;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) x[j] = mk(bufs[pad6(i + 64 * j)]);
+                for (int j = 0; j < 16; ++j) x[j] = mk(F[pad4(b + 256 * j)]);
 #pragma unroll
-            for (int j = 1; j < 64; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(itw[j * 64 + i])));
-            dft<64, -1>(x);
+                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(whi[(j * k) & 255])));
+                dft<16, -1>(x);
+                bar();
 #pragma unroll
-            for (int j = 0; j < 64; ++j) bufs[pad6(i + 64 * j)] = f2(x[j]);
+                for (int j = 0; j < 16; ++j) F[pad4(16 * (b - k) + k + 16 * j)] = f2(x[j]);
+            }
+            bar();
+            // pass 3: Ls = 256, twiddle e^{-2 pi i j b / 4096} = conj(w^{16 j b})
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = mk(F[pad4(b + 256 * j)]);
+#pragma unroll
+            for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], pkx::conj(wL((16 * j * b) & (L - 1))));
+            dft<16, -1>(x);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) F[pad4(b + 256 * j)] = f2(x[j]);
             if (tid == 0) {
                 ssc[0] = 0.5f * pow2f(e0);
                 ssc[1] = 0.5f * pow2f(e1);
             }
         }
         bar();
-        // ---- solve: j_q = q - N (elements q - N, q); Z(0) = X(0), Z(k) = 2 X(k)
+        // ---- solve: class q has j_q = q - N (elements q - N, q); Z(0) = X(0), Z(k) = 2 X(k)
         {
             const float h0 = ssc[0], h1 = ssc[1];
             for (int q = tid; q <= N / 2; q += NT) {
-                const pk zq = mk(bufs[pad6(q)]), zm = mk(bufs[pad6((N - q) & (N - 1))]);
+                const pk zq = mk(F[pad4(q)]), zm = mk(F[pad4((N - q) & (N - 1))]);
                 const pk G0 = mul(add(zq, pkx::conj(zm)), bc(h0));
                 const pk G1 = mul(rot<-1>(sub(zq, pkx::conj(zm))), bc(h1));
-                const float2 *Qq = tb.Qt + q * 4;
-                const pk v0 = add(pkx::cmul(G0, mk(__ldg(Qq + 0))), pkx::cmul(G1, mk(__ldg(Qq + 2))));
-                const pk v1 = add(pkx::cmul(G0, mk(__ldg(Qq + 1))), pkx::cmul(G1, mk(__ldg(Qq + 3))));
+                pk v0, v1;
+                if (tb.deriv) {
+                    // (1, ik): a(j) = ((j+N) G0 + i G1)/N^2, a(j+N) = (-j G0 - i G1)/N^2, j = q - N
+                    const float jn = (float)(q - N), inv = 1.f / ((float)N * (float)N);
+                    const pk iG1 = rot<1>(G1);
+                    v0 = add(mul(G0, bc((jn + (float)N) * inv)), mul(iG1, bc(inv)));
+                    v1 = sub(mul(G0, bc(-jn * inv)), mul(iG1, bc(inv)));
+                } else {
+                    const float2 *Qq = tb.Qt + q * 4;
+                    v0 = add(pkx::cmul(G0, mk(__ldg(Qq + 0))), pkx::cmul(G1, mk(__ldg(Qq + 2))));
+                    v1 = add(pkx::cmul(G0, mk(__ldg(Qq + 1))), pkx::cmul(G1, mk(__ldg(Qq + 3))));
+                }
                 if (q == 0) {  // elements -N (= -K) and 0
                     Z[0] = make_float2(f2(v1).x, 0.f);
                     Z[K] = f2(pkx::conj(v0));  // 2 * conj(a(-K)) / 2
@@ -139,42 +172,50 @@ __global__ void __launch_bounds__(hilk::NT, 1)
             }
         }
         bar();
-        // ---- 2 rounds of 4 phases: p1 = 8 r + 4 hh + c
-        for (int r = 0; r < 2; ++r) {
-            const int p1 = 8 * r + 4 * hh + c;
+        // ---- 4 rounds of 8 phases p1 = 8 r + c
+        const int c = tid & 7;
+        const int bt = tid >> 3;  // pass-1 butterfly (0..31); pass 2 runs bt and bt + 32
+        float2 *buf = bufs + c * BUF;
+        for (int r = 0; r < 4; ++r) {
+            const int p1 = 8 * r + c;
             pk x[64];
-            // pass 1 (Ls = 1): Zin(k') = Z(k') w^{k' p1} (+ Z(K) w^{K p1} at k' = 0), w = e^{2 pi i/L}
+            {  // pass 1 (Ls = 1): k' = bt + 32 j; Zin(k') = w^{k' p1} (Z(k') + u Z(k' + S)),
+               // w^{k' p1} = w^{bt p1} e^{2 pi i j p1 / 2048} (itw row p1)
+                const pk u = mk(whi[8 * p1]);  // e^{2 pi i 2048 p1 / L}
+                const pk wb = wL(bt * p1);
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const int kp = t + 64 * j;
-                const int m = (kp * p1) & (L - 1);
-                const pk w = pkx::cmul(mk(whi[m >> 8]), mk(wlo[m & 255]));
-                x[j] = pkx::cmul(mk(Z[kp]), w);
-            }
-            if (t == 0) {
-                const int m = (K * p1) & (L - 1);
-                const pk w = pkx::cmul(mk(whi[m >> 8]), mk(wlo[m & 255]));
-                x[0] = add(x[0], pkx::cmul(mk(Z[K]), w));
+                for (int j = 0; j < 64; ++j) {
+                    const int kp = bt + 32 * j;
+                    const pk s = add(mk(Z[kp]), pkx::cmul(mk(Z[kp + S]), u));
+                    x[j] = pkx::cmul(s, pkx::cmul(wb, mk(itw[p1 * ITW_LD + j])));
+                }
+                if (bt == 0) {  // k' = 0 also receives k = 2S = K: u^2 Z(K)
+                    x[0] = add(x[0], pkx::cmul(mk(Z[K]), mk(whi[(16 * p1) & 255])));  // e^{2 pi i 4096 p1 / L}
+                }
             }
             dft<64, 1>(x);
-            bar();  // previous round's pass-2 loads are done before buffers are rewritten
+            bar();  // previous round's pass-2 loads are complete before the buffers are rewritten
 #pragma unroll
-            for (int j = 0; j < 64; ++j) buf[pad6(64 * t + j)] = f2(x[j]);
+            for (int j = 0; j < 64; ++j) buf[pad6(64 * bt + j)] = f2(x[j]);
             bar();
-            // pass 2 (Ls = 64)
-#pragma unroll
-            for (int j = 0; j < 64; ++j) x[j] = mk(buf[pad6(t + 64 * j)]);
-#pragma unroll
-            for (int j = 1; j < 64; ++j) x[j] = pkx::cmul(x[j], mk(itw[j * 64 + t]));
-            dft<64, 1>(x);
-            // outputs p = 16 p2 + p1, p2 = t + 64 j: z = f + i Hf
+            // pass 2 (Ls = 64): radix 32 on butterflies t = bt and bt + 32; outputs p2 = t + 64 j
             float *fr = f + row * (int64_t)L + p1, *hr = hf + row * (int64_t)L + p1;
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-                const float2 z = f2(x[j]);
-                const int64_t o = (int64_t)R * (t + 64 * j);
-                fr[o] = z.x;
-                hr[o] = z.y;
+            for (int hh = 0; hh < 2; ++hh) {
+                const int t = bt + 32 * hh;
+                pk y[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) y[j] = mk(buf[pad6(t + 64 * j)]);
+#pragma unroll
+                for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(itw[j * ITW_LD + t]));
+                dft<32, 1>(y);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float2 z = f2(y[j]);
+                    const int64_t o = (int64_t)R * (t + 64 * j);
+                    __stcs(fr + o, z.x);
+                    __stcs(hr + o, z.y);
+                }
             }
         }
     }
@@ -190,18 +231,19 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     using namespace hilk;
     HilbertTables tb;
     tb.Qt = (const float2 *)ax.Qt;
-    const float2 *base = (const float2 *)ax.rowtab;  // [whi 256][wlo 256][itw 4096]
+    const float2 *base = (const float2 *)ax.rowtab;  // [whi 256][wlo 256][itw 32 x 65]
     tb.whi = base;
     tb.wlo = base + 256;
     tb.itw = base + 512;
-    const size_t smem = (size_t)(K + 2 + 4 * BUF + 512 + 4096) * 8;
+    tb.deriv = ax.bank_deriv01;
+    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8;
     cudaError_t e = cudaFuncSetAttribute(mci_hilbert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    int64_t grid = nsm & ~1;  // CTA pairs, one row per pair
-    if (grid > 2 * rows) grid = 2 * rows;
+    int64_t grid = nsm;
+    if (grid > rows) grid = rows;
     if (n_launches) *n_launches += 1;
     mci_hilbert_kernel<<<(unsigned)grid, NT, smem, st>>>((const float *)g, (float *)f, (float *)hf, rows, tb);
     return cudaGetLastError();

@@ -228,11 +228,14 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, +1);
             ax.special = 2;
         } else if (mci::hilbert_supported(ax)) {
-            // Hilbert kernel tables: [whi: 256][wlo: 256][itw: 64x64]
+            // Hilbert kernel tables: [whi: 256][wlo: 256][itw: 32 x 65 (row stride 65; col 64 unused)]
+            ax.bank_deriv01 = (M == 2 && n_null == 0 && sys[0].kind == MCI_SYS_IDENTITY &&
+                               sys[1].kind == MCI_SYS_DERIVATIVE && sys[1].order == 1 && !getenv("MCI_ROW_QTAB"))
+                                  ? 1 : 0;
             offs.push_back(blob.size());
             push_roots(blob, L, 256, 256, +1);
             push_roots(blob, L, 256, 1, +1);
-            for (int j = 0; j < 64; ++j) push_roots(blob, 4096, 64, j, +1);
+            for (int j = 0; j < 32; ++j) push_roots(blob, 2048, 65, j, +1);
             ax.special = 3;
         }
     }

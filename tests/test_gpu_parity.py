@@ -158,6 +158,33 @@ def test_cfg3_shape_hilbert():
     assert row_rel(f[0], fr) < 1e-5 and row_rel(hf[0], hr) < 1e-5
 
 
+@pytest.mark.parametrize("qtab", [False, True])
+def test_hilbert_kernel_vs_oracle_and_generic(qtab, monkeypatch):
+    """The specialised config-3 kernel (mci_hilbert.cu; closed-form (1, ik) inverse or
+    the Q table) on a batch larger than the persistent grid, with non-bandlimited
+    rows: within tolerance of the oracle (sampled rows) and of the generic fused
+    kernel (all rows), and bit-for-bit independent of batch size."""
+    m = mci()
+    c = synth.CONFIGS[3]
+    rows = 157
+    g = np.concatenate([synth.cfg3_rows(np.arange(8))] * 20)[:rows].copy()
+    g[1::3] = np.random.default_rng(11).standard_normal(g[1::3].shape).astype(np.float32) * 3.0
+    if qtab:
+        monkeypatch.setenv("MCI_ROW_QTAB", "1")
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"], hilbert=True)
+    f, hf = run_plan(plan, g)
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    pick = [1, 156]
+    assert row_rel(f[pick], P.eval(g[pick])).max() < F32_TOL
+    assert row_rel(hf[pick], P.eval(g[pick], hilbert=True)).max() < F32_TOL
+    monkeypatch.setenv("MCI_DISABLE_ROW", "1")
+    generic = m.Plan(c["M"], c["N"], c["L"], c["bank"], hilbert=True)
+    fg, hg = run_plan(generic, g)
+    assert row_rel(f, fg).max() < F32_TOL and row_rel(hf, hg).max() < F32_TOL
+    f1, h1 = run_plan(plan, g[-1:])
+    assert np.array_equal(f1[0], f[-1]) and np.array_equal(h1[0], hf[-1])
+
+
 # -------------------------------------------------------------------------- config 4
 def test_fourstep_small_delay():
     """Four-step path at a size the oracle tabulates: M=4, N=4096, L=65536."""
