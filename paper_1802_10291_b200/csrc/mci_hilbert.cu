@@ -38,6 +38,23 @@ __device__ __forceinline__ int pad6(int a) { return a + (a >> 6); }
 __device__ __forceinline__ int pad4(int a) { return a + (a >> 4); }  // forward 4096-point buffer
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 __device__ __forceinline__ void bar() { __syncthreads(); }
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// next row's input arrives by TMA bulk copy (cp.async.bulk + mbarrier) while this row is transformed
+__device__ __forceinline__ void stage_row(float *dst, const float *src, uint64_t *mb) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(mb)), "r"(M * N * 4) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(M * N * 4), "r"(su32(mb))
+                 : "memory");
+}
+__device__ __forceinline__ void stage_wait(uint64_t *mb, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(su32(mb)), "r"(parity)
+                     : "memory");
+}
 }  // namespace hilk
 
 struct HilbertTables {
@@ -60,6 +77,8 @@ __global__ void __launch_bounds__(hilk::NT, 1)
     float2 *wlo = whi + 256;                        // 256
     float2 *itw = wlo + 256;                        // 32 x 65
     float2 *F = bufs;                               // forward spectrum, pad4 layout (4352 slots)
+    float *stage = reinterpret_cast<float *>(itw + 32 * ITW_LD);  // [2][4096] input row
+    __shared__ __align__(8) uint64_t mbar;
     __shared__ float smx[8][2];
     __shared__ float ssc[2];
     for (int i = threadIdx.x; i < 256; i += NT) {
@@ -67,13 +86,20 @@ __global__ void __launch_bounds__(hilk::NT, 1)
         wlo[i] = tb.wlo[i];
     }
     for (int i = threadIdx.x; i < 32 * ITW_LD; i += NT) itw[i] = tb.itw[i];
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mbar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (blockIdx.x < rows) stage_row(stage, g + blockIdx.x * (int64_t)(M * N), &mbar);
+    }
     __syncthreads();
+    uint32_t parity = 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
     // w = e^{+2 pi i m / L}, m in [0, L)
     auto wL = [&](int m) { return pkx::cmul(mk(whi[m >> 8]), mk(wlo[m & 255])); };
 
     for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
-        const float *g0 = g + row * (int64_t)(M * N), *g1 = g0 + N;
+        stage_wait(&mbar, parity);
+        parity ^= 1;
         // ---- forward: 4096-point FFT of (g0 + i g1), radix 16 x 16 x 16 (Stockham), all threads
         {
             const int b = tid;
@@ -81,7 +107,7 @@ __global__ void __launch_bounds__(hilk::NT, 1)
             float m0 = 0.f, m1 = 0.f;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const float a0 = __ldcs(g0 + b + 256 * j), a1 = __ldcs(g1 + b + 256 * j);
+                const float a0 = stage[b + 256 * j], a1 = stage[N + b + 256 * j];
                 m0 = fmaxf(m0, fabsf(a0));
                 m1 = fmaxf(m1, fabsf(a1));
                 x[j] = mk(a0, a1);
@@ -96,6 +122,10 @@ __global__ void __launch_bounds__(hilk::NT, 1)
                 smx[warp][1] = m1;
             }
             bar();  // maxima visible; previous row's last reads of the buffers are complete
+            if (tid == 0 && row + gridDim.x < rows) {  // stage consumed: fetch the next row
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                stage_row(stage, g + (row + gridDim.x) * (int64_t)(M * N), &mbar);
+            }
             m0 = smx[0][0];
             m1 = smx[0][1];
 #pragma unroll
@@ -236,7 +266,7 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     tb.wlo = base + 256;
     tb.itw = base + 512;
     tb.deriv = ax.bank_deriv01;
-    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8;
+    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4;
     cudaError_t e = cudaFuncSetAttribute(mci_hilbert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148;
