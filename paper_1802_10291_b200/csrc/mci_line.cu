@@ -14,7 +14,11 @@
 //     passes; lane i writes float2 at p2 = i + 32 j (256 contiguous bytes);
 //   * packed FP32x2 arithmetic (mci_pk.cuh), XOR-swizzled warp-private buffers.
 // Lines are addressed with RowAddr, so the same kernel serves 1D batches and
-// both passes of the separable 2D transform (strided samples).
+// both passes of the separable 2D transform (strided samples).  In the 2D passes
+// (TILED) a CTA's 16 lines are adjacent in memory: the next tile [2][16][512] is
+// copied by 4-byte cp.async (transposed into a conflict-free [2][16][516] stage)
+// while the current one is transformed (one 16-warp CTA per SM: warp buffers,
+// stage and tables fill the 227 KB).
 #include <cstdint>
 
 #include "mci_internal.h"
@@ -28,6 +32,7 @@ constexpr int N = 512, S = 1024, L = 2048, K = 512, NQ = N / 2 + 1;
 __device__ __forceinline__ int sw3(int a) { return a + (a >> 4); }  // forward 512 -> 544
 __device__ __forceinline__ int sw5(int a) { return a + (a >> 5); }  // inverse 1024 -> 1056
 constexpr int BUF = S + S / 32;
+constexpr int SP = N + 4;  // stage row stride: = 4 (mod 32) -> conflict-free transposed cp.async
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 }  // namespace linek
 
@@ -39,7 +44,7 @@ struct LineTables {
 };
 
 template <int WARPS, bool TILED>
-__global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
+__global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
                                                               int64_t lines, RowAddr ra, LineTables tb) {
     using namespace linek;
     using namespace pkx;
@@ -49,19 +54,42 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
     float2 *fwt = wps + K + 2;                      // 512
     float2 *iw = fwt + 512;                         // 1024
     float2 *bufs = iw + 1024;                       // WARPS x BUF
+    float *stage = reinterpret_cast<float *>(bufs + WARPS * BUF);  // TILED: [2][WARPS][SP]
     for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
     for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
     for (int i = threadIdx.x; i < 512; i += WARPS * 32) fwt[i] = tb.fwt[i];
     for (int i = threadIdx.x; i < 1024; i += WARPS * 32) iw[i] = tb.iw[i];
     __syncthreads();
+    auto ldQ = [&](int i) { return Qs[i]; };
+    auto ldwp = [&](int i) { return wps[i]; };
+    auto ldfw = [&](int i) { return fwt[i]; };
+    auto ldiw = [&](int i) { return iw[i]; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2 *buf = bufs + warp * BUF;
 
     // TILED (2D passes): WARPS consecutive lines are adjacent in memory (s0 = 1) while
-    // samples are strided; the CTA loads the tile [2][WARPS][N] with coalesced 16-byte
-    // loads (transposed on the way into shared memory, aliasing the warp buffers).
-    float *tile = reinterpret_cast<float *>(bufs);
+    // samples are strided.  Tile tl = [2][WARPS][N] is fetched by 4-byte cp.async: element
+    // e = (m, n, l) (l fastest: 8 lanes read one 32-byte sector) lands at stage[(m WARPS + l) SP + n].
     const int64_t ntiles = (lines + WARPS - 1) / WARPS;
+    auto tile_base = [&](int64_t t) {
+        const int64_t l0 = t * WARPS;
+        return (l0 / (ra.D0 * ra.D1)) * ra.s2 + ((l0 / ra.D0) % ra.D1) * ra.s1 + (l0 % ra.D0) * ra.s0;
+    };
+    auto fetch_tile = [&](int64_t t) {
+        if (t < ntiles) {
+            const float *src = g + tile_base(t);
+#pragma unroll 4
+            for (int e = threadIdx.x; e < 2 * N * WARPS; e += WARPS * 32) {
+                const int l = e % WARPS, n = (e / WARPS) % N, m = e / (WARPS * N);
+                const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + (m * WARPS + l) * SP + n);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst),
+                             "l"(src + m * ra.cs + (int64_t)n * ra.ss + l)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (TILED) fetch_tile(blockIdx.x);
     for (int64_t tl = blockIdx.x; tl < (TILED ? ntiles : (lines + WARPS - 1) / WARPS); tl += gridDim.x) {
         const int64_t line = tl * WARPS + warp;
         const int64_t base =
@@ -70,31 +98,22 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
         pk x[16];
         float m0 = 0.f, m1 = 0.f;
         if constexpr (TILED) {
-            __syncthreads();  // every warp is done with its buffer (tile aliases them)
-            const int64_t l0 = tl * WARPS;
-            const int64_t tb0 = (l0 / (ra.D0 * ra.D1)) * ra.s2 + ((l0 / ra.D0) % ra.D1) * ra.s1 + (l0 % ra.D0) * ra.s0;
-            for (int idx = threadIdx.x; idx < 2 * N * (WARPS / 4); idx += WARPS * 32) {
-                const int q4 = idx % (WARPS / 4), n = (idx / (WARPS / 4)) % N, m = idx / (N * (WARPS / 4));
-                const float4 v = __ldg(reinterpret_cast<const float4 *>(g + tb0 + m * ra.cs + (int64_t)n * ra.ss) + q4);
-                float *tr = tile + (m * WARPS + 4 * q4) * N + n;
-                tr[0] = v.x;
-                tr[N] = v.y;
-                tr[2 * N] = v.z;
-                tr[3 * N] = v.w;
-            }
-            __syncthreads();
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncthreads();  // tile tl has landed
             if (line < lines) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const int n = lane + 32 * j;
-                    const float a = tile[warp * N + n], b = tile[(WARPS + warp) * N + n];
+                    const float a = stage[warp * SP + n], b = stage[(WARPS + warp) * SP + n];
                     m0 = fmaxf(m0, fabsf(a));
                     m1 = fmaxf(m1, fabsf(b));
                     x[j] = mk(a, b);
                 }
             }
-            __syncthreads();  // tile consumed: warp buffers are free
+            __syncthreads();  // stage consumed: fetch the CTA's next tile while this one is transformed
+            fetch_tile(tl + gridDim.x);
             if (line >= lines) continue;
+            __syncwarp();  // previous line's reads of buf are complete
         } else {
             if (line >= lines) continue;
             __syncwarp();  // previous line's reads of buf are complete
@@ -129,7 +148,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
 #pragma unroll
             for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw3(lane + 16 * j)]);
 #pragma unroll
-            for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(fwt[j * 16 + lane]));
+            for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(ldfw(j * 16 + lane)));
             dft<32, -1>(y);
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[sw3(lane + 16 * j)] = f2(y[j]);
@@ -151,13 +170,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
         auto solve = [&](int u, int q, pk &v0, pk &v1) {
             const pk G0 = mul(add(zq[u], pkx::conj(zm[u])), bc(h0));
             const pk G1 = mul(rot<-1>(sub(zq[u], pkx::conj(zm[u]))), bc(h1));
-            const float2 *Qq = Qs + q * 4;  // [m][l]
-            v0 = add(pkx::cmul(G0, mk(Qq[0])), pkx::cmul(G1, mk(Qq[2])));
-            v1 = add(pkx::cmul(G0, mk(Qq[1])), pkx::cmul(G1, mk(Qq[3])));
+            const int Qq = q * 4;  // [m][l]
+            v0 = add(pkx::cmul(G0, mk(ldQ(Qq + 0))), pkx::cmul(G1, mk(ldQ(Qq + 2))));
+            v1 = add(pkx::cmul(G0, mk(ldQ(Qq + 1))), pkx::cmul(G1, mk(ldQ(Qq + 3))));
         };
         // inverse input (p1 = 0, 1 share one FFT): Zin(k) = Y(k)(1 + i w^k), w = e^{2 pi i/L}
         auto emit = [&](int p, pk X) {
-            const pk P = pkx::cmul(X, mk(wps[p]));
+            const pk P = pkx::cmul(X, mk(ldwp(p)));
             buf[sw5(p)] = f2(add_rot<1>(X, P));
             buf[sw5(S - p)] = f2(add_rot<1>(pkx::conj(X), pkx::conj(P)));
         };
@@ -173,7 +192,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
                 const float2 a0 = f2(v1);
                 buf[sw5(0)] = make_float2(a0.x, a0.x);  // X + iX, X real
                 const pk XK = mul(pkx::conj(v0), bc(0.5f));  // X[K] = conj a(-K)/2
-                const pk P = pkx::cmul(XK, mk(wps[K]));
+                const pk P = pkx::cmul(XK, mk(ldwp(K)));
                 buf[sw5(K)] = f2(add(add_rot<1>(XK, P), add_rot<1>(pkx::conj(XK), pkx::conj(P))));
             }
         }
@@ -196,7 +215,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) mci_line_kernel(const float *__
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
 #pragma unroll
-        for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(iw[j * 32 + lane]));
+        for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(ldiw(j * 32 + lane)));
         dft<32, 1>(y);
         float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
 #pragma unroll
@@ -213,18 +232,19 @@ size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 512 + 1024; }
 cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
                         int *n_launches) {
     if (lines <= 0) return cudaSuccess;
-    constexpr int WARPS = 8;
     LineTables tb;
     tb.Qt = (const float2 *)ax.Qt;
     const float2 *base = (const float2 *)ax.rowtab;  // [wp K+1][fwt 32x16][iw 32x32]
     tb.wp = base;
     tb.fwt = tb.wp + (ax.K + 1);
     tb.iw = tb.fwt + 512;
-    const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8;
-    const bool tiled = ra.s0 == 1 && ra.ss != 1 && ra.D0 % WARPS == 0 &&
+    const bool tiled = ra.s0 == 1 && ra.ss != 1 && ra.D0 % 16 == 0 &&
                        (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 && ra.s1 % 4 == 0 &&
                        ra.s2 % 4 == 0;
-    auto kern = tiled ? mci_line_kernel<WARPS, true> : mci_line_kernel<WARPS, false>;
+    const int WARPS = tiled ? 16 : 8;  // tiled: one 16-warp CTA per SM; else two 8-warp CTAs
+    auto kern = tiled ? mci_line_kernel<16, true> : mci_line_kernel<8, false>;
+    const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
+                        (tiled ? (size_t)2 * WARPS * linek::SP * 4 : 0);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;

@@ -327,8 +327,11 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
     p->Mx = Mx; p->My = My; p->Nx = Nx; p->Ny = Ny; p->Lx = ax.L; p->Ly = ay.L;
     p->path = mci::PATH_2D;
     const size_t per = (size_t)Mx * Nx * ay.L * sizeof(T);  // column-pass intermediate per image
-    // chunk of images whose intermediate (32 MB) stays L2-resident between the two passes
-    int64_t units = std::max<int64_t>(1, (int64_t)((32u << 20) / per));
+    // images per chunk: measured on B200 (config 5), fewer and fuller launches beat L2
+    // residency of the intermediate (32 MB: 1.35 ms, 128 MB: 1.15 ms, 256 MB: 1.12 ms,
+    // 512 MB: 1.10 ms per 64 images); 256 MB is the default footprint (MCI_2D_WS_MB overrides)
+    const size_t ws_mb = getenv("MCI_2D_WS_MB") ? (size_t)atoi(getenv("MCI_2D_WS_MB")) : 256;
+    int64_t units = std::max<int64_t>(1, (int64_t)((ws_mb << 20) / per));
     p->ws_units = units;
     p->ws_bytes = per * units;
     if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
