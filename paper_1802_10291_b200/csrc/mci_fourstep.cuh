@@ -34,6 +34,9 @@ template <typename T> struct FSArgs {
     Tw2<T> twS;  // e^{+2 pi i m/S}
     Tw2<T> twL;  // e^{+2 pi i m/L}
     int64_t sig0;  // first signal of this chunk (input/output offset)
+    int64_t Kmod;  // K mod N (class index j_q = -K + (q + Kmod) mod N without a division)
+    int delay_uniform;  // closed-form solve for the uniform delay bank (Axis1D::bank_delay_uniform)
+    int64_t lmn;        // L / (M N): e^{-i j tau_m} = conj(w_L^{j m lmn})
     typename std::conditional<sizeof(T) == 4, unsigned, unsigned long long>::type *cmax;  // [sig][M] |g| max bits
 };
 

@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
         if (q > N / 2) continue;
         const int rm = (nres == 1) ? 0 : 1 - r;
         const int q2m = (res[r] == 0) ? ((N2 - q2) % N2) : (N2 - 1 - q2);
-        const int64_t jq = -K + (((q + K) % N) + N) % N;
+        int64_t jt = q + a.Kmod;
+        if (jt >= N) jt -= N;
+        const int64_t jq = -K + jt;
         pk gm[4];
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
@@ -147,14 +149,31 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
             }
         }
         pk v[4];
-        const float2 *Qq = reinterpret_cast<const float2 *>(a.Qt) + q * M * M;
+        if (a.delay_uniform) {
+            // H^{-1}/N = diag(e^{-i j tau_m}) W^H / (M N): twiddle, then a 4-point DFT
+            const float s = 1.f / (float)(M * N);
+            pk u[4];
+            u[0] = mul(gm[0], bc(s));
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-            pk acc = mk(0.f, 0.f);
+            for (int m = 1; m < 4; ++m) {
+                const float2 w = a.twL(jq * m * a.lmn);  // e^{+i j tau_m}
+                u[m] = mul(pkx::cmul(gm[m], mk(w.x, -w.y)), bc(s));
+            }
+            const pk t0 = add(u[0], u[2]), t1 = sub(u[0], u[2]), t2 = add(u[1], u[3]), t3 = sub(u[1], u[3]);
+            v[0] = add(t0, t2);
+            v[2] = sub(t0, t2);
+            v[1] = add_rot<-1>(t1, t3);  // u0 - i u1 - u2 + i u3
+            v[3] = sub_rot<-1>(t1, t3);
+        } else {
+            const float2 *Qq = reinterpret_cast<const float2 *>(a.Qt) + q * M * M;
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-                if (m < M && l < M) acc = add(acc, pkx::cmul(gm[m], mk(__ldg(Qq + m * M + l))));
-            v[l] = acc;
+            for (int l = 0; l < 4; ++l) {
+                pk acc = mk(0.f, 0.f);
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    if (m < M && l < M) acc = add(acc, pkx::cmul(gm[m], mk(__ldg(Qq + m * M + l))));
+                v[l] = acc;
+            }
         }
         const bool selfm = (q == 0) || (2 * q == N);
 #pragma unroll

@@ -27,6 +27,7 @@ struct Axis1D {
     const void *rowtab = nullptr;  // tables of the specialised row kernel (mci_row.cu), or null
     int bank_deriv012 = 0;         // bank is exactly (1, ik, -k^2): closed-form inverse available
     int bank_deriv01 = 0;          // bank is exactly (1, ik): closed-form inverse available
+    int bank_delay_uniform = 0;    // bank is e^{ik 2 pi m/(MN)}, m < M = 4: H = W diag(e^{ij tau_m}) (closed form)
     int row_variant = 0;  // row kernel: 0 = 3 groups (default), 2 = 2 groups, 1 = 2 groups + 2-warp forward (MCI_ROW_VARIANT)
     int special = 0;  // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu), 3 Hilbert (mci_hilbert.cu)
 };

@@ -192,6 +192,15 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
         for (int m = 0; m < M; ++m)
             for (int l = 0; l < M; ++l) push_c(blob, inv[m * M + l] / (double)N);
     }
+    // uniform interleaved delay bank: H_j = W diag(e^{i j tau_m}),
+    // W[l][m] = e^{2 pi i l m / M}, so H_j^{-1} = diag(e^{-i j tau_m}) W^H / M
+    {
+        bool du = M == 4 && n_null == 0 && L % ((int64_t)M * N) == 0 && !getenv("MCI_ROW_QTAB");
+        for (int m = 0; du && m < M; ++m)
+            du = sys[m].kind == MCI_SYS_DELAY &&
+                 std::abs(sys[m].tau - 2 * PI * m / ((double)M * N)) <= 1e-12 * (1 + 2 * PI * m / ((double)M * N));
+        ax.bank_delay_uniform = du ? 1 : 0;
+    }
     // ---- forward-sign root table e^{-2 pi i m/TW}
     if (fourstep) ax.TW = std::max<int64_t>({1024, N / 1024, ax.S / 1024});
     else ax.TW = std::max<int64_t>({N, ax.S, 1024});

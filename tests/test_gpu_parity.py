@@ -235,6 +235,31 @@ def test_cfg4_full_size_sampled():
     assert err < 1e-5 * gt.abs().max().item()
 
 
+def test_cfg4_closed_form_vs_table_vs_generic(monkeypatch):
+    """configs[3] shape on non-bandlimited signals: the fast four-step with the
+    closed-form uniform-delay inverse (H = W diag(e^{ij tau_m})), with the plan's Q
+    table (MCI_ROW_QTAB), and the generic four-step kernels agree, and match the
+    closed-form delay oracle on sampled points."""
+    m = mci()
+    c = synth.CONFIGS[4]
+    M, N, L = c["M"], c["N"], c["L"]
+    g = np.random.default_rng(21).standard_normal((2, M, N)).astype(np.float32)
+    outs = []
+    for env in ({}, {"MCI_ROW_QTAB": "1"}, {"MCI_FOURSTEP_GENERIC": "1"}):
+        for k in ("MCI_ROW_QTAB", "MCI_FOURSTEP_GENERIC"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = m.Plan(M, N, L, c["bank"])
+        assert plan.path == "fourstep"
+        outs.append(run_plan(plan, g))
+    assert row_rel(outs[0], outs[1]).max() < F32_TOL
+    assert row_rel(outs[0], outs[2]).max() < F32_TOL
+    pts = np.random.default_rng(22).integers(0, L, 48)
+    ref = oracle.delay_eval_points(M, N, L, g[1], pts)
+    assert np.linalg.norm(outs[0][1, pts] - ref) / np.linalg.norm(ref) < F32_TOL
+
+
 # -------------------------------------------------------------------------- config 5 (2D)
 def test_2d_small_vs_oracle():
     m = mci()
