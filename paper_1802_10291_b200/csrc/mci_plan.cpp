@@ -301,10 +301,12 @@ mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *
     set_ptrs(ax, p->tables, offs, sizeof(T));
     p->ax = ax;
     if (p->path == mci::PATH_FOURSTEP) {
-        // workspace for a chunk of signals; sized so intermediates stay L2-resident (~80 MB)
+        // workspace for a chunk of signals.  Measured on B200 (config 4, 16 signals of
+        // 20 MB intermediates): fewer, fuller launches beat L2 residency (96 MB: 0.491 ms,
+        // 192 MB: 0.464 ms, 384 MB: 0.427 ms); 384 MB default (MCI_FS_WS_MB overrides)
         const size_t per = mci::fourstep_ws_bytes_per_signal(ax);
-        int64_t units = std::max<int64_t>(1, (int64_t)((96u << 20) / per));
-        units = std::min<int64_t>(units, 8);
+        const size_t ws_mb = getenv("MCI_FS_WS_MB") ? (size_t)atoi(getenv("MCI_FS_WS_MB")) : 384;
+        int64_t units = std::max<int64_t>(1, (int64_t)((ws_mb << 20) / per));
         p->ws_units = units;
         p->ws_bytes = per * units;
         if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
