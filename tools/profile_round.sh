@@ -1,20 +1,25 @@
 #!/bin/bash
 # Round profiling recipe (run under gpurun from the repo root; 1 GPU).
-# Plain run first (must exit 0), then the ncu launch list of the same command,
-# then one full capture of the dominant kernel per config.
+# 1. default bench line per config (cpu_baseline + e2e included), must exit 0;
+# 2. ncu launch list (gpu__time_duration per launch) of the same command;
+# 3. one full capture of the dominant kernel per config (cache control off, so DRAM
+#    bytes are those of the steady state, not of a flushed L2).
 set -u
 OUT=gpurun_out
 mkdir -p $OUT
+for c in 1 2 3 4 5; do
+  timeout 600 python bench.py --config $c > $OUT/bench_c$c.json 2> $OUT/bench_c$c.err || echo "bench cfg$c failed"
+done
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 for c in 2 3 4 5; do
-  timeout 300 $CMD --config $c > $OUT/plain_c$c.log 2>&1 || { echo "plain run cfg$c failed"; continue; }
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches_c$c.csv $CMD --config $c > $OUT/ncu_launch_c$c.log 2>&1
   echo "launches cfg$c rc=$?"
 done
 declare -A KREGEX=([2]="mci_row" [3]="mci_hilbert" [4]="mci_fsf_fb" [5]="mci_line")
+declare -A SKIP=([2]=4 [3]=4 [4]=2 [5]=8)
 for c in 2 3 4 5; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX[$c]} -s 4 -c 1 \
-      -o $OUT/full_c$c $CMD --config $c > $OUT/ncu_full_c$c.log 2>&1
+  timeout 900 ncu --set full --clock-control none --cache-control none --import-source on \
+      -k regex:${KREGEX[$c]} -s ${SKIP[$c]} -c 1 -o $OUT/full_c$c $CMD --config $c > $OUT/ncu_full_c$c.log 2>&1
   echo "full cfg$c rc=$?"
 done
