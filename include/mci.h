@@ -3,7 +3,8 @@
  *
  * Method: arXiv 1802.10291, "fast multichannel interpolation".
  * A real 2*pi-periodic signal f whose spectrum lies in the band
- * I^N = {K1 .. K1+M*N-1}, K1 = -M*N/2, is reconstructed from N uniform
+ * I^N = {K1 .. K1+M*N-1}, K1 = -floor(M*N/2) (odd M*N: the symmetric band of
+ * Examples 1-2), is reconstructed from N uniform
  * samples g_m(t_n), t_n = 2*pi*n/N, of each of M channel responses
  * g_m = h_m * f (Eq. sysfunction).  The output is
  *   f(t_p) = Re T_N f(t_p),  t_p = 2*pi*p/L,  p = 0..L-1,
@@ -47,10 +48,10 @@ typedef struct mci_plan_s *mci_plan; /* opaque */
 typedef enum {
     MCI_OK = 0,
     MCI_E_ARG = 1,         /* NULL pointer, non-positive size, bad enum            */
-    MCI_E_BAND = 2,        /* M*N odd or band invalid                               */
-    MCI_E_ALIAS = 3,       /* L < M*N, L odd, or L not a multiple of N */
+    MCI_E_BAND = 2,        /* band invalid (M*N < 2)                                */
+    MCI_E_ALIAS = 3,       /* L < M*N or L not a multiple of N        */
     MCI_E_SINGULAR = 4,    /* some H_n singular (see mci_last_singular_bin)         */
-    MCI_E_SIZE = 5,        /* sizes not supported (non powers of two, too large)    */
+    MCI_E_SIZE = 5,        /* sizes not supported (N < 2, or too large for a path)  */
     MCI_E_CUDA = 6,        /* a CUDA runtime call or kernel launch failed           */
     MCI_E_UNSUPPORTED = 7  /* valid request this build does not implement           */
 } mci_status;
@@ -78,8 +79,13 @@ enum { MCI_OUT_HILBERT = 1u }; /* plan also produces Hf */
 /* ---- plans ------------------------------------------------------------------------ */
 
 /* 1D plan: M channels (1..8), N samples per channel, L output points.
- * Requirements: N and L powers of two, M*N even, L >= M*N, L % N == 0,
- * Hermitian bank (b_m(-k) = conj b_m(k), true for every built-in kind).
+ * Requirements: N >= 2, L >= M*N, L % N == 0, Hermitian bank (b_m(-k) =
+ * conj b_m(k), true for every built-in kind).  N and L powers of two with M*N
+ * even use the specialised paths (fused per-row kernels, four-step for long
+ * signals); any other sizes (e.g. the paper's SISR widths 107..170, L = 3N, odd
+ * M*N) use the arbitrary-length path (mixed-radix FFTs, one CTA per row; it
+ * needs 2 max(ceil(M/2) N, L) + M N complex values of shared memory <= 200 KB,
+ * else MCI_E_SIZE).
  * H_n (entry (l,m) = b_m(n + l N), Eq. defH) must be
  * invertible for every n in I_1 except the listed Remark-1 null bins
  * (PAPER.md:325-327), whose inverse is set to zero.  Singular: some pivot

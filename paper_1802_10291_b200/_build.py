@@ -16,7 +16,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
-]
+] + os.environ.get("MCI_NVCC_EXTRA", "").split()  # experiment switches, e.g. -DMCI_ROW_PREFETCH=1
 
 
 def sources():

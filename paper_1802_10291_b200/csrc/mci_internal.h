@@ -10,6 +10,12 @@
 
 namespace mci {
 
+// Radix plan of a mixed-radix transform (arbitrary-length path): n passes, radices r[].
+struct AnyRadix {
+    int n = 0;
+    int r[24] = {0};
+};
+
 // Per-plan device tables for one 1D axis (fused or four-step path).
 struct Axis1D {
     int M = 0;
@@ -29,7 +35,11 @@ struct Axis1D {
     int bank_deriv01 = 0;          // bank is exactly (1, ik): closed-form inverse available
     int bank_delay_uniform = 0;    // bank is e^{ik 2 pi m/(MN)}, m < M = 4: H = W diag(e^{ij tau_m}) (closed form)
     int row_variant = 0;  // row kernel: 0 = 3 groups (default), 2 = 2 groups, 1 = 2 groups + 2-warp forward (MCI_ROW_VARIANT)
-    int special = 0;  // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu), 3 Hilbert (mci_hilbert.cu)
+    int special = 0;  // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu), 3 Hilbert (mci_hilbert.cu),
+                      // 4 arbitrary lengths (mci_anylen.cu: Qt has all N classes, twF = e^{-2 pi i m/N} [N],
+                      //   twLhi = e^{+2 pi i m/L} [L], band K1 = -floor(MN/2))
+    int64_t K1 = 0;   // lowest band frequency (arbitrary-length path)
+    AnyRadix radN, radL;
 };
 
 enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2 };
@@ -59,6 +69,11 @@ cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const
                         cudaStream_t st, int *n_launches);
 cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const void *g, void *f, cudaStream_t st,
                        int *n_launches);
+
+bool anylen_supported(const Axis1D &ax);
+size_t anylen_smem_bytes(const Axis1D &ax);
+cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
+                          cudaStream_t st, int *n_launches);
 
 cudaError_t launch_fourstep(const Axis1D &ax, int64_t batch, const void *g, void *f, void *ws,
                             int64_t ws_signals, cudaStream_t st, int *n_launches);

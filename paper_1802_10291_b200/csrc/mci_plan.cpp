@@ -257,6 +257,94 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
     return MCI_OK;
 }
 
+// Arbitrary-length axis (mci_anylen.cu): any N >= 2, L % N == 0,
+// L >= MN, band K1 = -floor(MN/2).  Q~ for every class q in [0, N), full root tables.
+bool use_anylen(int M, int64_t N, int64_t L) {
+    return !(is_pow2(N) && is_pow2(L) && ((int64_t)M * N) % 2 == 0) || getenv("MCI_FORCE_ANYLEN");
+}
+
+mci::AnyRadix radix_plan(int64_t n) {
+    mci::AnyRadix p;
+    auto push = [&](int r) { p.r[p.n++] = r; };
+    while (n % 4 == 0 && p.n < 23) { push(4); n /= 4; }
+    if (n % 2 == 0) { push(2); n /= 2; }
+    for (int r : {3, 5, 7})
+        while (n % r == 0 && p.n < 23) { push(r); n /= r; }
+    for (int64_t d = 11; d * d <= n && p.n < 23; d += 2)
+        while (n % d == 0) { push((int)d); n /= d; }
+    if (n > 1) push((int)n);
+    return p;
+}
+
+template <typename T>
+mci_status build_axis_any(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_system *sys,
+                          const int64_t *null_bins, int n_null, bool analytic, std::vector<T> &blob,
+                          std::vector<size_t> &offs, double &cond_max) {
+    if (M < 1 || M > 8 || !sys) return MCI_E_ARG;
+    if (N < 2) return MCI_E_SIZE;
+    const int64_t MN = (int64_t)M * N;
+    if (MN < 2) return MCI_E_BAND;
+    if (L < MN || L % N) return MCI_E_ALIAS;
+    const int64_t K1 = -(MN / 2);
+    for (int m = 0; m < M; ++m) {
+        const mci_system &s = sys[m];
+        if (s.kind < MCI_SYS_IDENTITY || s.kind > MCI_SYS_TABLE) return MCI_E_ARG;
+        if (s.kind == MCI_SYS_DERIVATIVE && s.order < 0) return MCI_E_ARG;
+        if (s.kind == MCI_SYS_TABLE) {
+            if (!s.table) return MCI_E_ARG;
+            for (int64_t k = 1; -k >= K1 && k < K1 + MN; ++k) {  // Hermitian requirement (real output)
+                cd a = sys_multiplier(s, K1, k), b = sys_multiplier(s, K1, -k);
+                if (std::abs(a - std::conj(b)) > 1e-12 * (1 + std::abs(a))) return MCI_E_UNSUPPORTED;
+            }
+        }
+    }
+    ax.M = M; ax.N = N; ax.L = L; ax.K = -K1; ax.K1 = K1; ax.analytic = analytic ? 1 : 0;
+    ax.S = L; ax.R = 1;
+    ax.radN = radix_plan(N);
+    ax.radL = radix_plan(L);
+    if (ax.radN.n > 23 || ax.radL.n > 23) return MCI_E_SIZE;
+    offs.push_back(blob.size());  // Qt: every class
+    std::vector<cd> H(M * M), inv;
+    cond_max = 0.0;
+    for (int64_t q = 0; q < N; ++q) {
+        const int64_t jq = K1 + (((q - K1) % N) + N) % N;
+        bool is_null = false;
+        for (int z = 0; z < n_null; ++z)
+            if (null_bins[z] == jq) is_null = true;
+        double rowmax = 0.0;
+        for (int l = 0; l < M; ++l)
+            for (int m = 0; m < M; ++m) {
+                H[l * M + m] = sys_multiplier(sys[m], K1, jq + (int64_t)l * N);
+                rowmax = std::max(rowmax, std::abs(H[l * M + m]));
+            }
+        if (is_null) {
+            inv.assign(M * M, 0.0);
+        } else {
+            if (!lu_inverse(M, H, inv, 1e-12 * rowmax)) {
+                g_last_singular = jq;
+                return MCI_E_SINGULAR;
+            }
+            double n1 = 0, n2 = 0;
+            for (int c = 0; c < M; ++c) {
+                double s1 = 0, s2 = 0;
+                for (int r = 0; r < M; ++r) { s1 += std::abs(H[r * M + c]); s2 += std::abs(inv[r * M + c]); }
+                n1 = std::max(n1, s1);
+                n2 = std::max(n2, s2);
+            }
+            cond_max = std::max(cond_max, n1 * n2);
+        }
+        for (int m = 0; m < M; ++m)
+            for (int l = 0; l < M; ++l) push_c(blob, inv[m * M + l] / (double)N);
+    }
+    offs.push_back(blob.size());  // twF = e^{-2 pi i m / N}
+    push_roots(blob, N, N, 1, -1);
+    offs.push_back(blob.size());  // twLhi = e^{+2 pi i m / L}
+    push_roots(blob, L, L, 1, +1);
+    ax.LO = L;  // (twLlo unused on this path)
+    ax.special = 4;
+    return MCI_OK;
+}
+
 template <typename T>
 mci_status upload(mci_plan p, std::vector<T> &blob) {
     void *d = nullptr;
@@ -287,6 +375,16 @@ mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *
     // try the fused path first
     mci::Axis1D ax;
     ax.dtype = p->dtype;
+    if (use_anylen(M, N, L)) {  // arbitrary lengths / odd band
+        mci_status s = build_axis_any<T>(ax, M, N, L, sys, null_bins, n_null, analytic, blob, offs, p->cond_max);
+        if (s != MCI_OK) return s;
+        if (!mci::anylen_supported(ax)) return MCI_E_SIZE;
+        if ((s = upload<T>(p, blob)) != MCI_OK) return s;
+        set_ptrs(ax, p->tables, offs, sizeof(T));
+        p->ax = ax;
+        p->path = mci::PATH_FUSED;
+        return MCI_OK;
+    }
     mci_status s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, false, blob, offs, p->cond_max);
     if (s != MCI_OK) return s;
     if (!mci::fused_supported(ax)) {
@@ -322,11 +420,22 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
     double cx = 0, cy = 0;
     mci::Axis1D ax, ay;
     ax.dtype = ay.dtype = p->dtype;
-    mci_status s = build_axis<T>(ax, Mx, Nx, (int64_t)scale * Nx, sx, nullptr, 0, false, false, bx, ox, cx);
+    auto axis = [&](mci::Axis1D &a, int M, int64_t N, const mci_system *sy_, std::vector<T> &b, std::vector<size_t> &o,
+                    double &c) -> mci_status {
+        const int64_t L = (int64_t)scale * N;
+        if (use_anylen(M, N, L)) {
+            mci_status st = build_axis_any<T>(a, M, N, L, sy_, nullptr, 0, false, b, o, c);
+            if (st == MCI_OK && !mci::anylen_supported(a)) st = MCI_E_SIZE;
+            return st;
+        }
+        mci_status st = build_axis<T>(a, M, N, L, sy_, nullptr, 0, false, false, b, o, c);
+        if (st == MCI_OK && !mci::fused_supported(a)) st = MCI_E_UNSUPPORTED;
+        return st;
+    };
+    mci_status s = axis(ax, Mx, Nx, sx, bx, ox, cx);
     if (s != MCI_OK) return s;
-    s = build_axis<T>(ay, My, Ny, (int64_t)scale * Ny, sy, nullptr, 0, false, false, by, oy, cy);
+    s = axis(ay, My, Ny, sy, by, oy, cy);
     if (s != MCI_OK) return s;
-    if (!mci::fused_supported(ax) || !mci::fused_supported(ay)) return MCI_E_UNSUPPORTED;
     p->cond_max = std::max(cx, cy);
     const size_t nx = bx.size();
     bx.insert(bx.end(), by.begin(), by.end());
@@ -391,6 +500,7 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
 namespace mci {
 cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                         cudaStream_t st, int *nl) {
+    if (ax.special == 4) return launch_anylen(ax, ra, rows, g, f, hf, st, nl);
     if (ax.special == 1 && ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N)
         return launch_row(ax, ax.rowtab, rows, g, f, st, nl);
     if (ax.special == 2) return launch_line(ax, ra, rows, g, f, st, nl);
@@ -560,10 +670,10 @@ const char *mci_status_str(mci_status s) {
     switch (s) {
     case MCI_OK: return "ok";
     case MCI_E_ARG: return "invalid argument";
-    case MCI_E_BAND: return "invalid band (M*N must be even)";
-    case MCI_E_ALIAS: return "L must be a power of two, >= M*N and a multiple of N";
+    case MCI_E_BAND: return "invalid band (M*N < 2)";
+    case MCI_E_ALIAS: return "L must be >= M*N and a multiple of N";
     case MCI_E_SINGULAR: return "system matrix H_n singular (see mci_last_singular_bin)";
-    case MCI_E_SIZE: return "unsupported size (N must be a power of two)";
+    case MCI_E_SIZE: return "unsupported size (N < 2, or too large for the arbitrary-length path)";
     case MCI_E_CUDA: return "CUDA error";
     case MCI_E_UNSUPPORTED: return "unsupported configuration";
     }

@@ -40,9 +40,11 @@ def _create(M, N, L, bank, dtype=0, flags=0, null=()):
 def test_alias_band_size_errors():
     f = [("identity",), ("derivative", 1)]
     assert _create(2, 32, 32, f)[0] == mci.MCI_E_ALIAS          # L < MN
-    assert _create(2, 32, 96, f)[0] == mci.MCI_E_ALIAS          # L not a power of two
-    assert _create(2, 24, 256, f)[0] == mci.MCI_E_SIZE          # N not a power of two
+    assert _create(2, 32, 80, f)[0] == mci.MCI_E_ALIAS          # L not a multiple of N
+    assert _create(2, 24, 36, f)[0] == mci.MCI_E_ALIAS          # arbitrary-length path: L < MN
+    assert _create(2, 24, 60, f)[0] == mci.MCI_E_ALIAS          # arbitrary-length path: L % N != 0
     assert _create(1, 1, 16, [("identity",)])[0] == mci.MCI_E_SIZE
+    assert _create(2, 40000, 160000, f)[0] == mci.MCI_E_SIZE    # exceeds the arbitrary-length path
     assert _create(3, 1, 16, [("identity",)] * 3)[0] in (mci.MCI_E_SIZE, mci.MCI_E_BAND)
     assert _create(0, 32, 256, f)[0] == mci.MCI_E_ARG
     assert _create(2, 32, 256, f, dtype=7)[0] == mci.MCI_E_ARG

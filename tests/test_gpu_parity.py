@@ -334,3 +334,74 @@ def test_row_kernel_vs_oracle_and_generic(L, rows, qtab, variant, monkeypatch):
     # a single row computed alone gives the same bits
     one = run_plan(plan, g[-1:])
     assert np.array_equal(one[0], out[-1])
+
+
+# -------------------------------------------------------------------------- NEXT-1: arbitrary lengths
+# the paper's SISR widths (107 prime, 120,
+# 160, 166 = 2 x 83, 170 = 2 x 5 x 17; L = 3 N = M N for the (f, f', f'') bank, so
+# the output grid is exactly the band size) and odd symmetric bands (M N odd).
+@pytest.mark.parametrize("N", [107, 120, 166, 170])
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_anylen_sisr_widths(N, dtype):
+    m = mci()
+    M, L = 3, 3 * N
+    bank = BANKS["f_df_ddf"]
+    rng = np.random.default_rng(N)
+    g = rng.standard_normal((5, M, N)) * np.array([1.0, N / 4.0, (N / 4.0) ** 2])[None, :, None]
+    plan = m.Plan(M, N, L, bank, dtype=dtype)
+    tt = torch.float32 if dtype == "f32" else torch.float64
+    out = run_plan(plan, g.astype(np.float32 if dtype == "f32" else np.float64), dtype=tt)
+    P = oracle.OraclePlan(M, N, L, bank)
+    ref = P.eval(g.astype(np.float32).astype(np.float64) if dtype == "f32" else g)
+    tol = F32_TOL if dtype == "f32" else F64_TOL
+    assert row_rel(out, ref).max() < tol
+
+
+@pytest.mark.parametrize("M,N,L,bank_name,hilbert", [
+    (1, 33, 99, "f", False),         # odd band, plain trigonometric interpolation
+    (2, 45, 180, "f_df", True),      # odd N, even band, analytic output
+    (2, 100, 1000, "f_df", False),   # L = 10 N (radices 4, 5, 2)
+    (3, 49, 196, "f_df_ddf", True),  # radix 7, odd band, Hilbert
+    (2, 1000, 4000, "f_df", True),   # larger, several passes
+    (2, 97, 194, "f_hf", False),     # Hilbert-channel bank, prime N
+])
+def test_anylen_shapes_vs_oracle(M, N, L, bank_name, hilbert):
+    m = mci()
+    bank = BANKS[bank_name]
+    g = np.random.default_rng(N + L).standard_normal((3, M, N)).astype(np.float32)
+    plan = m.Plan(M, N, L, bank, hilbert=hilbert)
+    res = run_plan(plan, g)
+    P = oracle.OraclePlan(M, N, L, bank)
+    f = res[0] if hilbert else res
+    assert row_rel(f, P.eval(g)).max() < F32_TOL
+    if hilbert:
+        assert row_rel(res[1], P.eval(g, hilbert=True)).max() < F32_TOL
+
+
+def test_anylen_forced_matches_fused(monkeypatch):
+    """Power-of-two shapes forced through the arbitrary-length kernel agree with the
+    specialised / generic fused kernels (and batch-size independence)."""
+    m = mci()
+    g = np.random.default_rng(9).standard_normal((40, 2, 256)).astype(np.float32)
+    ref = run_plan(m.Plan(2, 256, 2048, BANKS["f_df"]), g)
+    monkeypatch.setenv("MCI_FORCE_ANYLEN", "1")
+    out = run_plan(m.Plan(2, 256, 2048, BANKS["f_df"]), g)
+    assert row_rel(out, ref).max() < F32_TOL
+    one = run_plan(m.Plan(2, 256, 2048, BANKS["f_df"]), g[-1:])
+    assert np.array_equal(one[0], out[-1])
+
+
+def test_anylen_2d_vs_oracle():
+    """Separable 2D with non-power-of-two image sizes (both passes on the
+    arbitrary-length kernel, strided sample axis)."""
+    m = mci()
+    Nx, Ny, scale = 40, 36, 3
+    bank = BANKS["f_df"]
+    g = np.random.default_rng(12).standard_normal((2, 2, 2, Ny, Nx)).astype(np.float32)
+    plan = m.Plan2D(2, Nx, bank, 2, Ny, bank, scale)
+    out = plan.execute(torch.from_numpy(g).cuda()).double().cpu().numpy()
+    px = oracle.OraclePlan(2, Nx, Nx * scale, bank)
+    py = oracle.OraclePlan(2, Ny, Ny * scale, bank)
+    for i in range(2):
+        ref = oracle.eval_2d(g[i], px, py)
+        assert np.linalg.norm(out[i] - ref) / np.linalg.norm(ref) < F32_TOL
