@@ -6,7 +6,7 @@ M=3 channels (f, f', f''), N=1024 samples each -> L=16384 outputs, fp32.
 A step is one pass of the whole hot path (forward DFTs, per-class solves,
 assembly, inverse FFTs, stores) over the batch, i.e. one mci_execute_1d.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl mci|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..6] [--impl mci|reference]
 
 N > 1: one process per GPU (torchrun), each rank runs its own batch (rows are
 independent: weak scaling, no collective on the data path); time = max over
@@ -53,7 +53,7 @@ def workload(cfg):
                     out_floats_per_unit=c["size"] ** 2)
     M, N, L, B = c["M"], c["N"], c["L"], c["batch"]
     nout = 2 if c.get("hilbert") else 1
-    bank = {1: "1, ik", 2: "1, ik, -k^2", 3: "1, ik (+Hf)", 4: "delays 2 pi m/(4N)"}[cfg]
+    bank = {1: "1, ik", 2: "1, ik, -k^2", 3: "1, ik (+Hf)", 4: "delays 2 pi m/(4N)", 6: "1, ik, -k^2 (NEXT-1, odd band)"}[cfg]
     return dict(name=f"cfg{cfg}: {B} x (M={M}, N={N}) -> L={L} x {nout} out, bank {bank}",
                 units=B, outs_per_unit=L * nout, in_per_unit=M * N, out_floats_per_unit=L * nout)
 
@@ -69,6 +69,8 @@ def make_inputs(cfg, rank):
         return synth.cfg3_rows(np.arange(c["batch"]), seed=3 + 1000 * rank)
     if cfg == 4:
         return synth.cfg4_signals(np.arange(c["batch"]), seed=4 + 1000 * rank)[0]
+    if cfg == 6:
+        return synth.cfg2_batch_fast(c["batch"], seed=6 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
     # cfg5: generate a few distinct images and tile them to the batch (content does not
     # change the arithmetic or the bytes; generation of 64 2048^2 images would dominate)
     distinct = 4
@@ -216,6 +218,9 @@ def make_row(cfg, r):
         return synth.cfg1()["g"]
     if cfg == 2:
         return synth.cfg2_rows([r])
+    if cfg == 6:
+        c = synth.CONFIGS[6]
+        return synth.cfg2_batch_fast(256, seed=6, M=c["M"], N=c["N"], bank=c["bank"])[r % 256][None]
     return synth.cfg3_rows([r])
 
 
@@ -227,8 +232,8 @@ def run_reference(args, rank, world):
     c = synth.CONFIGS[cfg]
     w = workload(cfg)
     threads = os.cpu_count() or 1
-    # each step = one row (cfg1-3), 64 points (cfg4) or 4 columns (cfg5) of the workload
-    if cfg in (1, 2, 3):
+    # each step = one row (cfg1-3, 6), 64 points (cfg4) or 4 columns (cfg5) of the workload
+    if cfg in (1, 2, 3, 6):
         P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
         P.kernel_table()
         if c.get("hilbert"):
@@ -292,7 +297,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6])
     ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -369,11 +374,11 @@ def main():
     peak, peak_src = load_peaks()
     launches = plan.launches(units)
     alg_bytes = units * (w["in_per_unit"] + w["out_floats_per_unit"]) * esz
-    per_launch_ms = ms_step / launches if cfg in (1, 2, 3) else ms_step
-    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9 if cfg in (1, 2, 3) else alg_bytes / (ms_step / 1e3) / 1e9
+    per_launch_ms = ms_step / launches if cfg in (1, 2, 3, 6) else ms_step
+    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9 if cfg in (1, 2, 3, 6) else alg_bytes / (ms_step / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": load_traffic(w["name"]), "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": alg_bytes if cfg in (1, 2, 3) else None,
+            "algorithmic_bytes_per_launch": alg_bytes if cfg in (1, 2, 3, 6) else None,
             "algorithmic_bytes_per_step": alg_bytes}
     # secondary ceiling: the FP32 pipe.  Algorithmic flops per unit =
     # SURVEY.md §8(d) counts (2.5 n log2 n per real FFT, 5 n log2 n complex, 8 M^2 per class).

@@ -14,9 +14,12 @@
 //   inverse DFT of length L of Xf placed at k mod L (the k = +-L/2 pair of an even
 //   band with L = MN folds onto one bin) -> real f; for Hf the one-sided spectrum
 //   Z(0) = Xf(0), Z(k) = 2 Xf(k) (Example 4) gives z = f + i Hf.
-// FFTs: runtime mixed-radix Stockham passes in shared memory (radix 4, 2, 3, 5 and 7
-// codelets; any other prime factor p as a direct p-point pass parallel over its
-// outputs), twiddles from the plan's fp64-rounded root tables.  One CTA per row.
+// FFTs: runtime mixed-radix Stockham passes in shared memory (compile-time radix 4, 2,
+// 3, 5 and 7 codelets; any other prime factor p as a direct p-point pass parallel over
+// its outputs, root index advanced without division), root tables (fp64-rounded) and
+// Q~ staged in shared memory.  A warp owns a row (8 rows per CTA, warp-synchronous)
+// when its working set is small, else a 256-thread CTA does.
+#include <algorithm>
 #include <cstdint>
 
 #include "mci_fft.cuh"
@@ -34,6 +37,7 @@ template <typename T> struct AnyArgs {
     const cv<T> *Q;    // [N][M][M]  H_{j_q}^{-1}[m][l] / N for every class q
     const cv<T> *twN;  // [N] e^{-2 pi i m / N}
     const cv<T> *twL;  // [L] e^{+2 pi i m / L}
+    int qsm;           // Q~ copied to shared memory (else read through L1)
 };
 
 namespace anyk {
@@ -42,77 +46,139 @@ template <typename V> __device__ __forceinline__ V crot(V a, int s) {  // a * (s
     return s > 0 ? V{-a.y, a.x} : V{a.y, -a.x};
 }
 
-// one Stockham pass of radix r over `cnt` transforms of length n stored with stride n:
-// butterfly b in [0, n/r), k = b mod Ls: x_j = in[b + j n/r] * w^{j k}, w = root^(n/(Ls r)),
-// out[(b - k) r + k + j Ls] = DFT_r(x)_j.  `root(m)` = e^{s 2 pi i m / n}.
-template <typename T, int NT>
-__device__ void stockham_pass(const cv<T> *in, cv<T> *out, int n, int cnt, int r, int Ls, int s, const cv<T> *root) {
+// Row group of G threads: one warp (G = 32, warp-synchronous) or the whole CTA.
+template <int G> __device__ __forceinline__ void gsync() {
+    if constexpr (G == 32) __syncwarp();
+    else __syncthreads();
+}
+
+// in-register DFT of compile-time size R in {2, 3, 4, 5, 7}; w_R^m = root[m nb] (root table of the
+// transform, e^{s 2 pi i m / n}, nb = n / R) for the 5- and 7-point kernels
+template <typename T, int R>
+__device__ __forceinline__ void dft_small(cv<T> *x, int s, const cv<T> *root, int nb) {
     using V = cv<T>;
-    const int nb = n / r, tws = n / (Ls * r);
-    if (r <= 7 && r != 6) {
-        for (int idx = threadIdx.x; idx < cnt * nb; idx += NT) {
-            const int c = idx / nb, b = idx - c * nb, k = b % Ls;
-            const V *src = in + (int64_t)c * n;
-            V *dst = out + (int64_t)c * n;
-            V x[7];
-            for (int j = 0; j < r; ++j) {
-                V v = src[b + j * nb];
-                if (j && k) v = cmul(v, __ldg(root + (int64_t)j * k * tws % n));
-                x[j] = v;
-            }
-            V y[7];
-            if (r == 2) {
-                y[0] = cadd(x[0], x[1]);
-                y[1] = csub(x[0], x[1]);
-            } else if (r == 4) {
-                const V t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]), t2 = cadd(x[1], x[3]), t3 = csub(x[1], x[3]);
-                y[0] = cadd(t0, t2);
-                y[2] = csub(t0, t2);
-                y[1] = cadd(t1, crot(t3, s));
-                y[3] = csub(t1, crot(t3, s));
-            } else if (r == 3) {
-                const T h = (T)0.86602540378443864676;  // sqrt(3)/2
-                const V t1 = cadd(x[1], x[2]);
-                const V t2 = V{x[0].x - (T)0.5 * t1.x, x[0].y - (T)0.5 * t1.y};
-                const V t3 = cscale(crot(csub(x[1], x[2]), s), h);
-                y[0] = cadd(x[0], t1);
-                y[1] = cadd(t2, t3);
-                y[2] = csub(t2, t3);
-            } else if (r == 1) {
-                y[0] = x[0];
-            } else {  // 5, 7: direct with the root table, w_r^{jm} = root(j m n / r)
-                for (int m = 0; m < r; ++m) {
-                    V acc = x[0];
-                    for (int j = 1; j < r; ++j) acc = cadd(acc, cmul(x[j], __ldg(root + (int64_t)((j * m) % r) * nb)));
-                    y[m] = acc;
-                }
-            }
-            for (int j = 0; j < r; ++j) dst[(b - k) * r + k + j * Ls] = y[j];
+    if constexpr (R == 2) {
+        const V t = x[0];
+        x[0] = cadd(t, x[1]);
+        x[1] = csub(t, x[1]);
+    } else if constexpr (R == 4) {
+        const V t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]), t2 = cadd(x[1], x[3]), t3 = csub(x[1], x[3]);
+        x[0] = cadd(t0, t2);
+        x[2] = csub(t0, t2);
+        x[1] = cadd(t1, crot(t3, s));
+        x[3] = csub(t1, crot(t3, s));
+    } else if constexpr (R == 3) {
+        const T h = (T)0.86602540378443864676;  // sqrt(3)/2
+        const V t1 = cadd(x[1], x[2]);
+        const V t2 = V{x[0].x - (T)0.5 * t1.x, x[0].y - (T)0.5 * t1.y};
+        const V t3 = cscale(crot(csub(x[1], x[2]), s), h);
+        x[0] = cadd(x[0], t1);
+        x[1] = cadd(t2, t3);
+        x[2] = csub(t2, t3);
+    } else {
+        V w[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) w[m] = root[m * nb];
+        V y[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) {
+            V acc = x[0];
+#pragma unroll
+            for (int j = 1; j < R; ++j) acc = cadd(acc, cmul(x[j], w[(j * m) % R]));
+            y[m] = acc;
         }
-    } else {  // any other radix: direct r-point pass, parallel over (butterfly, output)
-        for (int idx = threadIdx.x; idx < cnt * n; idx += NT) {
-            const int c = idx / n, rem = idx - c * n, b = rem / r, m = rem - b * r, k = b % Ls;
-            const V *src = in + (int64_t)c * n;
-            V acc = V{0, 0};
-            for (int j = 0; j < r; ++j) {
-                V v = src[b + j * nb];
-                // twiddle w^{j k} times the DFT kernel w_r^{j m}: one root of index (j (k tws + m nb)) mod n
-                const int64_t e = ((int64_t)j * ((int64_t)k * tws + (int64_t)m * nb)) % n;
-                acc = cadd(acc, cmul(v, __ldg(root + e)));
-            }
-            out[(int64_t)c * n + (b - k) * r + k + m * Ls] = acc;
-        }
+#pragma unroll
+        for (int m = 0; m < R; ++m) x[m] = y[m];
     }
 }
 
-// full transform: returns the buffer holding the result (a or b)
-template <typename T, int NT>
-__device__ cv<T> *fft_any(cv<T> *a, cv<T> *b, int n, int cnt, const AnyRadix &pl, int s, const cv<T> *root) {
+// one Stockham pass of radix R over `cnt` transforms of length n stored with stride n:
+// butterfly b in [0, n/R), k = b mod Ls: x_j = in[b + j n/R] w^{j k}, w = root^(n/(Ls R)),
+// out[(b - k) R + k + j Ls] = DFT_R(x)_j.  root(m) = e^{s 2 pi i m / n} (shared memory).
+template <typename T, int R, int G>
+__device__ __forceinline__ void pass_r(const cv<T> *in, cv<T> *out, int n, int cnt, int Ls, int s, const cv<T> *root,
+                                       int lane) {
+    using V = cv<T>;
+    const int nb = n / R, tws = n / (Ls * R);
+    for (int idx = lane; idx < cnt * nb; idx += G) {
+        const int c = idx / nb, b = idx - c * nb, k = b % Ls;
+        const V *src = in + c * n;
+        V x[R];
+        const int d = k * tws;  // < n
+        int e = 0;
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            x[j] = src[b + j * nb];
+            if (j) {
+                e += d;
+                if (e >= n) e -= n;
+                if (k) x[j] = cmul(x[j], root[e]);
+            }
+        }
+        dft_small<T, R>(x, s, root, nb);
+        V *dst = out + c * n + (b - k) * R + k;
+#pragma unroll
+        for (int j = 0; j < R; ++j) dst[j * Ls] = x[j];
+    }
+}
+
+// any other (prime) radix r: direct r-point pass.  A thread computes U consecutive outputs
+// m0 .. m0+U-1 of one butterfly, so each input is loaded once for U outputs: the kernel
+// root of output m0 + t is W^{j d} (W^{j nb})^t with d = k tws + m0 nb (the twiddle w^{jk}
+// and the DFT kernel w_r^{j m} combined, index advanced without division), i.e. one table
+// load and U - 1 multiplications per input instead of U loads (the pass is bound by
+// shared-memory bandwidth).
+template <typename T, int G>
+__device__ void pass_direct(const cv<T> *in, cv<T> *out, int n, int cnt, int r, int Ls, const cv<T> *root, int lane) {
+    using V = cv<T>;
+    constexpr int U = 4;
+    const int nb = n / r, tws = n / (Ls * r), mbk = (r + U - 1) / U;
+    for (int idx = lane; idx < cnt * nb * mbk; idx += G) {
+        const int c = idx / (nb * mbk), rem = idx - c * (nb * mbk), b = rem / mbk, m0 = (rem - b * mbk) * U,
+                  k = b % Ls;
+        const V *src = in + c * n + b;
+        int d = k * tws + m0 * nb;  // < 2 n
+        if (d >= n) d -= n;
+        V acc[U];
+#pragma unroll
+        for (int t = 0; t < U; ++t) acc[t] = src[0];
+        int e = 0, f = 0;  // e = j d mod n, f = j nb mod n
+        for (int j = 1; j < r; ++j) {
+            e += d;
+            if (e >= n) e -= n;
+            f += nb;
+            if (f >= n) f -= n;
+            const V x = src[j * nb], st = root[f];
+            V w = root[e];
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                acc[t] = cadd(acc[t], cmul(x, w));
+                if (t + 1 < U) w = cmul(w, st);
+            }
+        }
+        V *dst = out + c * n + (b - k) * r + k;
+#pragma unroll
+        for (int t = 0; t < U; ++t)
+            if (m0 + t < r) dst[(m0 + t) * Ls] = acc[t];
+    }
+}
+
+// full transform; returns the buffer holding the result (a or b)
+template <typename T, int G>
+__device__ cv<T> *fft_any(cv<T> *a, cv<T> *b, int n, int cnt, const AnyRadix &pl, int s, const cv<T> *root, int lane) {
     int Ls = 1;
     for (int i = 0; i < pl.n; ++i) {
-        stockham_pass<T, NT>(a, b, n, cnt, pl.r[i], Ls, s, root);
-        __syncthreads();
-        Ls *= pl.r[i];
+        const int r = pl.r[i];
+        switch (r) {
+        case 2: pass_r<T, 2, G>(a, b, n, cnt, Ls, s, root, lane); break;
+        case 3: pass_r<T, 3, G>(a, b, n, cnt, Ls, s, root, lane); break;
+        case 4: pass_r<T, 4, G>(a, b, n, cnt, Ls, s, root, lane); break;
+        case 5: pass_r<T, 5, G>(a, b, n, cnt, Ls, s, root, lane); break;
+        case 7: pass_r<T, 7, G>(a, b, n, cnt, Ls, s, root, lane); break;
+        default: pass_direct<T, G>(a, b, n, cnt, r, Ls, root, lane); break;
+        }
+        gsync<G>();
+        Ls *= r;
         cv<T> *t = a;
         a = b;
         b = t;
@@ -120,38 +186,59 @@ __device__ cv<T> *fft_any(cv<T> *a, cv<T> *b, int n, int cnt, const AnyRadix &pl
     return a;
 }
 
+template <typename T, int G> __device__ __forceinline__ T group_max(T v, T *red) {
+    if constexpr (G == 32) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    } else {
+        return block_max<G>(v, red);
+    }
+}
+
 }  // namespace anyk
 
-template <typename T, int NT>
-__global__ void __launch_bounds__(NT) mci_anylen_kernel(const AnyArgs<T> a) {
+// smem layout: [twN: N][twL: L][Q~: N M M if qsm] then per group [b0: bl][b1: bl][A: MN]
+template <typename T, int G, int GPB>
+__global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a) {
     using V = cv<T>;
     using namespace anyk;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, N = a.N, L = a.L, MN = a.MN, K1 = a.K1, Kmax = a.Kmax;
     const int npair = (M + 1) / 2;
     const int bl = max(npair * N, L);
-    V *b0 = reinterpret_cast<V *>(smem_raw);
+    V *twN = reinterpret_cast<V *>(smem_raw);
+    V *twL = twN + N;
+    V *Qs = twL + L;
+    const int qn = a.qsm ? N * M * M : 0;
+    const int grp = threadIdx.x / G, lane = threadIdx.x % G;
+    V *b0 = Qs + qn + (size_t)grp * (2 * bl + MN);
     V *b1 = b0 + bl;
     V *A = b1 + bl;  // a(k), k = K1 .. K1 + MN - 1
-    __shared__ T red[NT / 32];
-    __shared__ int escale[8];
-    const int tid = threadIdx.x;
-    for (int64_t row = blockIdx.x; row < a.rows; row += gridDim.x) {
+    for (int i = threadIdx.x; i < N; i += G * GPB) twN[i] = a.twN[i];
+    for (int i = threadIdx.x; i < L; i += G * GPB) twL[i] = a.twL[i];
+    for (int i = threadIdx.x; i < qn; i += G * GPB) Qs[i] = a.Q[i];
+    const V *Qt = a.qsm ? Qs : a.Q;
+    __shared__ T red[(G > 32 ? G : 32) / 32];
+    __shared__ int escale_s[GPB][8];
+    int *escale = escale_s[grp];
+    __syncthreads();
+    for (int64_t row = (int64_t)blockIdx.x * GPB + grp; row < a.rows; row += (int64_t)gridDim.x * GPB) {
         const RowAddr &ra = a.ra;
         const int64_t base = (row / (ra.D0 * ra.D1)) * ra.s2 + ((row / ra.D0) % ra.D1) * ra.s1 + (row % ra.D0) * ra.s0;
         // ---- load channel pairs z_c = g_{2c} + i g_{2c+1}, per-channel exact power-of-two scaling
         for (int c = 0; c < npair; ++c) {
             T m0 = 0, m1 = 0;
-            for (int n = tid; n < N; n += NT) {
+            for (int n = lane; n < N; n += G) {
                 const T re = __ldg(a.g + base + (int64_t)(2 * c) * ra.cs + (int64_t)n * ra.ss);
                 const T im = (2 * c + 1 < M) ? __ldg(a.g + base + (int64_t)(2 * c + 1) * ra.cs + (int64_t)n * ra.ss) : T(0);
                 b0[c * N + n] = V{re, im};
                 m0 = fmax(m0, fabs(re));
                 m1 = fmax(m1, fabs(im));
             }
-            m0 = block_max<NT>(m0, red);
-            m1 = block_max<NT>(m1, red);
-            if (tid == 0) {
+            m0 = group_max<T, G>(m0, red);
+            m1 = group_max<T, G>(m1, red);
+            if (lane == 0) {
                 int e0 = 0, e1 = 0;
                 if (m0 > 0) frexp(m0, &e0);
                 if (m1 > 0) frexp(m1, &e1);
@@ -159,19 +246,22 @@ __global__ void __launch_bounds__(NT) mci_anylen_kernel(const AnyArgs<T> a) {
                 escale[2 * c + 1] = e1;
             }
         }
-        __syncthreads();
-        for (int idx = tid; idx < npair * N; idx += NT) {
+        gsync<G>();
+        for (int idx = lane; idx < npair * N; idx += G) {
             const int c = idx / N;
             const V z = b0[idx];
             b0[idx] = V{ldexp(z.x, -escale[2 * c]), ldexp(z.y, -escale[2 * c + 1])};
         }
-        __syncthreads();
+        gsync<G>();
         // ---- forward DFTs G_c[q] = sum_n z_c[n] e^{-2 pi i q n / N}
-        V *Z = fft_any<T, NT>(b0, b1, N, npair, a.rn, -1, a.twN);
+        V *Z = fft_any<T, G>(b0, b1, N, npair, a.rn, -1, twN, lane);
         // ---- per-class solve for every class q: a(j_q + l N), j_q = K1 + ((q - K1) mod N)
-        for (int q = tid; q < N; q += NT) {
+        const int q0 = (int)((((int64_t)-K1) % N + N) % N);  // (q - K1) mod N = (q + q0) mod N
+        for (int q = lane; q < N; q += G) {
             const int qm = q == 0 ? 0 : N - q;
-            const int jq = K1 + (int)((((int64_t)q - K1) % N + N) % N);
+            int t = q + q0;
+            if (t >= N) t -= N;
+            const int jq = K1 + t;
             V v[8];
 #pragma unroll
             for (int l = 0; l < 8; ++l) v[l] = V{0, 0};
@@ -180,12 +270,16 @@ __global__ void __launch_bounds__(NT) mci_anylen_kernel(const AnyArgs<T> a) {
                 V gm = (m & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}  // (zc - zm) / (2i)
                                : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};  // (zc + zm) / 2
                 gm = V{ldexp(gm.x, escale[m]), ldexp(gm.y, escale[m])};
-                const V *qrow = a.Q + ((int64_t)q * M + m) * M;
-                for (int l = 0; l < M; ++l) v[l] = cadd(v[l], cmul(gm, __ldg(qrow + l)));
+                const V *qrow = Qt + ((int64_t)q * M + m) * M;
+#pragma unroll
+                for (int l = 0; l < 8; ++l)
+                    if (l < M) v[l] = cadd(v[l], cmul(gm, qrow[l]));
             }
-            for (int l = 0; l < M; ++l) A[jq + l * N - K1] = v[l];
+#pragma unroll
+            for (int l = 0; l < 8; ++l)
+                if (l < M) A[jq + l * N - K1] = v[l];
         }
-        __syncthreads();
+        gsync<G>();
         // ---- inverse input: bin i of the length-L transform
         //      real:     sum over k = i (mod L), |k| <= Kmax, of Xf(k) = (a(k) + conj a(-k)) / 2
         //      analytic: Xf(0) at i = 0, 2 Xf(i) for 0 < i <= Kmax
@@ -194,7 +288,7 @@ __global__ void __launch_bounds__(NT) mci_anylen_kernel(const AnyArgs<T> a) {
             const V p = af(k), m = cconj(af(-k));
             return V{(T)0.5 * (p.x + m.x), (T)0.5 * (p.y + m.y)};
         };
-        for (int i = tid; i < L; i += NT) {
+        for (int i = lane; i < L; i += G) {
             V z = V{0, 0};
             if (!a.analytic) {
                 if (i <= Kmax) z = xf(i);
@@ -205,34 +299,41 @@ __global__ void __launch_bounds__(NT) mci_anylen_kernel(const AnyArgs<T> a) {
             }
             b0[i] = z;
         }
-        __syncthreads();
-        V *out = fft_any<T, NT>(b0, b1, L, 1, a.rl, +1, a.twL);
+        gsync<G>();
+        V *out = fft_any<T, G>(b0, b1, L, 1, a.rl, +1, twL, lane);
         T *frow = a.f + row * (int64_t)L;
         T *hrow = a.analytic ? a.hf + row * (int64_t)L : nullptr;
-        for (int p = tid; p < L; p += NT) {
+        for (int p = lane; p < L; p += G) {
             const V z = out[p];
             frow[p] = z.x;
             if (hrow) hrow[p] = z.y;
         }
-        __syncthreads();
+        gsync<G>();
     }
 }
 
-size_t anylen_smem_bytes(const Axis1D &ax) {
-    const size_t vs = ax.dtype == MCI_F64 ? 16 : 8;
+// shared memory: root tables + Q~ (if small) + per row group [2 bl + MN] complex values
+static size_t group_elems(const Axis1D &ax) {
     const int64_t npair = (ax.M + 1) / 2;
-    const int64_t bl = std::max<int64_t>(npair * ax.N, ax.L);
-    return (size_t)(2 * bl + (int64_t)ax.M * ax.N) * vs;
+    return (size_t)(2 * std::max<int64_t>(npair * ax.N, ax.L) + (int64_t)ax.M * ax.N);
 }
+static bool q_in_smem(const Axis1D &ax) { return ax.N * ax.M * ax.M <= 4096; }
+static size_t smem_for(const Axis1D &ax, int groups) {
+    const size_t vs = ax.dtype == MCI_F64 ? 16 : 8;
+    return (size_t)(ax.N + ax.L + (q_in_smem(ax) ? ax.N * ax.M * ax.M : 0) + groups * group_elems(ax)) * vs;
+}
+// warp per row (8 rows per CTA) when a row's working set is small, else one 256-thread CTA per row
+static bool warp_rows(const Axis1D &ax) { return smem_for(ax, 8) <= 96 * 1024; }
+
+size_t anylen_smem_bytes(const Axis1D &ax) { return warp_rows(ax) ? smem_for(ax, 8) : smem_for(ax, 1); }
 
 bool anylen_supported(const Axis1D &ax) {
     return ax.M <= 8 && ax.N <= 65536 && ax.L <= (1 << 22) && anylen_smem_bytes(ax) <= 200 * 1024;
 }
 
-template <typename T>
+template <typename T, int G, int GPB>
 static cudaError_t anylen_launch_t(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                                    cudaStream_t st) {
-    constexpr int NT = 256;
     AnyArgs<T> a;
     a.M = ax.M; a.N = (int)ax.N; a.L = (int)ax.L; a.MN = (int)(ax.M * ax.N);
     a.K1 = (int)ax.K1; a.Kmax = (int)(-ax.K1); a.analytic = ax.analytic;
@@ -242,17 +343,19 @@ static cudaError_t anylen_launch_t(const Axis1D &ax, const RowAddr &ra, int64_t 
     a.Q = (const cv<T> *)ax.Qt;
     a.twN = (const cv<T> *)ax.twF;
     a.twL = (const cv<T> *)ax.twLhi;
-    const size_t smem = anylen_smem_bytes(ax);
-    auto kern = mci_anylen_kernel<T, NT>;
+    a.qsm = q_in_smem(ax) ? 1 : 0;
+    const size_t smem = smem_for(ax, GPB);
+    auto kern = mci_anylen_kernel<T, G, GPB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G * GPB, smem);
     int64_t grid = (int64_t)nsm * (occ < 1 ? 1 : occ);
-    if (grid > rows) grid = rows;
-    kern<<<(unsigned)grid, NT, smem, st>>>(a);
+    const int64_t need = (rows + GPB - 1) / GPB;
+    if (grid > need) grid = need;
+    kern<<<(unsigned)grid, G * GPB, smem, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -260,8 +363,11 @@ cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, con
                           cudaStream_t st, int *n_launches) {
     if (rows <= 0) return cudaSuccess;
     if (n_launches) *n_launches += 1;
-    return ax.dtype == MCI_F64 ? anylen_launch_t<double>(ax, ra, rows, g, f, hf, st)
-                               : anylen_launch_t<float>(ax, ra, rows, g, f, hf, st);
+    if (warp_rows(ax))
+        return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 8>(ax, ra, rows, g, f, hf, st)
+                                   : anylen_launch_t<float, 32, 8>(ax, ra, rows, g, f, hf, st);
+    return ax.dtype == MCI_F64 ? anylen_launch_t<double, 256, 1>(ax, ra, rows, g, f, hf, st)
+                               : anylen_launch_t<float, 256, 1>(ax, ra, rows, g, f, hf, st);
 }
 
 }  // namespace mci

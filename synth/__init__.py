@@ -158,6 +158,10 @@ CONFIGS = {
             bank=[("delay", 2 * math.pi * m / (4 * 262144)) for m in range(4)], dtype="f32"),
     5: dict(Mx=2, My=2, N=512, scale=4, batch=64, size=2048,
             bank=[("identity",), ("derivative", 1)], dtype="f32"),
+    # SURVEY.md §8(f) NEXT-1 measurement line: the paper's prime SISR width (PAPER.md:896-931,
+    # 321 / 3 = 107) with the (f, f', f'') bank, L = 3N = MN (odd band, odd output length)
+    6: dict(M=3, N=107, L=321, batch=65536,
+            bank=[("identity",), ("derivative", 1), ("derivative", 2)], dtype="f32"),
 }
 
 

@@ -405,3 +405,22 @@ def test_anylen_2d_vs_oracle():
     for i in range(2):
         ref = oracle.eval_2d(g[i], px, py)
         assert np.linalg.norm(out[i] - ref) / np.linalg.norm(ref) < F32_TOL
+
+
+def test_cfg6_full_batch_sampled():
+    """Config 6 (NEXT-1 measurement line: 65,536 rows, M=3, N=107, L=321, odd band) in
+    the bench launch: sampled rows vs the oracle, every row consistent at the coarse
+    sites (f(t_n) = g_0[n], PAPER.md:546-585)."""
+    m = mci()
+    c = synth.CONFIGS[6]
+    g = synth.cfg2_batch_fast(c["batch"], seed=6, M=c["M"], N=c["N"], bank=c["bank"])
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"])
+    gt = torch.from_numpy(g).cuda()
+    f = plan.execute(gt)
+    torch.cuda.synchronize()
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    pick = [0, 12345, c["batch"] - 1]
+    out = f[pick].double().cpu().numpy()
+    assert row_rel(out, P.eval(g[pick])).max() < F32_TOL
+    err = (f[:, :: c["L"] // c["N"]] - gt[:, 0]).abs().max().item()
+    assert err < 2e-5 * gt[:, 0].abs().max().item()
