@@ -15,8 +15,9 @@
 //   band with L = MN folds onto one bin) -> real f; for Hf the one-sided spectrum
 //   Z(0) = Xf(0), Z(k) = 2 Xf(k) (Example 4) gives z = f + i Hf.
 // FFTs: runtime mixed-radix Stockham passes in shared memory (compile-time radix 4, 2,
-// 3, 5 and 7 codelets; any other prime factor p as a direct p-point pass parallel over
-// its outputs, root index advanced without division), root tables (fp64-rounded) and
+// 3, 5 and 7 codelets; the largest prime factor p > 16 by Bluestein's chirp-z transform
+// through two power-of-two FFTs of length M >= 2p - 1; other primes as a direct p-point
+// pass parallel over its outputs, root index advanced without division), root tables (fp64-rounded) and
 // Q~ staged in shared memory.  A warp owns a row (8 rows per CTA, warp-synchronous)
 // when its working set is small, else a 256-thread CTA does.
 #include <algorithm>
@@ -163,12 +164,78 @@ __device__ void pass_direct(const cv<T> *in, cv<T> *out, int n, int cnt, int r, 
     }
 }
 
+// Bluestein (chirp-z) state of one transform: tables and the group's two M-point buffers
+template <typename T> struct Blue {
+    int p = 0, M = 0;
+    const cv<T> *c, *H, *wm, *wp;  // chirp [p], H^ [M] (1/M folded in), e^{-2 pi i m/M}, e^{+2 pi i m/M}
+    cv<T> *t0, *t1;
+};
+
+template <typename T, int G>
+__device__ cv<T> *fft_pow2(cv<T> *a, cv<T> *b, int n, int s, const cv<T> *root, int lane) {
+    int Ls = 1;
+    while (Ls < n) {
+        if (n / Ls >= 4) {
+            pass_r<T, 4, G>(a, b, n, 1, Ls, s, root, lane);
+            Ls *= 4;
+        } else {
+            pass_r<T, 2, G>(a, b, n, 1, Ls, s, root, lane);
+            Ls *= 2;
+        }
+        gsync<G>();
+        cv<T> *t = a;
+        a = b;
+        b = t;
+    }
+    return a;
+}
+
+// radix-p pass by Bluestein: X_m = c_m (a (*) h)_m, a_j = x_j c_j (x twiddled), h = conj c,
+// as two M-point FFTs and a pointwise product with H^ = FFT(h)/M; butterflies one at a time
+template <typename T, int G>
+__device__ void pass_bluestein(const cv<T> *in, cv<T> *out, int n, int cnt, int Ls, const cv<T> *root, const Blue<T> &bl,
+                               int lane) {
+    using V = cv<T>;
+    const int p = bl.p, M = bl.M, nb = n / p, tws = n / (Ls * p);
+    for (int bf = 0; bf < cnt * nb; ++bf) {
+        const int c = bf / nb, b = bf - c * nb, k = b % Ls;
+        const V *src = in + c * n;
+        for (int i = lane; i < M; i += G) {
+            V v = V{0, 0};
+            if (i < p) {
+                v = src[b + i * nb];
+                if (k && i) v = cmul(v, root[(int)(((int64_t)i * k * tws) % n)]);
+                v = cmul(v, bl.c[i]);
+            }
+            bl.t0[i] = v;
+        }
+        gsync<G>();
+        V *R = fft_pow2<T, G>(bl.t0, bl.t1, M, -1, bl.wm, lane);
+        for (int i = lane; i < M; i += G) R[i] = cmul(R[i], bl.H[i]);
+        gsync<G>();
+        V *R2 = fft_pow2<T, G>(R, R == bl.t0 ? bl.t1 : bl.t0, M, +1, bl.wp, lane);
+        V *dst = out + c * n + (b - k) * p + k;
+        for (int m = lane; m < p; m += G) dst[m * Ls] = cmul(R2[m], bl.c[m]);
+        gsync<G>();
+    }
+}
+
 // full transform; returns the buffer holding the result (a or b)
 template <typename T, int G>
-__device__ cv<T> *fft_any(cv<T> *a, cv<T> *b, int n, int cnt, const AnyRadix &pl, int s, const cv<T> *root, int lane) {
+__device__ cv<T> *fft_any(cv<T> *a, cv<T> *b, int n, int cnt, const AnyRadix &pl, int s, const cv<T> *root,
+                          const Blue<T> &bl, int lane) {
     int Ls = 1;
     for (int i = 0; i < pl.n; ++i) {
         const int r = pl.r[i];
+        if (r == bl.p) {
+            pass_bluestein<T, G>(a, b, n, cnt, Ls, root, bl, lane);
+            gsync<G>();
+            Ls *= r;
+            cv<T> *t = a;
+            a = b;
+            b = t;
+            continue;
+        }
         switch (r) {
         case 2: pass_r<T, 2, G>(a, b, n, cnt, Ls, s, root, lane); break;
         case 3: pass_r<T, 3, G>(a, b, n, cnt, Ls, s, root, lane); break;
@@ -198,7 +265,8 @@ template <typename T, int G> __device__ __forceinline__ T group_max(T v, T *red)
 
 }  // namespace anyk
 
-// smem layout: [twN: N][twL: L][Q~: N M M if qsm] then per group [b0: bl][b1: bl][A: MN]
+// smem layout: [twN: N][twL: L][Q~: N M M if qsm][Bluestein tables N, L] then per group
+// [b0: bl][b1: bl][A: MN][t0: bM][t1: bM]
 template <typename T, int G, int GPB>
 __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a) {
     using V = cv<T>;
@@ -211,10 +279,32 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
     V *twL = twN + N;
     V *Qs = twL + L;
     const int qn = a.qsm ? N * M * M : 0;
+    V *btab = Qs + qn;
+    Blue<T> blN, blL;
+    const AnyRadix *rr[2] = {&a.rn, &a.rl};
+    Blue<T> *bb[2] = {&blN, &blL};
+    for (int t = 0; t < 2; ++t) {  // stage the Bluestein tables in shared memory
+        Blue<T> &q = *bb[t];
+        q.p = rr[t]->bp;
+        q.M = rr[t]->bM;
+        if (!q.p) continue;
+        V *c = btab, *H = c + q.p, *wm = H + q.M, *wp = wm + q.M;
+        for (int i = threadIdx.x; i < q.p; i += G * GPB) c[i] = ((const V *)rr[t]->bc)[i];
+        for (int i = threadIdx.x; i < q.M; i += G * GPB) {
+            H[i] = ((const V *)rr[t]->bH)[i];
+            wm[i] = ((const V *)rr[t]->bwm)[i];
+            wp[i] = ((const V *)rr[t]->bwp)[i];
+        }
+        q.c = c; q.H = H; q.wm = wm; q.wp = wp;
+        btab = wp + q.M;
+    }
+    const int bmx = max(blN.M, blL.M);
     const int grp = threadIdx.x / G, lane = threadIdx.x % G;
-    V *b0 = Qs + qn + (size_t)grp * (2 * bl + MN);
+    V *b0 = btab + (size_t)grp * (2 * bl + MN + 2 * bmx);
     V *b1 = b0 + bl;
     V *A = b1 + bl;  // a(k), k = K1 .. K1 + MN - 1
+    blN.t0 = blL.t0 = A + MN;
+    blN.t1 = blL.t1 = A + MN + bmx;
     for (int i = threadIdx.x; i < N; i += G * GPB) twN[i] = a.twN[i];
     for (int i = threadIdx.x; i < L; i += G * GPB) twL[i] = a.twL[i];
     for (int i = threadIdx.x; i < qn; i += G * GPB) Qs[i] = a.Q[i];
@@ -254,7 +344,7 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
         }
         gsync<G>();
         // ---- forward DFTs G_c[q] = sum_n z_c[n] e^{-2 pi i q n / N}
-        V *Z = fft_any<T, G>(b0, b1, N, npair, a.rn, -1, twN, lane);
+        V *Z = fft_any<T, G>(b0, b1, N, npair, a.rn, -1, twN, blN, lane);
         // ---- per-class solve for every class q: a(j_q + l N), j_q = K1 + ((q - K1) mod N)
         const int q0 = (int)((((int64_t)-K1) % N + N) % N);  // (q - K1) mod N = (q + q0) mod N
         for (int q = lane; q < N; q += G) {
@@ -300,7 +390,7 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
             b0[i] = z;
         }
         gsync<G>();
-        V *out = fft_any<T, G>(b0, b1, L, 1, a.rl, +1, twL, lane);
+        V *out = fft_any<T, G>(b0, b1, L, 1, a.rl, +1, twL, blL, lane);
         T *frow = a.f + row * (int64_t)L;
         T *hrow = a.analytic ? a.hf + row * (int64_t)L : nullptr;
         for (int p = lane; p < L; p += G) {
@@ -315,17 +405,28 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
 // shared memory: root tables + Q~ (if small) + per row group [2 bl + MN] complex values
 static size_t group_elems(const Axis1D &ax) {
     const int64_t npair = (ax.M + 1) / 2;
-    return (size_t)(2 * std::max<int64_t>(npair * ax.N, ax.L) + (int64_t)ax.M * ax.N);
+    return (size_t)(2 * std::max<int64_t>(npair * ax.N, ax.L) + (int64_t)ax.M * ax.N +
+                    2 * std::max(ax.radN.bM, ax.radL.bM));
 }
+static size_t blue_elems(const AnyRadix &r) { return r.bp ? (size_t)(r.bp + 3 * r.bM) : 0; }
 static bool q_in_smem(const Axis1D &ax) { return ax.N * ax.M * ax.M <= 4096; }
 static size_t smem_for(const Axis1D &ax, int groups) {
     const size_t vs = ax.dtype == MCI_F64 ? 16 : 8;
-    return (size_t)(ax.N + ax.L + (q_in_smem(ax) ? ax.N * ax.M * ax.M : 0) + groups * group_elems(ax)) * vs;
+    return (size_t)(ax.N + ax.L + (q_in_smem(ax) ? ax.N * ax.M * ax.M : 0) + blue_elems(ax.radN) + blue_elems(ax.radL) +
+                    groups * group_elems(ax)) * vs;
 }
-// warp per row (8 rows per CTA) when a row's working set is small, else one 256-thread CTA per row
-static bool warp_rows(const Axis1D &ax) { return smem_for(ax, 8) <= 96 * 1024; }
+// warp per row when a row's working set is small: the most rows per CTA (8, 4 or 2) that still
+// lets two CTAs share an SM; else one 256-thread CTA per row
+static int warp_groups(const Axis1D &ax) {
+    for (int gp : {8, 4, 2})
+        if (smem_for(ax, gp) <= 110 * 1024) return gp;
+    return smem_for(ax, 8) <= 200 * 1024 ? 8 : 0;
+}
 
-size_t anylen_smem_bytes(const Axis1D &ax) { return warp_rows(ax) ? smem_for(ax, 8) : smem_for(ax, 1); }
+size_t anylen_smem_bytes(const Axis1D &ax) {
+    const int gp = warp_groups(ax);
+    return gp ? smem_for(ax, gp) : smem_for(ax, 1);
+}
 
 bool anylen_supported(const Axis1D &ax) {
     return ax.M <= 8 && ax.N <= 65536 && ax.L <= (1 << 22) && anylen_smem_bytes(ax) <= 200 * 1024;
@@ -363,9 +464,16 @@ cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, con
                           cudaStream_t st, int *n_launches) {
     if (rows <= 0) return cudaSuccess;
     if (n_launches) *n_launches += 1;
-    if (warp_rows(ax))
+    const int gp = warp_groups(ax);
+    if (gp == 8)
         return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 8>(ax, ra, rows, g, f, hf, st)
                                    : anylen_launch_t<float, 32, 8>(ax, ra, rows, g, f, hf, st);
+    if (gp == 4)
+        return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 4>(ax, ra, rows, g, f, hf, st)
+                                   : anylen_launch_t<float, 32, 4>(ax, ra, rows, g, f, hf, st);
+    if (gp == 2)
+        return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 2>(ax, ra, rows, g, f, hf, st)
+                                   : anylen_launch_t<float, 32, 2>(ax, ra, rows, g, f, hf, st);
     return ax.dtype == MCI_F64 ? anylen_launch_t<double, 256, 1>(ax, ra, rows, g, f, hf, st)
                                : anylen_launch_t<float, 256, 1>(ax, ra, rows, g, f, hf, st);
 }

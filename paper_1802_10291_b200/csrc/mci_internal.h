@@ -14,6 +14,10 @@ namespace mci {
 struct AnyRadix {
     int n = 0;
     int r[24] = {0};
+    int bp = 0, bM = 0;  // Bluestein radix (a prime > 16, 0 if none) and its power-of-two length M >= 2 bp - 1
+    // device tables of the Bluestein pass: chirp c_j = e^{s pi i (j^2 mod 2p)/p} [bp],
+    // H^ = FFT(conj c)/M [bM], roots e^{-2 pi i m/M} and e^{+2 pi i m/M} [bM each]
+    const void *bc = nullptr, *bH = nullptr, *bwm = nullptr, *bwp = nullptr;
 };
 
 // Per-plan device tables for one 1D axis (fused or four-step path).

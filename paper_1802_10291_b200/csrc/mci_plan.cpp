@@ -273,7 +273,39 @@ mci::AnyRadix radix_plan(int64_t n) {
     for (int64_t d = 11; d * d <= n && p.n < 23; d += 2)
         while (n % d == 0) { push((int)d); n /= d; }
     if (n > 1) push((int)n);
+    // Bluestein (chirp-z) for the largest prime radix > 16 whose convolution fits M <= 4096
+    for (int i = 0; i < p.n; ++i)
+        if (p.r[i] > 16 && p.r[i] > p.bp && next_pow2(2 * (int64_t)p.r[i] - 1) <= 4096) p.bp = p.r[i];
+    if (p.bp) p.bM = (int)next_pow2(2 * (int64_t)p.bp - 1);
     return p;
+}
+
+// Bluestein tables for a radix-p pass of sign s (fp64): chirp, H^ = FFT_-(h)/M with
+// h_n = conj c_n (n < p), h_{M-n} = conj c_n (0 < n < p), and the M-point roots.
+// X_m = sum_j x_j e^{s 2 pi i j m / p} = c_m sum_j (x_j c_j) conj c_{m-j}  (jm = (j^2 + m^2 - (m-j)^2)/2).
+template <typename T> void push_bluestein(std::vector<T> &blob, int p, int M, int s, size_t off[4]) {
+    std::vector<cd> c(p), h(M, 0.0), H(M);
+    for (int j = 0; j < p; ++j) {
+        const int64_t e = ((int64_t)j * j) % (2 * p);
+        c[j] = std::polar(1.0, s * PI * (double)e / p);
+    }
+    for (int n = 0; n < p; ++n) {
+        h[n] = std::conj(c[n]);
+        if (n) h[M - n] = std::conj(c[n]);
+    }
+    for (int k = 0; k < M; ++k) {
+        cd acc = 0.0;
+        for (int n = 0; n < M; ++n) acc += h[n] * std::polar(1.0, -2 * PI * (double)(((int64_t)n * k) % M) / M);
+        H[k] = acc / (double)M;
+    }
+    off[0] = blob.size();
+    for (int j = 0; j < p; ++j) push_c(blob, c[j]);
+    off[1] = blob.size();
+    for (int k = 0; k < M; ++k) push_c(blob, H[k]);
+    off[2] = blob.size();
+    push_roots(blob, M, M, 1, -1);
+    off[3] = blob.size();
+    push_roots(blob, M, M, 1, +1);
 }
 
 template <typename T>
@@ -341,6 +373,20 @@ mci_status build_axis_any(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mc
     offs.push_back(blob.size());  // twLhi = e^{+2 pi i m / L}
     push_roots(blob, L, L, 1, +1);
     ax.LO = L;  // (twLlo unused on this path)
+    // Bluestein tables (offsets 3..6: forward N, 7..10: inverse L), resolved in set_ptrs_any
+    size_t ob[4];
+    if (ax.radN.bp) {
+        push_bluestein(blob, ax.radN.bp, ax.radN.bM, -1, ob);
+        for (size_t o : ob) offs.push_back(o);
+    } else {
+        for (int i = 0; i < 4; ++i) offs.push_back(0);
+    }
+    if (ax.radL.bp) {
+        push_bluestein(blob, ax.radL.bp, ax.radL.bM, +1, ob);
+        for (size_t o : ob) offs.push_back(o);
+    } else {
+        for (int i = 0; i < 4; ++i) offs.push_back(0);
+    }
     ax.special = 4;
     return MCI_OK;
 }
@@ -363,6 +409,18 @@ void set_ptrs(mci::Axis1D &ax, void *base, const std::vector<size_t> &offs, size
     ax.twF = b + offs[1] * elem;
     ax.twLhi = b + offs[2] * elem;
     ax.twLlo = b + (offs[2] + 2 * (ax.L / ax.LO)) * elem;
+    if (ax.special == 4) {  // arbitrary-length path: Bluestein tables
+        mci::AnyRadix *rp[2] = {&ax.radN, &ax.radL};
+        for (int t = 0; t < 2; ++t) {
+            if (!rp[t]->bp) continue;
+            rp[t]->bc = b + offs[3 + 4 * t] * elem;
+            rp[t]->bH = b + offs[4 + 4 * t] * elem;
+            rp[t]->bwm = b + offs[5 + 4 * t] * elem;
+            rp[t]->bwp = b + offs[6 + 4 * t] * elem;
+        }
+        ax.rowtab = nullptr;
+        return;
+    }
     ax.rowtab = offs.size() > 3 ? (const void *)(b + offs[3] * elem) : nullptr;
 }
 
