@@ -47,6 +47,22 @@ template <typename V> __device__ __forceinline__ V crot(V a, int s) {  // a * (s
     return s > 0 ? V{-a.y, a.x} : V{a.y, -a.x};
 }
 
+// x / d and x mod d for 0 <= x < 2^22 without an integer division: float reciprocal, one
+// correction step (|x inv - x/d| < 1)
+struct FDiv {
+    int d;
+    float inv;
+    __device__ __forceinline__ explicit FDiv(int d_) : d(d_), inv(1.f / (float)d_) {}
+    __device__ __forceinline__ int div(int x, int &rem) const {
+        int q = (int)((float)x * inv);
+        int r = x - q * d;
+        if (r < 0) { --q; r += d; }
+        else if (r >= d) { ++q; r -= d; }
+        rem = r;
+        return q;
+    }
+};
+
 // Row group of G threads: one warp (G = 32, warp-synchronous) or the whole CTA.
 template <int G> __device__ __forceinline__ void gsync() {
     if constexpr (G == 32) __syncwarp();
@@ -101,8 +117,11 @@ __device__ __forceinline__ void pass_r(const cv<T> *in, cv<T> *out, int n, int c
                                        int lane) {
     using V = cv<T>;
     const int nb = n / R, tws = n / (Ls * R);
-    for (int idx = lane; idx < cnt * nb; idx += G) {
-        const int c = idx / nb, b = idx - c * nb, k = b % Ls;
+    const FDiv fl(Ls);
+    for (int c = 0; c < cnt; ++c)
+    for (int b = lane; b < nb; b += G) {
+        int k;
+        fl.div(b, k);  // k = b mod Ls
         const V *src = in + c * n;
         V x[R];
         const int d = k * tws;  // < n
@@ -134,9 +153,13 @@ __device__ void pass_direct(const cv<T> *in, cv<T> *out, int n, int cnt, int r, 
     using V = cv<T>;
     constexpr int U = 4;
     const int nb = n / r, tws = n / (Ls * r), mbk = (r + U - 1) / U;
-    for (int idx = lane; idx < cnt * nb * mbk; idx += G) {
-        const int c = idx / (nb * mbk), rem = idx - c * (nb * mbk), b = rem / mbk, m0 = (rem - b * mbk) * U,
-                  k = b % Ls;
+    const FDiv fm(mbk), fl(Ls);
+    for (int c = 0; c < cnt; ++c)
+    for (int rem = lane; rem < nb * mbk; rem += G) {
+        int mb, k;
+        const int b = fm.div(rem, mb);
+        const int m0 = mb * U;
+        fl.div(b, k);
         const V *src = in + c * n + b;
         int d = k * tws + m0 * nb;  // < 2 n
         if (d >= n) d -= n;
@@ -197,17 +220,23 @@ __device__ void pass_bluestein(const cv<T> *in, cv<T> *out, int n, int cnt, int 
                                int lane) {
     using V = cv<T>;
     const int p = bl.p, M = bl.M, nb = n / p, tws = n / (Ls * p);
-    for (int bf = 0; bf < cnt * nb; ++bf) {
-        const int c = bf / nb, b = bf - c * nb, k = b % Ls;
+    for (int c = 0; c < cnt; ++c)
+    for (int b = 0; b < nb; ++b) {
+        const int k = b % Ls;
         const V *src = in + c * n;
+        const int d = k * tws;                         // twiddle index step (< n)
+        int e = (int)(((int64_t)lane * d) % n);        // index of element i = lane
+        const int dG = (int)(((int64_t)G * d) % n);    // advance per G elements
         for (int i = lane; i < M; i += G) {
             V v = V{0, 0};
             if (i < p) {
                 v = src[b + i * nb];
-                if (k && i) v = cmul(v, root[(int)(((int64_t)i * k * tws) % n)]);
+                if (e) v = cmul(v, root[e]);
                 v = cmul(v, bl.c[i]);
             }
             bl.t0[i] = v;
+            e += dG;
+            if (e >= n) e -= n;
         }
         gsync<G>();
         V *R = fft_pow2<T, G>(bl.t0, bl.t1, M, -1, bl.wm, lane);
