@@ -295,15 +295,18 @@ template <typename T, int G> __device__ __forceinline__ T group_max(T v, T *red)
 }  // namespace anyk
 
 // smem layout: [twN: N][twL: L][Q~: N M M if qsm][Bluestein tables N, L] then per group
-// [b0: bl][b1: bl][A: MN][t0: bM][t1: bM]
+// [b0: bl][b1: bl][A: RP MN | t0: bM, t1: bM].
+// Real output: a group takes RP = 2 rows at a time -- their 2M real channels share M complex
+// forward FFTs and one inverse FFT gives f(row 0) + i f(row 1) (both spectra are Hermitian).
+// Analytic output (z = f + i Hf is complex): one row at a time.
 template <typename T, int G, int GPB>
 __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a) {
     using V = cv<T>;
     using namespace anyk;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, N = a.N, L = a.L, MN = a.MN, K1 = a.K1, Kmax = a.Kmax;
-    const int npair = (M + 1) / 2;
-    const int bl = max(npair * N, L);
+    const int RP = a.analytic ? 1 : 2;
+    const int bl = max(((RP * M + 1) / 2) * N, L);
     V *twN = reinterpret_cast<V *>(smem_raw);
     V *twL = twN + N;
     V *Qs = twL + L;
@@ -329,28 +332,38 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
     }
     const int bmx = max(blN.M, blL.M);
     const int grp = threadIdx.x / G, lane = threadIdx.x % G;
-    V *b0 = btab + (size_t)grp * (2 * bl + MN + 2 * bmx);
+    V *b0 = btab + (size_t)grp * (2 * bl + max(RP * MN, 2 * bmx));
     V *b1 = b0 + bl;
-    V *A = b1 + bl;  // a(k), k = K1 .. K1 + MN - 1
-    blN.t0 = blL.t0 = A + MN;
-    blN.t1 = blL.t1 = A + MN + bmx;
+    V *A = b1 + bl;  // a(k) of row rl at A[rl MN + k - K1], k = K1 .. K1 + MN - 1
+    // Bluestein buffers alias A: A is written after the forward FFT and dead before the inverse
+    blN.t0 = blL.t0 = A;
+    blN.t1 = blL.t1 = A + bmx;
     for (int i = threadIdx.x; i < N; i += G * GPB) twN[i] = a.twN[i];
     for (int i = threadIdx.x; i < L; i += G * GPB) twL[i] = a.twL[i];
     for (int i = threadIdx.x; i < qn; i += G * GPB) Qs[i] = a.Q[i];
     const V *Qt = a.qsm ? Qs : a.Q;
     __shared__ T red[(G > 32 ? G : 32) / 32];
-    __shared__ int escale_s[GPB][8];
+    __shared__ int escale_s[GPB][16];
     int *escale = escale_s[grp];
     __syncthreads();
-    for (int64_t row = (int64_t)blockIdx.x * GPB + grp; row < a.rows; row += (int64_t)gridDim.x * GPB) {
+    const int64_t nunits = (a.rows + RP - 1) / RP;
+    for (int64_t u = (int64_t)blockIdx.x * GPB + grp; u < nunits; u += (int64_t)gridDim.x * GPB) {
         const RowAddr &ra = a.ra;
-        const int64_t base = (row / (ra.D0 * ra.D1)) * ra.s2 + ((row / ra.D0) % ra.D1) * ra.s1 + (row % ra.D0) * ra.s0;
+        const int64_t row0 = u * RP;
+        const int nr = (int)min((int64_t)RP, a.rows - row0);  // rows in this unit
+        const int nvc = nr * M, npv = (nvc + 1) / 2;            // real channels, complex FFTs
+        auto chan = [&](int vc) {  // address of virtual channel vc = rl M + m
+            const int64_t row = row0 + vc / M;
+            return a.g + (row / (ra.D0 * ra.D1)) * ra.s2 + ((row / ra.D0) % ra.D1) * ra.s1 + (row % ra.D0) * ra.s0 +
+                   (int64_t)(vc % M) * ra.cs;
+        };
         // ---- load channel pairs z_c = g_{2c} + i g_{2c+1}, per-channel exact power-of-two scaling
-        for (int c = 0; c < npair; ++c) {
+        for (int c = 0; c < npv; ++c) {
             T m0 = 0, m1 = 0;
+            const T *p0 = chan(2 * c), *p1 = (2 * c + 1 < nvc) ? chan(2 * c + 1) : nullptr;
             for (int n = lane; n < N; n += G) {
-                const T re = __ldg(a.g + base + (int64_t)(2 * c) * ra.cs + (int64_t)n * ra.ss);
-                const T im = (2 * c + 1 < M) ? __ldg(a.g + base + (int64_t)(2 * c + 1) * ra.cs + (int64_t)n * ra.ss) : T(0);
+                const T re = __ldg(p0 + (int64_t)n * ra.ss);
+                const T im = p1 ? __ldg(p1 + (int64_t)n * ra.ss) : T(0);
                 b0[c * N + n] = V{re, im};
                 m0 = fmax(m0, fabs(re));
                 m1 = fmax(m1, fabs(im));
@@ -366,16 +379,19 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
             }
         }
         gsync<G>();
-        for (int idx = lane; idx < npair * N; idx += G) {
-            const int c = idx / N;
-            const V z = b0[idx];
-            b0[idx] = V{ldexp(z.x, -escale[2 * c]), ldexp(z.y, -escale[2 * c + 1])};
+        for (int c = 0; c < npv; ++c) {
+            const int s0 = -escale[2 * c], s1 = -escale[2 * c + 1];
+            for (int n = lane; n < N; n += G) {
+                const V z = b0[c * N + n];
+                b0[c * N + n] = V{ldexp(z.x, s0), ldexp(z.y, s1)};
+            }
         }
         gsync<G>();
         // ---- forward DFTs G_c[q] = sum_n z_c[n] e^{-2 pi i q n / N}
-        V *Z = fft_any<T, G>(b0, b1, N, npair, a.rn, -1, twN, blN, lane);
+        V *Z = fft_any<T, G>(b0, b1, N, npv, a.rn, -1, twN, blN, lane);
         // ---- per-class solve for every class q: a(j_q + l N), j_q = K1 + ((q - K1) mod N)
         const int q0 = (int)((((int64_t)-K1) % N + N) % N);  // (q - K1) mod N = (q + q0) mod N
+        for (int rl = 0; rl < nr; ++rl)
         for (int q = lane; q < N; q += G) {
             const int qm = q == 0 ? 0 : N - q;
             int t = q + q0;
@@ -385,10 +401,11 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
 #pragma unroll
             for (int l = 0; l < 8; ++l) v[l] = V{0, 0};
             for (int m = 0; m < M; ++m) {
-                const V zc = Z[(m >> 1) * N + q], zm = cconj(Z[(m >> 1) * N + qm]);
-                V gm = (m & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}  // (zc - zm) / (2i)
-                               : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};  // (zc + zm) / 2
-                gm = V{ldexp(gm.x, escale[m]), ldexp(gm.y, escale[m])};
+                const int vc = rl * M + m;
+                const V zc = Z[(vc >> 1) * N + q], zm = cconj(Z[(vc >> 1) * N + qm]);
+                V gm = (vc & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}  // (zc - zm) / (2i)
+                                : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};  // (zc + zm) / 2
+                gm = V{ldexp(gm.x, escale[vc]), ldexp(gm.y, escale[vc])};
                 const V *qrow = Qt + ((int64_t)q * M + m) * M;
 #pragma unroll
                 for (int l = 0; l < 8; ++l)
@@ -396,32 +413,36 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
             }
 #pragma unroll
             for (int l = 0; l < 8; ++l)
-                if (l < M) A[jq + l * N - K1] = v[l];
+                if (l < M) A[rl * MN + jq + l * N - K1] = v[l];
         }
         gsync<G>();
         // ---- inverse input: bin i of the length-L transform
         //      real:     sum over k = i (mod L), |k| <= Kmax, of Xf(k) = (a(k) + conj a(-k)) / 2
         //      analytic: Xf(0) at i = 0, 2 Xf(i) for 0 < i <= Kmax
-        auto af = [&](int k) { return (k >= K1 && k < K1 + MN) ? A[k - K1] : V{0, 0}; };
-        auto xf = [&](int k) {
-            const V p = af(k), m = cconj(af(-k));
+        auto af = [&](int rl, int k) { return (k >= K1 && k < K1 + MN) ? A[rl * MN + k - K1] : V{0, 0}; };
+        auto xf = [&](int rl, int k) {
+            const V p = af(rl, k), m = cconj(af(rl, -k));
             return V{(T)0.5 * (p.x + m.x), (T)0.5 * (p.y + m.y)};
         };
         for (int i = lane; i < L; i += G) {
             V z = V{0, 0};
-            if (!a.analytic) {
-                if (i <= Kmax) z = xf(i);
-                if (i > 0 && L - i <= Kmax) z = cadd(z, xf(i - L));
+            if (!a.analytic) {  // Z0(i) + i Z1(i), Zr = row r's folded Hermitian spectrum
+                for (int rl = 0; rl < nr; ++rl) {
+                    V zr = V{0, 0};
+                    if (i <= Kmax) zr = xf(rl, i);
+                    if (i > 0 && L - i <= Kmax) zr = cadd(zr, xf(rl, i - L));
+                    z = rl ? cadd(z, crot(zr, 1)) : zr;
+                }
             } else {
-                if (i == 0) z = xf(0);
-                else if (i <= Kmax) z = cscale(xf(i), (T)2);
+                if (i == 0) z = xf(0, 0);
+                else if (i <= Kmax) z = cscale(xf(0, i), (T)2);
             }
             b0[i] = z;
         }
         gsync<G>();
         V *out = fft_any<T, G>(b0, b1, L, 1, a.rl, +1, twL, blL, lane);
-        T *frow = a.f + row * (int64_t)L;
-        T *hrow = a.analytic ? a.hf + row * (int64_t)L : nullptr;
+        T *frow = a.f + row0 * (int64_t)L;
+        T *hrow = a.analytic ? a.hf + row0 * (int64_t)L : (nr > 1 ? frow + L : nullptr);  // Hf, or row 1's f
         for (int p = lane; p < L; p += G) {
             const V z = out[p];
             frow[p] = z.x;
@@ -433,9 +454,9 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
 
 // shared memory: root tables + Q~ (if small) + per row group [2 bl + MN] complex values
 static size_t group_elems(const Axis1D &ax) {
-    const int64_t npair = (ax.M + 1) / 2;
-    return (size_t)(2 * std::max<int64_t>(npair * ax.N, ax.L) + (int64_t)ax.M * ax.N +
-                    2 * std::max(ax.radN.bM, ax.radL.bM));
+    const int64_t rp = ax.analytic ? 1 : 2;  // rows per unit (real output pairs rows)
+    return (size_t)(2 * std::max<int64_t>(((rp * ax.M + 1) / 2) * ax.N, ax.L) +
+                    std::max<int64_t>(rp * ax.M * ax.N, 2 * std::max(ax.radN.bM, ax.radL.bM)));
 }
 static size_t blue_elems(const AnyRadix &r) { return r.bp ? (size_t)(r.bp + 3 * r.bM) : 0; }
 static bool q_in_smem(const Axis1D &ax) { return ax.N * ax.M * ax.M <= 4096; }
