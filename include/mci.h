@@ -74,7 +74,11 @@ typedef struct {
     const double *table; /* host, 2*M*N doubles (MCI_SYS_TABLE); copied     */
 } mci_system;
 
-enum { MCI_OUT_HILBERT = 1u }; /* plan also produces Hf */
+enum {
+    MCI_OUT_HILBERT = 1u, /* plan also produces Hf                                            */
+    MCI_OFFGRID = 2u      /* plan also evaluates at arbitrary points (mci_execute_offgrid); it is
+                             built on the arbitrary-length path                                */
+};
 
 /* ---- plans ------------------------------------------------------------------------ */
 
@@ -109,6 +113,16 @@ void mci_plan_destroy(mci_plan p);
  * Input and output must not overlap.  Asynchronous on cuda_stream. */
 mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf,
                           void *cuda_stream);
+
+/* Off-grid evaluation (Eq. drictexpression / Lemma 2):
+ *   f[b][j] = Re T_N f_b(t_j) = sum_k Xf(k) e^{i k t_j},  Xf(k) = (a(k) + conj a(-k)) / 2,
+ *   hf[b][j] = H(Re T_N f_b)(t_j)  (only with MCI_OUT_HILBERT; else pass NULL),
+ * for arbitrary t_j in radians (any real value).  Plan created with MCI_OFFGRID.
+ * g: device [batch][M][N]; t: device [n_pts] (plan dtype), shared by all rows;
+ * f, hf: device [batch][n_pts].  Per row the spectrum is computed once, then every point
+ * is a direct sum over the band in fp64 (cost O(n_pts M N) per row). */
+mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t n_pts, const void *t, void *f,
+                               void *hf, void *cuda_stream);
 
 /* g: device [n_images][My][Mx][Ny][Nx]; out: device [n_images][Ly][Lx]. */
 mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out,

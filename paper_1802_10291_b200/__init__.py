@@ -24,6 +24,7 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "mci.h")
 MCI_OK, MCI_E_ARG, MCI_E_BAND, MCI_E_ALIAS, MCI_E_SINGULAR, MCI_E_SIZE, MCI_E_CUDA, MCI_E_UNSUPPORTED = range(8)
 MCI_F32, MCI_F64 = 0, 1
 MCI_OUT_HILBERT = 1
+MCI_OFFGRID = 2
 _KIND = {"identity": 0, "derivative": 1, "hilbert": 2, "delay": 3, "table": 4}
 PATH_NAMES = {0: "fused", 1: "fourstep", 2: "2d"}
 
@@ -59,6 +60,8 @@ def _lib_handle():
         L.mci_plan_destroy.restype = None
         L.mci_execute_1d.argtypes = [vp, i64, vp, vp, vp, vp]
         L.mci_execute_1d.restype = i32
+        L.mci_execute_offgrid.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp]
+        L.mci_execute_offgrid.restype = i32
         L.mci_execute_2d.argtypes = [vp, i64, vp, vp, vp]
         L.mci_execute_2d.restype = i32
         L.mci_execute_1d_host.argtypes = [vp, i64, vp, vp, vp]
@@ -126,17 +129,19 @@ def _check(status, what):
 class Plan:
     """1D MCI plan: M channels x N samples -> L outputs (f, optionally Hf)."""
 
-    def __init__(self, M, N, L, bank, null_bins=(), dtype="f32", hilbert=False):
+    def __init__(self, M, N, L, bank, null_bins=(), dtype="f32", hilbert=False, offgrid=False):
         lib = _lib_handle()
         self.M, self.N, self.L = int(M), int(N), int(L)
         self.dtype = dtype
         self.hilbert = bool(hilbert)
+        self.offgrid = bool(offgrid)
         sys_arr, self._keep = _systems(bank)
         nb = np.ascontiguousarray(np.asarray(list(null_bins), dtype=np.int64))
         h = ctypes.c_void_p()
         st = lib.mci_plan_create(ctypes.byref(h), self.M, self.N, self.L, ctypes.addressof(sys_arr),
                                  nb.ctypes.data if len(nb) else None, len(nb),
-                                 MCI_F64 if dtype == "f64" else MCI_F32, MCI_OUT_HILBERT if hilbert else 0)
+                                 MCI_F64 if dtype == "f64" else MCI_F32,
+                                 (MCI_OUT_HILBERT if hilbert else 0) | (MCI_OFFGRID if offgrid else 0))
         _check(st, "mci_plan_create")
         self._h = h
 
@@ -172,6 +177,24 @@ class Plan:
         st = _lib_handle().mci_execute_1d(self._h, batch, _dptr(g), _dptr(f), _dptr(hf) if self.hilbert else None,
                                           _stream(stream))
         _check(st, "mci_execute_1d")
+        return (f, hf) if self.hilbert else f
+
+    def execute_offgrid(self, g, t, f=None, hf=None, stream=None):
+        """f(t_j) = Re T_N f(t_j) (and Hf) at arbitrary points t (CUDA tensor [n_pts], radians);
+        plan created with offgrid=True.  Returns f [batch][n_pts] (and hf)."""
+        import torch
+        assert self.offgrid, "plan was not created with offgrid=True"
+        assert g.is_cuda and g.is_contiguous() and g.dtype == self.torch_dtype()
+        assert t.is_cuda and t.is_contiguous() and t.dtype == g.dtype and t.dim() == 1
+        batch = g.numel() // (self.M * self.N)
+        npts = t.numel()
+        if f is None:
+            f = torch.empty((batch, npts), dtype=g.dtype, device=g.device)
+        if self.hilbert and hf is None:
+            hf = torch.empty((batch, npts), dtype=g.dtype, device=g.device)
+        st = _lib_handle().mci_execute_offgrid(self._h, batch, _dptr(g), npts, _dptr(t), _dptr(f),
+                                               _dptr(hf) if self.hilbert else None, _stream(stream))
+        _check(st, "mci_execute_offgrid")
         return (f, hf) if self.hilbert else f
 
     def execute_host(self, g, f, hf=None):

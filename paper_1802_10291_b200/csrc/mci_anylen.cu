@@ -39,6 +39,9 @@ template <typename T> struct AnyArgs {
     const cv<T> *twN;  // [N] e^{-2 pi i m / N}
     const cv<T> *twL;  // [L] e^{+2 pi i m / L}
     int qsm;           // Q~ copied to shared memory (else read through L1)
+    int offgrid;       // evaluate at the points tp[0 .. npts) instead of the L grid (NEXT-3)
+    const T *tp;
+    int npts;
 };
 
 namespace anyk {
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
     using namespace anyk;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, N = a.N, L = a.L, MN = a.MN, K1 = a.K1, Kmax = a.Kmax;
-    const int RP = a.analytic ? 1 : 2;
+    const int RP = (a.analytic || a.offgrid) ? 1 : 2;
     const int bl = max(((RP * M + 1) / 2) * N, L);
     V *twN = reinterpret_cast<V *>(smem_raw);
     V *twL = twN + N;
@@ -424,6 +427,37 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
             const V p = af(rl, k), m = cconj(af(rl, -k));
             return V{(T)0.5 * (p.x + m.x), (T)0.5 * (p.y + m.y)};
         };
+        if (a.offgrid) {
+            // ---- off-grid evaluation (Eq. drictexpression / Lemma 2):
+            //      f(t) = Xf(0) + 2 sum_{k=1}^{Kmax} Re(Xf(k) e^{ikt}),  Hf(t) = 2 sum_k Im(Xf(k) e^{ikt});
+            //      fp64 rotation recurrence for e^{ikt}, re-seeded by sincos every 64 terms
+            for (int k = lane; k <= Kmax; k += G) b0[k] = xf(0, k);
+            gsync<G>();
+            T *frow = a.f + row0 * (int64_t)a.npts;
+            T *hrow = a.analytic ? a.hf + row0 * (int64_t)a.npts : nullptr;
+            for (int j = lane; j < a.npts; j += G) {
+                const double t = (double)a.tp[j];
+                double sw, cw, c = 1.0, sn = 0.0;
+                sincos(t, &sw, &cw);
+                double sf = (double)b0[0].x, sh = 0.0;
+                for (int k = 1; k <= Kmax; ++k) {
+                    if ((k & 63) == 0) {
+                        sincos((double)k * t, &sn, &c);
+                    } else {
+                        const double c2 = c * cw - sn * sw;
+                        sn = sn * cw + c * sw;
+                        c = c2;
+                    }
+                    const V x = b0[k];
+                    sf += 2.0 * ((double)x.x * c - (double)x.y * sn);
+                    sh += 2.0 * ((double)x.x * sn + (double)x.y * c);
+                }
+                frow[j] = (T)sf;
+                if (hrow) hrow[j] = (T)sh;
+            }
+            gsync<G>();
+            continue;
+        }
         for (int i = lane; i < L; i += G) {
             V z = V{0, 0};
             if (!a.analytic) {  // Z0(i) + i Z1(i), Zr = row r's folded Hermitian spectrum
@@ -484,8 +518,11 @@ bool anylen_supported(const Axis1D &ax) {
 
 template <typename T, int G, int GPB>
 static cudaError_t anylen_launch_t(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, const void *tp = nullptr, int64_t npts = 0) {
     AnyArgs<T> a;
+    a.offgrid = tp != nullptr;
+    a.tp = (const T *)tp;
+    a.npts = (int)npts;
     a.M = ax.M; a.N = (int)ax.N; a.L = (int)ax.L; a.MN = (int)(ax.M * ax.N);
     a.K1 = (int)ax.K1; a.Kmax = (int)(-ax.K1); a.analytic = ax.analytic;
     a.rn = ax.radN; a.rl = ax.radL;
@@ -510,22 +547,32 @@ static cudaError_t anylen_launch_t(const Axis1D &ax, const RowAddr &ra, int64_t 
     return cudaGetLastError();
 }
 
+static cudaError_t anylen_dispatch(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
+                                   cudaStream_t st, const void *tp, int64_t npts) {
+    const bool d = ax.dtype == MCI_F64;
+    switch (warp_groups(ax)) {
+    case 8: return d ? anylen_launch_t<double, 32, 8>(ax, ra, rows, g, f, hf, st, tp, npts)
+                     : anylen_launch_t<float, 32, 8>(ax, ra, rows, g, f, hf, st, tp, npts);
+    case 4: return d ? anylen_launch_t<double, 32, 4>(ax, ra, rows, g, f, hf, st, tp, npts)
+                     : anylen_launch_t<float, 32, 4>(ax, ra, rows, g, f, hf, st, tp, npts);
+    case 2: return d ? anylen_launch_t<double, 32, 2>(ax, ra, rows, g, f, hf, st, tp, npts)
+                     : anylen_launch_t<float, 32, 2>(ax, ra, rows, g, f, hf, st, tp, npts);
+    default: return d ? anylen_launch_t<double, 256, 1>(ax, ra, rows, g, f, hf, st, tp, npts)
+                      : anylen_launch_t<float, 256, 1>(ax, ra, rows, g, f, hf, st, tp, npts);
+    }
+}
+
 cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                           cudaStream_t st, int *n_launches) {
     if (rows <= 0) return cudaSuccess;
     if (n_launches) *n_launches += 1;
-    const int gp = warp_groups(ax);
-    if (gp == 8)
-        return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 8>(ax, ra, rows, g, f, hf, st)
-                                   : anylen_launch_t<float, 32, 8>(ax, ra, rows, g, f, hf, st);
-    if (gp == 4)
-        return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 4>(ax, ra, rows, g, f, hf, st)
-                                   : anylen_launch_t<float, 32, 4>(ax, ra, rows, g, f, hf, st);
-    if (gp == 2)
-        return ax.dtype == MCI_F64 ? anylen_launch_t<double, 32, 2>(ax, ra, rows, g, f, hf, st)
-                                   : anylen_launch_t<float, 32, 2>(ax, ra, rows, g, f, hf, st);
-    return ax.dtype == MCI_F64 ? anylen_launch_t<double, 256, 1>(ax, ra, rows, g, f, hf, st)
-                               : anylen_launch_t<float, 256, 1>(ax, ra, rows, g, f, hf, st);
+    return anylen_dispatch(ax, ra, rows, g, f, hf, st, nullptr, 0);
+}
+
+cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,
+                                  const void *t, void *f, void *hf, cudaStream_t st) {
+    if (rows <= 0 || n_pts <= 0) return cudaSuccess;
+    return anylen_dispatch(ax, ra, rows, g, f, hf, st, t, n_pts);
 }
 
 }  // namespace mci

@@ -78,6 +78,8 @@ bool anylen_supported(const Axis1D &ax);
 size_t anylen_smem_bytes(const Axis1D &ax);
 cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                           cudaStream_t st, int *n_launches);
+cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,
+                                  const void *t, void *f, void *hf, cudaStream_t st);
 
 cudaError_t launch_fourstep(const Axis1D &ax, int64_t batch, const void *g, void *f, void *ws,
                             int64_t ws_signals, cudaStream_t st, int *n_launches);

@@ -430,32 +430,47 @@ mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *
     std::vector<T> blob;
     std::vector<size_t> offs;
     const bool analytic = flags & MCI_OUT_HILBERT;
-    // try the fused path first
     mci::Axis1D ax;
     ax.dtype = p->dtype;
+    mci_status s;
     if (use_anylen(M, N, L)) {  // arbitrary lengths / odd band
-        mci_status s = build_axis_any<T>(ax, M, N, L, sys, null_bins, n_null, analytic, blob, offs, p->cond_max);
+        s = build_axis_any<T>(ax, M, N, L, sys, null_bins, n_null, analytic, blob, offs, p->cond_max);
         if (s != MCI_OK) return s;
         if (!mci::anylen_supported(ax)) return MCI_E_SIZE;
-        if ((s = upload<T>(p, blob)) != MCI_OK) return s;
-        set_ptrs(ax, p->tables, offs, sizeof(T));
-        p->ax = ax;
         p->path = mci::PATH_FUSED;
-        return MCI_OK;
-    }
-    mci_status s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, false, blob, offs, p->cond_max);
-    if (s != MCI_OK) return s;
-    if (!mci::fused_supported(ax)) {
-        blob.clear();
-        offs.clear();
-        s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, true, blob, offs, p->cond_max);
+    } else {
+        s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, false, blob, offs, p->cond_max);
         if (s != MCI_OK) return s;
-        if (!mci::fourstep_supported(ax)) return MCI_E_UNSUPPORTED;
-        p->path = mci::PATH_FOURSTEP;
+        if (!mci::fused_supported(ax)) {
+            blob.clear();
+            offs.clear();
+            s = build_axis<T>(ax, M, N, L, sys, null_bins, n_null, analytic, true, blob, offs, p->cond_max);
+            if (s != MCI_OK) return s;
+            if (!mci::fourstep_supported(ax)) return MCI_E_UNSUPPORTED;
+            p->path = mci::PATH_FOURSTEP;
+        }
     }
+    // off-grid evaluator (NEXT-3): an arbitrary-length axis on the minimal grid L' = M N in the
+    // plan's second axis slot (its inverse is never run; only the forward + solve tables are used)
+    std::vector<T> blob2;
+    std::vector<size_t> offs2;
+    mci::Axis1D ay;
+    ay.dtype = p->dtype;
+    if (flags & MCI_OFFGRID) {
+        double c2 = 0;
+        s = build_axis_any<T>(ay, M, N, (int64_t)M * N, sys, null_bins, n_null, analytic, blob2, offs2, c2);
+        if (s != MCI_OK) return s;
+        if (!mci::anylen_supported(ay)) return MCI_E_SIZE;
+    }
+    const size_t n1 = blob.size();
+    blob.insert(blob.end(), blob2.begin(), blob2.end());
     if ((s = upload<T>(p, blob)) != MCI_OK) return s;
     set_ptrs(ax, p->tables, offs, sizeof(T));
     p->ax = ax;
+    if (flags & MCI_OFFGRID) {
+        set_ptrs(ay, (char *)p->tables + n1 * sizeof(T), offs2, sizeof(T));
+        p->ay = ay;
+    }
     if (p->path == mci::PATH_FOURSTEP) {
         // workspace for a chunk of signals.  Measured on B200 (config 4, 16 signals of
         // 20 MB intermediates): fewer, fuller launches beat L2 residency (96 MB: 0.491 ms,
@@ -574,7 +589,7 @@ mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci
                            const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags) {
     if (!out) return MCI_E_ARG;
     *out = nullptr;
-    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~MCI_OUT_HILBERT) || n_null < 0 ||
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID)) || n_null < 0 ||
         (n_null > 0 && !null_bins))
         return MCI_E_ARG;
     mci_plan p = new (std::nothrow) mci_plan_s();
@@ -626,6 +641,21 @@ mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, voi
     if (!g || !f) return MCI_E_ARG;
     if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
     return exec_1d(p, batch, g, f, hf, (cudaStream_t)stream, nullptr);
+}
+
+mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t n_pts, const void *t, void *f,
+                               void *hf, void *stream) {
+    if (!p || p->path == mci::PATH_2D || !(p->flags & MCI_OFFGRID) || p->ay.special != 4 || batch < 0 ||
+        n_pts < 0 || n_pts > INT32_MAX)
+        return MCI_E_ARG;
+    if (batch == 0 || n_pts == 0) return MCI_OK;
+    if (!g || !t || !f) return MCI_E_ARG;
+    if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
+    mci::RowAddr ra;
+    ra.s2 = (int64_t)p->ax.M * p->ax.N;
+    ra.cs = p->ax.N;
+    ra.ss = 1;
+    return from_cuda(mci::launch_anylen_offgrid(p->ay, ra, batch, g, n_pts, t, f, hf, (cudaStream_t)stream));
 }
 
 mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out, void *stream) {

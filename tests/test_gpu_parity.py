@@ -432,3 +432,42 @@ def test_cfg6_full_batch_sampled():
     assert row_rel(out, P.eval(g[pick])).max() < F32_TOL
     err = (f[:, :: c["L"] // c["N"]] - gt[:, 0]).abs().max().item()
     assert err < 2e-5 * gt[:, 0].abs().max().item()
+
+
+# -------------------------------------------------------------------------- NEXT-3: off-grid evaluation
+@pytest.mark.parametrize("M,N,L,bank_name,hilbert,dtype", [
+    (2, 64, 256, "f_df", True, "f32"),
+    (3, 107, 321, "f_df_ddf", False, "f32"),   # odd band
+    (2, 120, 360, "f_df", True, "f64"),
+    (3, 1024, 16384, "f_df_ddf", True, "f32"),  # config-2 shape
+])
+def test_offgrid_vs_oracle(M, N, L, bank_name, hilbert, dtype):
+    """T_N f (and Hf) at arbitrary real t (Eq. drictexpression /
+    Lemma 2) vs the oracle's direct formula (pinned P1/P8); the
+    grid points t = 2 pi p / L reproduce mci_execute_1d."""
+    m = mci()
+    bank = BANKS[bank_name]
+    rng = np.random.default_rng(N + 7)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    # non-bandlimited rows with channel magnitudes of a derivative bank (|f^(m)| ~ (N/4)^m)
+    g = (rng.standard_normal((4, M, N)) * (N / 4.0) ** np.arange(M)[None, :, None]).astype(npdt)
+    t = np.concatenate([rng.uniform(-20.0, 20.0, 200), 2 * np.pi * np.arange(0, L, max(1, L // 50)) / L])
+    plan = m.Plan(M, N, L, bank, dtype=dtype, hilbert=hilbert, offgrid=True)
+    gt = torch.from_numpy(g).cuda()
+    tt = torch.from_numpy(t.astype(npdt)).cuda()
+    res = plan.execute_offgrid(gt, tt)
+    torch.cuda.synchronize()
+    f = (res[0] if hilbert else res).double().cpu().numpy()
+    P = oracle.OraclePlan(M, N, L, bank)
+    tq = t.astype(npdt).astype(np.float64)  # the points the GPU saw
+    tol = F64_TOL if dtype == "f64" else 5 * F32_TOL
+    for i in (0, 3):
+        assert row_rel(f[i], P.eval_offgrid(g[i], tq)) < tol
+        if hilbert:
+            assert row_rel(res[1][i].double().cpu().numpy(), P.eval_offgrid(g[i], tq, hilbert=True)) < tol
+    if dtype == "f64":  # fp32 t = 2 pi p / L is rounded (~4e-7 rad, i.e. K * 4e-7 of phase): fp64 only
+        grid = plan.execute(gt)
+        grid = (grid[0] if hilbert else grid).double().cpu().numpy()
+        pg = np.arange(0, L, max(1, L // 50))
+        assert row_rel(f[:, 200:], grid[:, pg]).max() < tol
