@@ -6,7 +6,7 @@ M=3 channels (f, f', f''), N=1024 samples each -> L=16384 outputs, fp32.
 A step is one pass of the whole hot path (forward DFTs, per-class solves,
 assembly, inverse FFTs, stores) over the batch, i.e. one mci_execute_1d.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..6] [--impl mci|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..7] [--impl mci|reference]
 
 N > 1: one process per GPU (torchrun), each rank runs its own batch (rows are
 independent: weak scaling, no collective on the data path); time = max over
@@ -33,6 +33,9 @@ import synth  # noqa: E402
 
 METRIC = "MCI output samples/sec (fp32) and achieved HBM GB/s vs B200 peak"
 UNIT = "samples/s"
+# FP64 FMA throughput measured on this pool's B200 (tools/microbench/f64_throughput.cu, 1965 MHz;
+# profiles/r01/microbench_f64.txt): the "alu" roofline peak of the off-grid evaluator (config 7)
+FP64_PEAK_TFLOPS = 33.24
 
 
 def load_peaks():
@@ -53,6 +56,11 @@ def workload(cfg):
                     out_floats_per_unit=c["size"] ** 2)
     M, N, L, B = c["M"], c["N"], c["L"], c["batch"]
     nout = 2 if c.get("hilbert") else 1
+    if cfg == 7:
+        return dict(name=f"cfg7: {c['batch']} x (M={c['M']}, N={c['N']}) -> {c['npts']} arbitrary points x 1 out, "
+                         f"bank 1, ik, -k^2 (NEXT-3 off-grid)",
+                    units=c["batch"], outs_per_unit=c["npts"], in_per_unit=c["M"] * c["N"],
+                    out_floats_per_unit=c["npts"])
     bank = {1: "1, ik", 2: "1, ik, -k^2", 3: "1, ik (+Hf)", 4: "delays 2 pi m/(4N)", 6: "1, ik, -k^2 (NEXT-1, odd band)"}[cfg]
     return dict(name=f"cfg{cfg}: {B} x (M={M}, N={N}) -> L={L} x {nout} out, bank {bank}",
                 units=B, outs_per_unit=L * nout, in_per_unit=M * N, out_floats_per_unit=L * nout)
@@ -71,6 +79,8 @@ def make_inputs(cfg, rank):
         return synth.cfg4_signals(np.arange(c["batch"]), seed=4 + 1000 * rank)[0]
     if cfg == 6:
         return synth.cfg2_batch_fast(c["batch"], seed=6 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
+    if cfg == 7:
+        return synth.cfg2_batch_fast(c["batch"], seed=7 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
     # cfg5: generate a few distinct images and tile them to the batch (content does not
     # change the arithmetic or the bytes; generation of 64 2048^2 images would dominate)
     distinct = 4
@@ -88,6 +98,8 @@ def algorithmic_flops(cfg):
         line = 2 * 2.5 * n * lg(n) + 8 * 4 * (n // 2 + 1) + 2.5 * L * lg(L)
         return (2 * n + L) * line  # per image: column pass Mx*Nx = 2n lines, row pass Ly = L lines
     M, N, L = c["M"], c["N"], c["L"]
+    if cfg == 7:  # forward + solve, then a complex multiply-add per band term per point
+        return M * 2.5 * N * lg(N) + 8 * M * M * (N // 2 + 1) + c["npts"] * (M * N // 2) * 8
     inv = 5 * L * lg(L) if c.get("hilbert") else 2.5 * L * lg(L)
     return M * 2.5 * N * lg(N) + 8 * M * M * (N // 2 + 1) + inv
 
@@ -106,7 +118,7 @@ def make_plan(cfg):
     if cfg == 5:
         return mci.Plan2D(2, c["N"], c["bank"], 2, c["N"], c["bank"], c["scale"])
     return mci.Plan(c["M"], c["N"], c["L"], c["bank"], dtype="f64" if cfg == 1 else "f32",
-                    hilbert=bool(c.get("hilbert")))
+                    hilbert=bool(c.get("hilbert")), offgrid=cfg == 7)
 
 
 class ClockSampler:
@@ -184,6 +196,19 @@ def oracle_sample(cfg, budget_s=12.0, max_steps=None):
                 break
         dt = time.perf_counter() - t0
         return n / dt, f"signal 0, {n} output points (closed-form delay kernel), M*N={M*N} terms each", threads
+    if cfg == 7:
+        P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
+        g = make_inputs(7, 0)[:64].astype(np.float64)
+        t = synth.offgrid_points(c["npts"]).astype(np.float32).astype(np.float64)
+        rows = 0
+        t0 = time.perf_counter()
+        while rows < len(g):
+            P.eval_offgrid(g[rows], t)
+            rows += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return rows * c["npts"] / dt, f"{rows} rows x {c['npts']} off-grid points (direct band sums)", threads
     if cfg == 5:
         px = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=threads)
         px.kernel_table()
@@ -255,6 +280,15 @@ def run_reference(args, rank, world):
             oracle.delay_eval_points(c["M"], c["N"], c["L"], gg[0], pts, threads=threads)
             return len(pts)
         sample = "64 output points of signal 0 per step (closed-form delay kernel)"
+    elif cfg == 7:
+        P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
+        g7 = make_inputs(7, 0)[:64].astype(np.float64)
+        t7 = synth.offgrid_points(c["npts"]).astype(np.float32).astype(np.float64)
+
+        def step(i):
+            P.eval_offgrid(g7[i % len(g7)], t7)
+            return c["npts"]
+        sample = f"one row's {c['npts']} off-grid points per step (direct band sums)"
     else:
         px = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=threads)
         px.kernel_table()
@@ -297,7 +331,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6, 7])
     ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -331,8 +365,14 @@ def main():
     units = w["units"]
     c = synth.CONFIGS[cfg]
     hilbert = bool(c.get("hilbert"))
+    tpts = None
     if cfg == 5:
         out = torch.empty((units, c["size"], c["size"]), dtype=tdt, device="cuda")
+        hf = None
+    elif cfg == 7:
+        t_host = synth.offgrid_points(c["npts"], seed=7 + 1000 * rank).astype(np.float32)
+        tpts = torch.from_numpy(t_host).cuda()
+        out = torch.empty((units, c["npts"]), dtype=tdt, device="cuda")
         hf = None
     else:
         out = torch.empty((units, c["L"]), dtype=tdt, device="cuda")
@@ -342,6 +382,8 @@ def main():
     def step():
         if cfg == 5:
             plan.execute(g, out)
+        elif cfg == 7:
+            plan.execute_offgrid(g, tpts, out)
         else:
             plan.execute(g, out, hf)
 
@@ -380,6 +422,13 @@ def main():
             "traffic": load_traffic(w["name"]), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": alg_bytes if cfg in (1, 2, 3, 6) else None,
             "algorithmic_bytes_per_step": alg_bytes}
+    if cfg == 7:  # direct band sums in fp64: bound by the FP64 FMA pipe
+        fl = algorithmic_flops(cfg) * units / (ms_step / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": fl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": fl / FP64_PEAK_TFLOPS, "traffic": load_traffic(w["name"]),
+                "peak_source": "measured FP64 DFMA throughput (tools/microbench/f64_throughput.cu, "
+                               "profiles/r01/microbench_f64.txt)",
+                "hbm_gbs_algorithmic": achieved}
     # secondary ceiling: the FP32 pipe.  Algorithmic flops per unit =
     # SURVEY.md §8(d) counts (2.5 n log2 n per real FFT, 5 n log2 n complex, 8 M^2 per class).
     flops = algorithmic_flops(cfg) * units
@@ -397,9 +446,17 @@ def main():
         hh = torch.empty(out.shape, dtype=tdt).pin_memory() if hilbert else None
         e_steps = max(3, min(args.steps, 10))
 
+        if cfg == 7:
+            th = torch.from_numpy(t_host).pin_memory()
+
         def estep():
             if cfg == 5:
                 plan.execute_host(gh, oh)
+            elif cfg == 7:  # public device API with the host copies inside the timed step
+                gd = gh.to("cuda", non_blocking=True)
+                td = th.to("cuda", non_blocking=True)
+                oh.copy_(plan.execute_offgrid(gd, td), non_blocking=True)
+                torch.cuda.synchronize()
             else:
                 plan.execute_host(gh, oh, hh)
         estep()
@@ -412,7 +469,7 @@ def main():
         if world > 1:
             et = max_over_ranks(et, dist, "cuda")
         e2e = {"value": total_samples / et, "unit": UNIT,
-               "h2d_bytes_per_step": int(gh.numel() * esz),
+               "h2d_bytes_per_step": int(gh.numel() * esz) + (int(th.numel() * esz) if cfg == 7 else 0),
                "d2h_bytes_per_step": int(oh.numel() * esz * (2 if hilbert else 1)),
                "ms_per_step": et * 1e3, "steps": e_steps}
 

@@ -430,30 +430,38 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
         if (a.offgrid) {
             // ---- off-grid evaluation (Eq. drictexpression / Lemma 2):
             //      f(t) = Xf(0) + 2 sum_{k=1}^{Kmax} Re(Xf(k) e^{ikt}),  Hf(t) = 2 sum_k Im(Xf(k) e^{ikt});
-            //      fp64 rotation recurrence for e^{ikt}, re-seeded by sincos every 64 terms
+            //      Horner's scheme in fp64 on z = e^{it}: p = sum_{k>=1} Xf(k) z^k (4 DFMA per term,
+            //      error ~ 2 Kmax eps), then f = Xf(0) + 2 Re p, Hf = 2 Im p
             for (int k = lane; k <= Kmax; k += G) b0[k] = xf(0, k);
             gsync<G>();
             T *frow = a.f + row0 * (int64_t)a.npts;
             T *hrow = a.analytic ? a.hf + row0 * (int64_t)a.npts : nullptr;
-            for (int j = lane; j < a.npts; j += G) {
-                const double t = (double)a.tp[j];
-                double sw, cw, c = 1.0, sn = 0.0;
-                sincos(t, &sw, &cw);
-                double sf = (double)b0[0].x, sh = 0.0;
-                for (int k = 1; k <= Kmax; ++k) {
-                    if ((k & 63) == 0) {
-                        sincos((double)k * t, &sn, &c);
-                    } else {
-                        const double c2 = c * cw - sn * sw;
-                        sn = sn * cw + c * sw;
-                        c = c2;
-                    }
-                    const V x = b0[k];
-                    sf += 2.0 * ((double)x.x * c - (double)x.y * sn);
-                    sh += 2.0 * ((double)x.x * sn + (double)x.y * c);
+            constexpr int PP = 4;  // points per thread: independent Horner chains (ILP)
+            for (int j0 = lane; j0 < a.npts; j0 += G * PP) {
+                double zr[PP], zi[PP], qr[PP], qi[PP];
+#pragma unroll
+                for (int u = 0; u < PP; ++u) {
+                    const int j = j0 + u * G;
+                    sincos(j < a.npts ? (double)a.tp[j] : 0.0, &zi[u], &zr[u]);
+                    qr[u] = qi[u] = 0.0;
                 }
-                frow[j] = (T)sf;
-                if (hrow) hrow[j] = (T)sh;
+                for (int k = Kmax; k >= 1; --k) {  // q <- (q + X_k) z
+                    const V x = b0[k];
+#pragma unroll
+                    for (int u = 0; u < PP; ++u) {
+                        const double ar = qr[u] + (double)x.x, ai = qi[u] + (double)x.y;
+                        qr[u] = fma(ar, zr[u], -ai * zi[u]);
+                        qi[u] = fma(ar, zi[u], ai * zr[u]);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PP; ++u) {
+                    const int j = j0 + u * G;
+                    if (j < a.npts) {
+                        frow[j] = (T)((double)b0[0].x + 2.0 * qr[u]);
+                        if (hrow) hrow[j] = (T)(2.0 * qi[u]);
+                    }
+                }
             }
             gsync<G>();
             continue;

@@ -162,7 +162,15 @@ CONFIGS = {
     # 321 / 3 = 107) with the (f, f', f'') bank, L = 3N = MN (odd band, odd output length)
     6: dict(M=3, N=107, L=321, batch=65536,
             bank=[("identity",), ("derivative", 1), ("derivative", 2)], dtype="f32"),
+    # SURVEY.md §8(f) NEXT-3 measurement line: config-2 rows evaluated at arbitrary points
+    7: dict(M=3, N=1024, L=16384, batch=2048, npts=1024,
+            bank=[("identity",), ("derivative", 1), ("derivative", 2)], dtype="f32"),
 }
+
+
+def offgrid_points(npts: int, seed: int = 7) -> np.ndarray:
+    """Evaluation points for config 7: uniform in [0, 2 pi), seeded (float64)."""
+    return np.random.default_rng([seed, 777]).uniform(0.0, 2 * math.pi, npts)
 
 
 def bank_of(cfg: int):

@@ -471,3 +471,19 @@ def test_offgrid_vs_oracle(M, N, L, bank_name, hilbert, dtype):
         grid = (grid[0] if hilbert else grid).double().cpu().numpy()
         pg = np.arange(0, L, max(1, L // 50))
         assert row_rel(f[:, 200:], grid[:, pg]).max() < tol
+
+
+def test_cfg7_full_batch_sampled():
+    """Config 7 (NEXT-3 measurement line: 2,048 config-2 rows at 1,024 arbitrary points)
+    in the bench launch: sampled rows vs the oracle's direct formula."""
+    m = mci()
+    c = synth.CONFIGS[7]
+    g = synth.cfg2_batch_fast(c["batch"], seed=7, M=c["M"], N=c["N"], bank=c["bank"])
+    t = synth.offgrid_points(c["npts"]).astype(np.float32)
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"], offgrid=True)
+    f = plan.execute_offgrid(torch.from_numpy(g).cuda(), torch.from_numpy(t).cuda())
+    torch.cuda.synchronize()
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    for i in (0, 1000, c["batch"] - 1):
+        ref = P.eval_offgrid(g[i], t.astype(np.float64))
+        assert row_rel(f[i].double().cpu().numpy(), ref) < F32_TOL
