@@ -6,7 +6,7 @@ M=3 channels (f, f', f''), N=1024 samples each -> L=16384 outputs, fp32.
 A step is one pass of the whole hot path (forward DFTs, per-class solves,
 assembly, inverse FFTs, stores) over the batch, i.e. one mci_execute_1d.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..7] [--impl mci|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..8] [--impl mci|reference]
 
 N > 1: one process per GPU (torchrun), each rank runs its own batch (rows are
 independent: weak scaling, no collective on the data path); time = max over
@@ -54,13 +54,18 @@ def workload(cfg):
         return dict(name=f"cfg5: {c['batch']} images, 4 channel images 512x512 -> 2048x2048 (separable, bank {{1,ik}}^2)",
                     units=c["batch"], outs_per_unit=c["size"] ** 2, in_per_unit=4 * n * n,
                     out_floats_per_unit=c["size"] ** 2)
-    M, N, L, B = c["M"], c["N"], c["L"], c["batch"]
-    nout = 2 if c.get("hilbert") else 1
+    if cfg == 8:
+        H, W, s = c["H"], c["W"], c["scale"]
+        return dict(name=f"cfg8: {c['batch']} images {H}x{W} -> {s * H}x{s * W} (SISR x{s}: centred differences, "
+                         f"bank 1, ik, -k^2, rows then columns; NEXT-2)",
+                    units=c["batch"], outs_per_unit=s * H * s * W, in_per_unit=H * W, out_floats_per_unit=s * H * s * W)
     if cfg == 7:
         return dict(name=f"cfg7: {c['batch']} x (M={c['M']}, N={c['N']}) -> {c['npts']} arbitrary points x 1 out, "
                          f"bank 1, ik, -k^2 (NEXT-3 off-grid)",
                     units=c["batch"], outs_per_unit=c["npts"], in_per_unit=c["M"] * c["N"],
                     out_floats_per_unit=c["npts"])
+    M, N, L, B = c["M"], c["N"], c["L"], c["batch"]
+    nout = 2 if c.get("hilbert") else 1
     bank = {1: "1, ik", 2: "1, ik, -k^2", 3: "1, ik (+Hf)", 4: "delays 2 pi m/(4N)", 6: "1, ik, -k^2 (NEXT-1, odd band)"}[cfg]
     return dict(name=f"cfg{cfg}: {B} x (M={M}, N={N}) -> L={L} x {nout} out, bank {bank}",
                 units=B, outs_per_unit=L * nout, in_per_unit=M * N, out_floats_per_unit=L * nout)
@@ -81,6 +86,9 @@ def make_inputs(cfg, rank):
         return synth.cfg2_batch_fast(c["batch"], seed=6 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
     if cfg == 7:
         return synth.cfg2_batch_fast(c["batch"], seed=7 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
+    if cfg == 8:  # 4 distinct images tiled to the batch (content does not change the arithmetic)
+        lr, _ = synth.sisr_images(range(4 * rank, 4 * rank + 4))
+        return np.ascontiguousarray(np.tile(lr, (c["batch"] // 4, 1, 1)))
     # cfg5: generate a few distinct images and tile them to the batch (content does not
     # change the arithmetic or the bytes; generation of 64 2048^2 images would dominate)
     distinct = 4
@@ -97,6 +105,12 @@ def algorithmic_flops(cfg):
         n, L = c["N"], c["N"] * c["scale"]
         line = 2 * 2.5 * n * lg(n) + 8 * 4 * (n // 2 + 1) + 2.5 * L * lg(L)
         return (2 * n + L) * line  # per image: column pass Mx*Nx = 2n lines, row pass Ly = L lines
+    if cfg == 8:  # per image: H row lines (3 channels, N = W -> sW), then sW column lines
+        H, W, s = c["H"], c["W"], c["scale"]
+
+        def line(n, L):
+            return 3 * 2.5 * n * lg(n) + 8 * 9 * (n // 2 + 1) + 2.5 * L * lg(L)
+        return H * line(W, s * W) + s * W * line(H, s * H)
     M, N, L = c["M"], c["N"], c["L"]
     if cfg == 7:  # forward + solve, then a complex multiply-add per band term per point
         return M * 2.5 * N * lg(N) + 8 * M * M * (N // 2 + 1) + c["npts"] * (M * N // 2) * 8
@@ -117,6 +131,8 @@ def make_plan(cfg):
     c = synth.CONFIGS[cfg]
     if cfg == 5:
         return mci.Plan2D(2, c["N"], c["bank"], 2, c["N"], c["bank"], c["scale"])
+    if cfg == 8:
+        return mci.SisrPlan(c["H"], c["W"], c["scale"])
     return mci.Plan(c["M"], c["N"], c["L"], c["bank"], dtype="f64" if cfg == 1 else "f32",
                     hilbert=bool(c.get("hilbert")), offgrid=cfg == 7)
 
@@ -196,6 +212,17 @@ def oracle_sample(cfg, budget_s=12.0, max_steps=None):
                 break
         dt = time.perf_counter() - t0
         return n / dt, f"signal 0, {n} output points (closed-form delay kernel), M*N={M*N} terms each", threads
+    if cfg == 8:
+        lr, _ = synth.sisr_images([0])
+        t0 = time.perf_counter()
+        n = 0
+        while True:
+            oracle.sisr(lr[0].astype(np.float64), c["scale"])
+            n += 1
+            if time.perf_counter() - t0 > budget_s / 2:
+                break
+        dt = time.perf_counter() - t0
+        return n * (c["scale"] ** 2) * c["H"] * c["W"] / dt, f"{n} image(s) {c['H']}x{c['W']} -> x{c['scale']}", threads
     if cfg == 7:
         P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
         g = make_inputs(7, 0)[:64].astype(np.float64)
@@ -280,6 +307,13 @@ def run_reference(args, rank, world):
             oracle.delay_eval_points(c["M"], c["N"], c["L"], gg[0], pts, threads=threads)
             return len(pts)
         sample = "64 output points of signal 0 per step (closed-form delay kernel)"
+    elif cfg == 8:
+        lr8, _ = synth.sisr_images([0])
+
+        def step(i):
+            oracle.sisr(lr8[0].astype(np.float64), c["scale"])
+            return (c["scale"] ** 2) * c["H"] * c["W"]
+        sample = "one image per step"
     elif cfg == 7:
         P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
         g7 = make_inputs(7, 0)[:64].astype(np.float64)
@@ -331,7 +365,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6, 7])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6, 7, 8])
     ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -369,6 +403,9 @@ def main():
     if cfg == 5:
         out = torch.empty((units, c["size"], c["size"]), dtype=tdt, device="cuda")
         hf = None
+    elif cfg == 8:
+        out = torch.empty((units, c["scale"] * c["H"], c["scale"] * c["W"]), dtype=tdt, device="cuda")
+        hf = None
     elif cfg == 7:
         t_host = synth.offgrid_points(c["npts"], seed=7 + 1000 * rank).astype(np.float32)
         tpts = torch.from_numpy(t_host).cuda()
@@ -380,7 +417,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        if cfg == 5:
+        if cfg in (5, 8):
             plan.execute(g, out)
         elif cfg == 7:
             plan.execute_offgrid(g, tpts, out)
@@ -452,6 +489,9 @@ def main():
         def estep():
             if cfg == 5:
                 plan.execute_host(gh, oh)
+            elif cfg == 8:  # public device API with the host copies inside the timed step
+                oh.copy_(plan.execute(gh.to("cuda", non_blocking=True)), non_blocking=True)
+                torch.cuda.synchronize()
             elif cfg == 7:  # public device API with the host copies inside the timed step
                 gd = gh.to("cuda", non_blocking=True)
                 td = th.to("cuda", non_blocking=True)

@@ -104,6 +104,18 @@ mci_status mci_plan_create_2d(mci_plan *out, int Mx, int64_t Nx, const mci_syste
                               int64_t Ny, const mci_system *sy, int scale, mci_dtype dtype,
                               unsigned flags);
 
+/* Single-image super-resolution by MCI: the
+ * paper's scheme on a periodic H x W low-resolution image, scale s >= 3 per axis.  Rows
+ * first: channels f, f', f'' along x by three-point centred differences on the grid
+ * t = 2 pi x / W (f' = (f[x+1] - f[x-1]) / (2d), f'' = (f[x+1] - 2 f[x] + f[x-1]) / d^2,
+ * d = 2 pi / W), then MCI with the Example-2 bank (1, ik, -k^2) to
+ * s W points; then the same along y on the row-interpolated image.  Any H, W >= 2
+ * (the paper's 107..170 included).  The plan owns a workspace for a chunk of images. */
+mci_status mci_plan_create_sisr(mci_plan *out, int64_t H, int64_t W, int scale, mci_dtype dtype);
+
+/* lr: device [n_images][H][W]; hr: device [n_images][s H][s W] (plan dtype). */
+mci_status mci_execute_sisr(mci_plan p, int64_t n_images, const void *lr, void *hr, void *cuda_stream);
+
 void mci_plan_destroy(mci_plan p);
 
 /* ---- execution (device buffers) ---------------------------------------------------- */
@@ -140,7 +152,7 @@ mci_status mci_execute_2d_host(mci_plan p, int64_t n_images, const void *g, void
 double mci_plan_cond_max(mci_plan p);          /* max ||H_n||_1 ||H_n^{-1}||_1 */
 int64_t mci_last_singular_bin(void);           /* n of the last MCI_E_SINGULAR (this thread) */
 size_t mci_plan_workspace_bytes(mci_plan p);   /* device bytes owned by the plan            */
-int mci_plan_path(mci_plan p);                 /* 0 fused 1D, 1 four-step 1D, 2 separable 2D */
+int mci_plan_path(mci_plan p);                 /* 0 fused 1D, 1 four-step 1D, 2 separable 2D, 3 SISR */
 int64_t mci_plan_launches(mci_plan p, int64_t batch); /* kernels one execute enqueues       */
 const char *mci_status_str(mci_status s);
 const char *mci_version(void);

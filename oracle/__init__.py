@@ -233,3 +233,35 @@ def eval_2d_columns(g, plan_x: OraclePlan, plan_y: OraclePlan, px_list):
             inter[:, my, ny] = plan_x.eval_points(g[my, :, ny, :], px_list)
     out[:] = plan_y.eval(inter).T
     return out
+
+
+def sisr(lr, scale=3):
+    """Single-image super-resolution by MCI as the paper describes it (PAPER.md:869-886;
+    SURVEY.md §8(f) NEXT-2), fp64, periodic image model.
+
+    "We first compute interpolation result for each row of image, and then apply
+    interpolation for each column by using the same operations.  The derivatives of
+    image are computed by three-point centered-difference formula" with the Example-2
+    bank (f, f', f'').  On the grid t = 2 pi x / W, d = 2 pi / W:
+    f' = (f[x+1] - f[x-1]) / (2 d), f'' = (f[x+1] - 2 f[x] + f[x-1]) / d^2 (periodic).
+    Returns the [scale H][scale W] image (real part after each pass)."""
+    lr = np.asarray(lr, dtype=np.float64)
+    H, W = lr.shape
+    bank = [("identity",), ("derivative", 1), ("derivative", 2)]
+    px = OraclePlan(3, W, scale * W, bank)
+    py = OraclePlan(3, H, scale * H, bank)
+
+    def fd(a, axis, n):
+        d = 2 * np.pi / n
+        fp, fm = np.roll(a, -1, axis), np.roll(a, 1, axis)
+        return np.stack([a, (fp - fm) / (2 * d), (fp - 2 * a + fm) / (d * d)])
+
+    rows = np.transpose(fd(lr, 1, W), (1, 0, 2))          # [H][3][W]
+    inter = px.eval(rows)                                  # [H][sW]
+    cols = np.transpose(fd(inter, 0, H), (2, 0, 1))        # [sW][3][H]
+    return px_py_out_t(py.eval(cols))                      # [sH][sW]
+
+
+def px_py_out_t(out_cols):
+    """Column-pass output [sW][sH] -> image [sH][sW]."""
+    return np.ascontiguousarray(np.asarray(out_cols).T)

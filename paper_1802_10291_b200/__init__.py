@@ -26,7 +26,7 @@ MCI_F32, MCI_F64 = 0, 1
 MCI_OUT_HILBERT = 1
 MCI_OFFGRID = 2
 _KIND = {"identity": 0, "derivative": 1, "hilbert": 2, "delay": 3, "table": 4}
-PATH_NAMES = {0: "fused", 1: "fourstep", 2: "2d"}
+PATH_NAMES = {0: "fused", 1: "fourstep", 2: "2d", 3: "sisr"}
 
 
 class MCIError(RuntimeError):
@@ -62,6 +62,10 @@ def _lib_handle():
         L.mci_execute_1d.restype = i32
         L.mci_execute_offgrid.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp]
         L.mci_execute_offgrid.restype = i32
+        L.mci_plan_create_sisr.argtypes = [ctypes.POINTER(vp), i64, i64, i32, i32]
+        L.mci_plan_create_sisr.restype = i32
+        L.mci_execute_sisr.argtypes = [vp, i64, vp, vp, vp]
+        L.mci_execute_sisr.restype = i32
         L.mci_execute_2d.argtypes = [vp, i64, vp, vp, vp]
         L.mci_execute_2d.restype = i32
         L.mci_execute_1d_host.argtypes = [vp, i64, vp, vp, vp]
@@ -261,3 +265,39 @@ class Plan2D:
 
 def version():
     return _lib_handle().mci_version().decode()
+
+
+class SisrPlan:
+    """Single-image super-resolution by MCI: periodic H x W images ->
+    scale*H x scale*W, rows then columns, channels f, f', f'' by three-point centred
+    differences, Example-2 bank."""
+
+    def __init__(self, H, W, scale=3, dtype="f32"):
+        lib = _lib_handle()
+        self.H, self.W, self.scale, self.dtype = int(H), int(W), int(scale), dtype
+        h = ctypes.c_void_p()
+        st = lib.mci_plan_create_sisr(ctypes.byref(h), self.H, self.W, self.scale,
+                                      MCI_F64 if dtype == "f64" else MCI_F32)
+        _check(st, "mci_plan_create_sisr")
+        self._h = h
+
+    def launches(self, n_images):
+        return int(_lib_handle().mci_plan_launches(self._h, int(n_images)))
+
+    def execute(self, lr, hr=None, stream=None):
+        """lr: CUDA tensor [n][H][W] (plan dtype).  Returns hr [n][scale H][scale W]."""
+        import torch
+        assert lr.is_cuda and lr.is_contiguous() and lr.shape[-2:] == (self.H, self.W)
+        n = lr.numel() // (self.H * self.W)
+        if hr is None:
+            hr = torch.empty((n, self.scale * self.H, self.scale * self.W), dtype=lr.dtype, device=lr.device)
+        st = _lib_handle().mci_execute_sisr(self._h, n, _dptr(lr), _dptr(hr), _stream(stream))
+        _check(st, "mci_execute_sisr")
+        return hr
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _lib is not None:
+            _lib.mci_plan_destroy(h)
+            self._h = None
+

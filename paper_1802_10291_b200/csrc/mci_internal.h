@@ -46,7 +46,7 @@ struct Axis1D {
     AnyRadix radN, radL;
 };
 
-enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2 };
+enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2, PATH_SISR = 3 };
 
 // Row addressing of the fused kernel: row r starts at
 //   (r / (D0*D1)) * s2 + ((r / D0) % D1) * s1 + (r % D0) * s0
@@ -80,6 +80,10 @@ cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, con
                           cudaStream_t st, int *n_launches);
 cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,
                                   const void *t, void *f, void *hf, cudaStream_t st);
+
+size_t sisr_ws_per_image(int H, int W, int s, int dtype);
+cudaError_t launch_sisr_chunk(const Axis1D &ax, const Axis1D &ay, int64_t ni, int H, int W, int s, const void *lr,
+                              void *hr, void *ws, cudaStream_t st, int *nl);
 
 cudaError_t launch_fourstep(const Axis1D &ax, int64_t batch, const void *g, void *f, void *ws,
                             int64_t ws_signals, cudaStream_t st, int *n_launches);

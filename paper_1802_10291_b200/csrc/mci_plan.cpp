@@ -273,9 +273,11 @@ mci::AnyRadix radix_plan(int64_t n) {
     for (int64_t d = 11; d * d <= n && p.n < 23; d += 2)
         while (n % d == 0) { push((int)d); n /= d; }
     if (n > 1) push((int)n);
-    // Bluestein (chirp-z) for the largest prime radix > 16 whose convolution fits M <= 4096
+    // Bluestein (chirp-z) for the largest prime radix > 40 whose convolution fits M <= 4096.  Its
+    // butterflies run one at a time (two M-point FFTs each), so below ~40 the direct pass, which
+    // is parallel over all n outputs, is cheaper (measured: radix 17 in 170 / 510, config 8)
     for (int i = 0; i < p.n; ++i)
-        if (p.r[i] > 16 && p.r[i] > p.bp && next_pow2(2 * (int64_t)p.r[i] - 1) <= 4096) p.bp = p.r[i];
+        if (p.r[i] > 40 && p.r[i] > p.bp && next_pow2(2 * (int64_t)p.r[i] - 1) <= 4096) p.bp = p.r[i];
     if (p.bp) p.bM = (int)next_pow2(2 * (int64_t)p.bp - 1);
     return p;
 }
@@ -583,6 +585,54 @@ cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const
 }
 }  // namespace mci
 
+namespace {
+// SISR plan (NEXT-2): two Example-2 axes (f, f', f'') on the W and H grids, scale s.
+template <typename T>
+mci_status create_sisr(mci_plan p, int64_t H, int64_t W, int s) {
+    static const mci_system bank[3] = {{MCI_SYS_IDENTITY, 0, 0.0, nullptr},
+                                       {MCI_SYS_DERIVATIVE, 1, 0.0, nullptr},
+                                       {MCI_SYS_DERIVATIVE, 2, 0.0, nullptr}};
+    std::vector<T> bx, by;
+    std::vector<size_t> ox, oy;
+    double cx = 0, cy = 0;
+    mci::Axis1D ax, ay;
+    ax.dtype = ay.dtype = p->dtype;
+    auto axis = [&](mci::Axis1D &a, int64_t N, std::vector<T> &b, std::vector<size_t> &o, double &c) -> mci_status {
+        const int64_t L = (int64_t)s * N;
+        if (use_anylen(3, N, L)) {
+            mci_status st = build_axis_any<T>(a, 3, N, L, bank, nullptr, 0, false, b, o, c);
+            if (st == MCI_OK && !mci::anylen_supported(a)) st = MCI_E_SIZE;
+            return st;
+        }
+        mci_status st = build_axis<T>(a, 3, N, L, bank, nullptr, 0, false, false, b, o, c);
+        if (st == MCI_OK && !mci::fused_supported(a)) st = MCI_E_UNSUPPORTED;
+        return st;
+    };
+    mci_status st = axis(ax, W, bx, ox, cx);
+    if (st != MCI_OK) return st;
+    st = axis(ay, H, by, oy, cy);
+    if (st != MCI_OK) return st;
+    p->cond_max = std::max(cx, cy);
+    const size_t nx = bx.size();
+    bx.insert(bx.end(), by.begin(), by.end());
+    if ((st = upload<T>(p, bx)) != MCI_OK) return st;
+    set_ptrs(ax, p->tables, ox, sizeof(T));
+    set_ptrs(ay, (char *)p->tables + nx * sizeof(T), oy, sizeof(T));
+    p->ax = ax;
+    p->ay = ay;
+    p->Mx = p->My = 3;
+    p->Nx = W; p->Ny = H; p->Lx = s * W; p->Ly = s * H;
+    p->path = mci::PATH_SISR;
+    const size_t per = mci::sisr_ws_per_image((int)H, (int)W, s, p->dtype);
+    const size_t ws_mb = getenv("MCI_2D_WS_MB") ? (size_t)atoi(getenv("MCI_2D_WS_MB")) : 256;
+    p->ws_units = std::max<int64_t>(1, (int64_t)((ws_mb << 20) / per));
+    p->ws_bytes = per * p->ws_units;
+    if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
+    return MCI_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci_system *sys,
@@ -603,6 +653,39 @@ mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci
         return s;
     }
     *out = p;
+    return MCI_OK;
+}
+
+mci_status mci_plan_create_sisr(mci_plan *out, int64_t H, int64_t W, int scale, mci_dtype dtype) {
+    if (!out) return MCI_E_ARG;
+    *out = nullptr;
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || scale < 3 || H < 2 || W < 2 || H > (1 << 20) || W > (1 << 20))
+        return MCI_E_ARG;
+    mci_plan p = new (std::nothrow) mci_plan_s();
+    if (!p) return MCI_E_ARG;
+    p->dtype = dtype;
+    mci_status s = dtype == MCI_F64 ? create_sisr<double>(p, H, W, scale) : create_sisr<float>(p, H, W, scale);
+    if (s != MCI_OK) {
+        mci_plan_destroy(p);
+        return s;
+    }
+    *out = p;
+    return MCI_OK;
+}
+
+mci_status mci_execute_sisr(mci_plan p, int64_t n_images, const void *lr, void *hr, void *stream) {
+    if (!p || p->path != mci::PATH_SISR || n_images < 0) return MCI_E_ARG;
+    if (n_images == 0) return MCI_OK;
+    if (!lr || !hr) return MCI_E_ARG;
+    const size_t es = esize(p->dtype);
+    const int H = (int)p->Ny, W = (int)p->Nx, s = (int)(p->Lx / p->Nx);
+    for (int64_t i0 = 0; i0 < n_images; i0 += p->ws_units) {
+        const int64_t ni = std::min<int64_t>(p->ws_units, n_images - i0);
+        cudaError_t e = mci::launch_sisr_chunk(p->ax, p->ay, ni, H, W, s, (const char *)lr + i0 * (int64_t)H * W * es,
+                                               (char *)hr + i0 * (int64_t)s * H * s * W * es, p->ws,
+                                               (cudaStream_t)stream, nullptr);
+        if (e != cudaSuccess) return MCI_E_CUDA;
+    }
     return MCI_OK;
 }
 
@@ -751,6 +834,7 @@ int64_t mci_plan_launches(mci_plan p, int64_t batch) {
     if (!p || batch <= 0) return 0;
     if (p->path == mci::PATH_FUSED) return 1;
     const int64_t chunks = (batch + p->ws_units - 1) / p->ws_units;
+    if (p->path == mci::PATH_SISR) return 5 * chunks;  // fd rows, MCI x, fd cols, MCI y, transpose
     return p->path == mci::PATH_FOURSTEP ? 4 * chunks : 2 * chunks;
 }
 

@@ -165,6 +165,9 @@ CONFIGS = {
     # SURVEY.md §8(f) NEXT-3 measurement line: config-2 rows evaluated at arbitrary points
     7: dict(M=3, N=1024, L=16384, batch=2048, npts=1024,
             bank=[("identity",), ("derivative", 1), ("derivative", 2)], dtype="f32"),
+    # SURVEY.md §8(f) NEXT-2 measurement line: the paper's x3 SISR on 510 x 510 images
+    # (LR 170 x 170, "Baby (510 x 510)"), 64 synthetic images
+    8: dict(H=170, W=170, scale=3, batch=64, dtype="f32"),
 }
 
 
@@ -392,3 +395,31 @@ def cfg5_images(indices, seed: int = 5, size: int = 2048, N: int = 512):
         g[i] = image_channels(img, N)
         truths.append(img)
     return g, truths
+
+
+# ---- SISR inputs -----------------------------
+def gaussian_blur_5x5(img: np.ndarray, sigma: float = 1.0) -> np.ndarray:
+    """5 x 5 Gaussian blur, standard deviation sigma, normalised, periodic boundary
+    (the paper's step 1; periodic to match the periodic signal model)."""
+    ax = np.arange(-2, 3)
+    k1 = np.exp(-ax * ax / (2.0 * sigma * sigma))
+    k1 /= k1.sum()
+    out = np.zeros_like(img, dtype=np.float64)
+    for dy in range(5):
+        for dx in range(5):
+            out += k1[dy] * k1[dx] * np.roll(np.roll(img, ax[dy], axis=0), ax[dx], axis=1)
+    return out
+
+
+def sisr_images(indices, hr_size: int = 510, scale: int = 3, seed: int = 8):
+    """SISR workload: HR ground truths (the config-5 generator at hr_size, periodic),
+    blurred 5x5 / sigma 1 and decimated by `scale` at phase 0 -> LR float32 [I][H][W]."""
+    indices = list(indices)
+    n = hr_size // scale
+    lr = np.empty((len(indices), n, n), dtype=np.float32)
+    hrs = []
+    for i, ix in enumerate(indices):
+        hr = cfg5_image(ix, seed=seed, size=hr_size, corr=4.0, shapes=12)
+        lr[i] = gaussian_blur_5x5(hr)[::scale, ::scale]
+        hrs.append(hr)
+    return lr, hrs

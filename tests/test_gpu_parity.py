@@ -487,3 +487,40 @@ def test_cfg7_full_batch_sampled():
     for i in (0, 1000, c["batch"] - 1):
         ref = P.eval_offgrid(g[i], t.astype(np.float64))
         assert row_rel(f[i].double().cpu().numpy(), ref) < F32_TOL
+
+
+# -------------------------------------------------------------------------- NEXT-2: SISR
+@pytest.mark.parametrize("H,W,s,dtype", [(14, 18, 3, "f32"), (23, 17, 3, "f64"), (40, 36, 4, "f32"),
+                                         (32, 32, 4, "f32")])
+def test_sisr_vs_oracle(H, W, s, dtype):
+    """the paper's SISR scheme (rows then columns, centred
+    differences, Example-2 bank) vs oracle.sisr (pinned P11)."""
+    m = mci()
+    npdt, tdt = (np.float64, torch.float64) if dtype == "f64" else (np.float32, torch.float32)
+    lr = np.random.default_rng(H * W + s).standard_normal((3, H, W)).astype(npdt)
+    plan = m.SisrPlan(H, W, s, dtype=dtype)
+    hr = plan.execute(torch.from_numpy(lr).cuda()).double().cpu().numpy()
+    tol = F64_TOL if dtype == "f64" else F32_TOL
+    for i in range(3):
+        ref = oracle.sisr(lr[i].astype(np.float64), s)
+        assert np.linalg.norm(hr[i] - ref) / np.linalg.norm(ref) < tol
+        assert np.max(np.abs(hr[i][::s, ::s] - lr[i])) < (1e-10 if dtype == "f64" else 1e-4) * np.abs(lr[i]).max()
+
+
+def test_cfg8_full_batch_sampled():
+    """Config 8 (NEXT-2 measurement line: 64 LR 170 x 170 -> 510 x 510) in the bench
+    launch: sampled images vs oracle.sisr; PSNR vs the HR ground truth is sane."""
+    m = mci()
+    c = synth.CONFIGS[8]
+    lr, hrs = synth.sisr_images(range(4))
+    lr_b = np.ascontiguousarray(np.tile(lr, (c["batch"] // 4, 1, 1)))
+    plan = m.SisrPlan(c["H"], c["W"], c["scale"])
+    out = plan.execute(torch.from_numpy(lr_b).cuda())
+    torch.cuda.synchronize()
+    for i in (0, c["batch"] - 1):
+        ref = oracle.sisr(lr_b[i].astype(np.float64), c["scale"])
+        got = out[i].double().cpu().numpy()
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) < F32_TOL
+    got = np.clip(out[0].double().cpu().numpy(), 0, 255)
+    psnr = 10 * np.log10(255.0 ** 2 / np.mean((got - hrs[0]) ** 2))
+    assert psnr > 20.0, psnr

@@ -361,3 +361,31 @@ def test_cfg1_exact_fp64():
     d = synth.cfg1()
     P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
     assert rel(P.eval(d["g"])[0], d["truth"][0]) < 1e-12
+
+
+# ---------------------------------------------------------------- P11: SISR pipeline (NEXT-2)
+def test_p11_sisr_consistency_constant_and_smooth():
+    """oracle.sisr: (a) the identity channel is reproduced at the
+    sample sites of both passes, so HR[3i][3j] = LR[i][j] exactly (Theorem consistency,
+    PAPER.md:546-585); (b) a constant image stays constant; (c) for a smooth separable
+    trig polynomial the centred differences are O(d^2)-accurate derivatives, so the
+    output matches the true fine-grid image to that order (a wrong 2 pi / N derivative
+    scaling, a sign or a swapped channel fails by O(1))."""
+    rng = np.random.default_rng(11)
+    H, W, s = 14, 18, 3
+    lr = rng.standard_normal((H, W))
+    hr = oracle.sisr(lr, s)
+    assert hr.shape == (s * H, s * W)
+    assert np.max(np.abs(hr[::s, ::s] - lr)) < 1e-10
+    c = oracle.sisr(np.full((H, W), 2.5), s)
+    assert np.max(np.abs(c - 2.5)) < 1e-10
+    H, W = 40, 36
+    x = np.arange(W) * 2 * np.pi / W
+    y = np.arange(H) * 2 * np.pi / H
+    f = lambda yy, xx: np.cos(yy[:, None] * 2 + 0.3) * np.sin(xx[None, :] + 0.1)
+    out = oracle.sisr(f(y, x), s)
+    xf = np.arange(s * W) * 2 * np.pi / (s * W)
+    yf = np.arange(s * H) * 2 * np.pi / (s * H)
+    truth = f(yf, xf)
+    err = np.linalg.norm(out - truth) / np.linalg.norm(truth)
+    assert err < 5e-3, err
