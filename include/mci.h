@@ -76,8 +76,13 @@ typedef struct {
 
 enum {
     MCI_OUT_HILBERT = 1u, /* plan also produces Hf                                            */
-    MCI_OFFGRID = 2u      /* plan also evaluates at arbitrary points (mci_execute_offgrid); it is
+    MCI_OFFGRID = 2u,     /* plan also evaluates at arbitrary points (mci_execute_offgrid); it is
                              built on the arbitrary-length path                                */
+    MCI_COMPLEX = 4u      /* complex-valued f: complex channel samples
+                             in, T_N f itself out (no real part, no Hermitian assembly); any bank
+                             (Hermitian or not) and any band K1 (mci_plan_create_band), e.g.
+                             Example 5.  Not combinable with MCI_OUT_HILBERT or
+                             MCI_OFFGRID in this build (MCI_E_UNSUPPORTED).                      */
 };
 
 /* ---- plans ------------------------------------------------------------------------ */
@@ -96,6 +101,14 @@ enum {
  * < 1e-12 * max row norm (SPEC.md:184 reading).  Host arrays are copied. */
 mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci_system *sys,
                            const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags);
+
+/* As mci_plan_create with an explicit band {K1 .. K1+M*N-1} (any integer K1; the real-output
+ * paths need the Hermitian reading of the band, see mci_plan_create, so K1 is only free with
+ * MCI_COMPLEX or when K1 = -floor(M*N/2)).  With MCI_COMPLEX, mci_execute_1d takes g as
+ * [batch][M][N] complex (interleaved re, im in the plan dtype) and writes f as [batch][L]
+ * complex; hf must be NULL. */
+mci_status mci_plan_create_band(mci_plan *out, int M, int64_t N, int64_t L, int64_t K1, const mci_system *sys,
+                                const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags);
 
 /* 2D separable plan: tensor bank {sx} x {sy}; channel images
  * g[n][My][Mx][Ny][Nx]; output [n][scale*Ny][scale*Nx].  Re is taken after

@@ -167,6 +167,25 @@ class OraclePlan:
         assert rc == 0
         return out
 
+    def eval_complex(self, g):
+        """T_N f on the L points, complex (no real part), for complex rows g[R][M][N]
+        (SURVEY.md §8(f) NEXT-3, C2C): f(t_p) = (1/N) sum_m sum_n g_m[n] y_m(t_p - t_n) with
+        the complex kernels y_m(t) = sum_k r_m(k) e^{ikt} (Eq. appxi operator PAPER.md:311,
+        544; Theorem 1).  Direct sums (small sizes)."""
+        g = np.asarray(g, dtype=np.complex128).reshape(-1, self.M, self.N)
+        L, N = self.L, self.N
+        assert L % N == 0
+        s = np.arange(L)
+        k = np.arange(self.K1, self.K1 + self.MN)
+        Yc = self.r @ np.exp(2j * np.pi * np.mod(np.outer(k, s), L) / L)   # [M][L], y_m(2 pi s / L)
+        out = np.zeros((g.shape[0], L), dtype=np.complex128)
+        step = L // N
+        for n in range(N):
+            idx = (s - n * step) % L
+            for m in range(self.M):
+                out += g[:, m, n, None] * Yc[m, idx][None, :]
+        return out / N
+
     def eval_offgrid(self, g_row, t, hilbert=False):
         g = np.ascontiguousarray(np.asarray(g_row, dtype=np.float64).reshape(self.M, self.N))
         t = np.ascontiguousarray(np.asarray(t, dtype=np.float64))

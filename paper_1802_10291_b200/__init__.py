@@ -25,6 +25,8 @@ MCI_OK, MCI_E_ARG, MCI_E_BAND, MCI_E_ALIAS, MCI_E_SINGULAR, MCI_E_SIZE, MCI_E_CU
 MCI_F32, MCI_F64 = 0, 1
 MCI_OUT_HILBERT = 1
 MCI_OFFGRID = 2
+MCI_COMPLEX = 4
+K1_DEFAULT = -(2 ** 63)
 _KIND = {"identity": 0, "derivative": 1, "hilbert": 2, "delay": 3, "table": 4}
 PATH_NAMES = {0: "fused", 1: "fourstep", 2: "2d", 3: "sisr"}
 
@@ -54,6 +56,8 @@ def _lib_handle():
         vp, i64, i32, u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint
         L.mci_plan_create.argtypes = [ctypes.POINTER(vp), i32, i64, i64, vp, vp, i32, i32, u32]
         L.mci_plan_create.restype = i32
+        L.mci_plan_create_band.argtypes = [ctypes.POINTER(vp), i32, i64, i64, i64, vp, vp, i32, i32, u32]
+        L.mci_plan_create_band.restype = i32
         L.mci_plan_create_2d.argtypes = [ctypes.POINTER(vp), i32, i64, vp, i32, i64, vp, i32, i32, u32]
         L.mci_plan_create_2d.restype = i32
         L.mci_plan_destroy.argtypes = [vp]
@@ -133,19 +137,22 @@ def _check(status, what):
 class Plan:
     """1D MCI plan: M channels x N samples -> L outputs (f, optionally Hf)."""
 
-    def __init__(self, M, N, L, bank, null_bins=(), dtype="f32", hilbert=False, offgrid=False):
+    def __init__(self, M, N, L, bank, null_bins=(), dtype="f32", hilbert=False, offgrid=False,
+                 complex=False, K1=None):
         lib = _lib_handle()
         self.M, self.N, self.L = int(M), int(N), int(L)
         self.dtype = dtype
         self.hilbert = bool(hilbert)
         self.offgrid = bool(offgrid)
+        self.complex = bool(complex)
         sys_arr, self._keep = _systems(bank)
         nb = np.ascontiguousarray(np.asarray(list(null_bins), dtype=np.int64))
         h = ctypes.c_void_p()
-        st = lib.mci_plan_create(ctypes.byref(h), self.M, self.N, self.L, ctypes.addressof(sys_arr),
-                                 nb.ctypes.data if len(nb) else None, len(nb),
-                                 MCI_F64 if dtype == "f64" else MCI_F32,
-                                 (MCI_OUT_HILBERT if hilbert else 0) | (MCI_OFFGRID if offgrid else 0))
+        flags = (MCI_OUT_HILBERT if hilbert else 0) | (MCI_OFFGRID if offgrid else 0) | (MCI_COMPLEX if complex else 0)
+        st = lib.mci_plan_create_band(ctypes.byref(h), self.M, self.N, self.L,
+                                      K1_DEFAULT if K1 is None else int(K1), ctypes.addressof(sys_arr),
+                                      nb.ctypes.data if len(nb) else None, len(nb),
+                                      MCI_F64 if dtype == "f64" else MCI_F32, flags)
         _check(st, "mci_plan_create")
         self._h = h
 
@@ -166,6 +173,8 @@ class Plan:
 
     def torch_dtype(self):
         import torch
+        if self.complex:
+            return torch.complex128 if self.dtype == "f64" else torch.complex64
         return torch.float64 if self.dtype == "f64" else torch.float32
 
     def execute(self, g, f=None, hf=None, stream=None):

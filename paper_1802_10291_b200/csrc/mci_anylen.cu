@@ -40,6 +40,7 @@ template <typename T> struct AnyArgs {
     const cv<T> *twL;  // [L] e^{+2 pi i m / L}
     int qsm;           // Q~ copied to shared memory (else read through L1)
     int offgrid;       // evaluate at the points tp[0 .. npts) instead of the L grid (NEXT-3)
+    int cplx;          // complex f (NEXT-3 C2C): g, f complex (V), T_N f without real part
     const T *tp;
     int npts;
 };
@@ -308,8 +309,8 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
     using namespace anyk;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, N = a.N, L = a.L, MN = a.MN, K1 = a.K1, Kmax = a.Kmax;
-    const int RP = (a.analytic || a.offgrid) ? 1 : 2;
-    const int bl = max(((RP * M + 1) / 2) * N, L);
+    const int RP = (a.analytic || a.offgrid || a.cplx) ? 1 : 2;
+    const int bl = max((a.cplx ? M : (RP * M + 1) / 2) * N, L);
     V *twN = reinterpret_cast<V *>(smem_raw);
     V *twL = twN + N;
     V *Qs = twL + L;
@@ -354,14 +355,33 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
         const RowAddr &ra = a.ra;
         const int64_t row0 = u * RP;
         const int nr = (int)min((int64_t)RP, a.rows - row0);  // rows in this unit
-        const int nvc = nr * M, npv = (nvc + 1) / 2;            // real channels, complex FFTs
+        const int nvc = nr * M, npv = a.cplx ? M : (nvc + 1) / 2;  // real channels, complex FFTs
         auto chan = [&](int vc) {  // address of virtual channel vc = rl M + m
             const int64_t row = row0 + vc / M;
             return a.g + (row / (ra.D0 * ra.D1)) * ra.s2 + ((row / ra.D0) % ra.D1) * ra.s1 + (row % ra.D0) * ra.s0 +
                    (int64_t)(vc % M) * ra.cs;
         };
-        // ---- load channel pairs z_c = g_{2c} + i g_{2c+1}, per-channel exact power-of-two scaling
-        for (int c = 0; c < npv; ++c) {
+        // ---- load channel pairs z_c = g_{2c} + i g_{2c+1} (complex mode: z_m = g_m), per-channel
+        //      exact power-of-two scaling
+        if (a.cplx) {
+            const V *gc = reinterpret_cast<const V *>(a.g);
+            const int64_t rb = (row0 / (ra.D0 * ra.D1)) * ra.s2 + ((row0 / ra.D0) % ra.D1) * ra.s1 + (row0 % ra.D0) * ra.s0;
+            for (int c = 0; c < M; ++c) {
+                T mx = 0;
+                for (int n = lane; n < N; n += G) {
+                    const V v = gc[rb + (int64_t)c * ra.cs + (int64_t)n * ra.ss];
+                    b0[c * N + n] = v;
+                    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+                }
+                mx = group_max<T, G>(mx, red);
+                if (lane == 0) {
+                    int e0 = 0;
+                    if (mx > 0) frexp(mx, &e0);
+                    escale[2 * c] = escale[2 * c + 1] = e0;
+                }
+            }
+        }
+        for (int c = 0; c < (a.cplx ? 0 : npv); ++c) {
             T m0 = 0, m1 = 0;
             const T *p0 = chan(2 * c), *p1 = (2 * c + 1 < nvc) ? chan(2 * c + 1) : nullptr;
             for (int n = lane; n < N; n += G) {
@@ -405,10 +425,16 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
             for (int l = 0; l < 8; ++l) v[l] = V{0, 0};
             for (int m = 0; m < M; ++m) {
                 const int vc = rl * M + m;
-                const V zc = Z[(vc >> 1) * N + q], zm = cconj(Z[(vc >> 1) * N + qm]);
-                V gm = (vc & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}  // (zc - zm) / (2i)
-                                : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};  // (zc + zm) / 2
-                gm = V{ldexp(gm.x, escale[vc]), ldexp(gm.y, escale[vc])};
+                V gm;
+                if (a.cplx) {  // own FFT per channel: G_m = Z_m
+                    const V zc = Z[m * N + q];
+                    gm = V{ldexp(zc.x, escale[2 * m]), ldexp(zc.y, escale[2 * m])};
+                } else {
+                    const V zc = Z[(vc >> 1) * N + q], zm = cconj(Z[(vc >> 1) * N + qm]);
+                    gm = (vc & 1) ? V{(T)0.5 * (zc.y - zm.y), (T)-0.5 * (zc.x - zm.x)}  // (zc - zm) / (2i)
+                                  : V{(T)0.5 * (zc.x + zm.x), (T)0.5 * (zc.y + zm.y)};  // (zc + zm) / 2
+                    gm = V{ldexp(gm.x, escale[vc]), ldexp(gm.y, escale[vc])};
+                }
                 const V *qrow = Qt + ((int64_t)q * M + m) * M;
 #pragma unroll
                 for (int l = 0; l < 8; ++l)
@@ -468,7 +494,10 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
         }
         for (int i = lane; i < L; i += G) {
             V z = V{0, 0};
-            if (!a.analytic) {  // Z0(i) + i Z1(i), Zr = row r's folded Hermitian spectrum
+            if (a.cplx) {  // T_N f: a(k) at bin k mod L (M N <= L: at most one k per bin)
+                if (i >= K1 && i < K1 + MN) z = A[i - K1];
+                else if (i - L >= K1 && i - L < K1 + MN) z = A[i - L - K1];
+            } else if (!a.analytic) {  // Z0(i) + i Z1(i), Zr = row r's folded Hermitian spectrum
                 for (int rl = 0; rl < nr; ++rl) {
                     V zr = V{0, 0};
                     if (i <= Kmax) zr = xf(rl, i);
@@ -483,6 +512,12 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
         }
         gsync<G>();
         V *out = fft_any<T, G>(b0, b1, L, 1, a.rl, +1, twL, blL, lane);
+        if (a.cplx) {
+            V *fo = reinterpret_cast<V *>(a.f) + row0 * (int64_t)L;
+            for (int p = lane; p < L; p += G) fo[p] = out[p];
+            gsync<G>();
+            continue;
+        }
         T *frow = a.f + row0 * (int64_t)L;
         T *hrow = a.analytic ? a.hf + row0 * (int64_t)L : (nr > 1 ? frow + L : nullptr);  // Hf, or row 1's f
         for (int p = lane; p < L; p += G) {
@@ -496,8 +531,9 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
 
 // shared memory: root tables + Q~ (if small) + per row group [2 bl + MN] complex values
 static size_t group_elems(const Axis1D &ax) {
-    const int64_t rp = ax.analytic ? 1 : 2;  // rows per unit (real output pairs rows)
-    return (size_t)(2 * std::max<int64_t>(((rp * ax.M + 1) / 2) * ax.N, ax.L) +
+    const int64_t rp = (ax.analytic || ax.cplx) ? 1 : 2;  // rows per unit (real output pairs rows)
+    const int64_t nfft = ax.cplx ? ax.M : (rp * ax.M + 1) / 2;
+    return (size_t)(2 * std::max<int64_t>(nfft * ax.N, ax.L) +
                     std::max<int64_t>(rp * ax.M * ax.N, 2 * std::max(ax.radN.bM, ax.radL.bM)));
 }
 static size_t blue_elems(const AnyRadix &r) { return r.bp ? (size_t)(r.bp + 3 * r.bM) : 0; }
@@ -529,6 +565,7 @@ static cudaError_t anylen_launch_t(const Axis1D &ax, const RowAddr &ra, int64_t 
                                    cudaStream_t st, const void *tp = nullptr, int64_t npts = 0) {
     AnyArgs<T> a;
     a.offgrid = tp != nullptr;
+    a.cplx = ax.cplx;
     a.tp = (const T *)tp;
     a.npts = (int)npts;
     a.M = ax.M; a.N = (int)ax.N; a.L = (int)ax.L; a.MN = (int)(ax.M * ax.N);

@@ -43,6 +43,7 @@ struct Axis1D {
                       // 4 arbitrary lengths (mci_anylen.cu: Qt has all N classes, twF = e^{-2 pi i m/N} [N],
                       //   twLhi = e^{+2 pi i m/L} [L], band K1 = -floor(MN/2))
     int64_t K1 = 0;   // lowest band frequency (arbitrary-length path)
+    int cplx = 0;     // complex f: complex channels in, T_N f out (arbitrary-length path, MCI_COMPLEX)
     AnyRadix radN, radL;
 };
 

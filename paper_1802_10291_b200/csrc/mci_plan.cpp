@@ -310,29 +310,33 @@ template <typename T> void push_bluestein(std::vector<T> &blob, int p, int M, in
     push_roots(blob, M, M, 1, +1);
 }
 
+constexpr int64_t K1_DEFAULT = INT64_MIN;
+
 template <typename T>
 mci_status build_axis_any(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_system *sys,
                           const int64_t *null_bins, int n_null, bool analytic, std::vector<T> &blob,
-                          std::vector<size_t> &offs, double &cond_max) {
+                          std::vector<size_t> &offs, double &cond_max, int64_t K1_in = K1_DEFAULT,
+                          bool cplx = false) {
     if (M < 1 || M > 8 || !sys) return MCI_E_ARG;
     if (N < 2) return MCI_E_SIZE;
     const int64_t MN = (int64_t)M * N;
     if (MN < 2) return MCI_E_BAND;
     if (L < MN || L % N) return MCI_E_ALIAS;
-    const int64_t K1 = -(MN / 2);
+    const int64_t K1 = K1_in == K1_DEFAULT ? -(MN / 2) : K1_in;
     for (int m = 0; m < M; ++m) {
         const mci_system &s = sys[m];
         if (s.kind < MCI_SYS_IDENTITY || s.kind > MCI_SYS_TABLE) return MCI_E_ARG;
         if (s.kind == MCI_SYS_DERIVATIVE && s.order < 0) return MCI_E_ARG;
         if (s.kind == MCI_SYS_TABLE) {
             if (!s.table) return MCI_E_ARG;
-            for (int64_t k = 1; -k >= K1 && k < K1 + MN; ++k) {  // Hermitian requirement (real output)
+            for (int64_t k = 1; !cplx && -k >= K1 && k < K1 + MN; ++k) {  // Hermitian requirement (real output)
                 cd a = sys_multiplier(s, K1, k), b = sys_multiplier(s, K1, -k);
                 if (std::abs(a - std::conj(b)) > 1e-12 * (1 + std::abs(a))) return MCI_E_UNSUPPORTED;
             }
         }
     }
     ax.M = M; ax.N = N; ax.L = L; ax.K = -K1; ax.K1 = K1; ax.analytic = analytic ? 1 : 0;
+    ax.cplx = cplx ? 1 : 0;
     ax.S = L; ax.R = 1;
     ax.radN = radix_plan(N);
     ax.radL = radix_plan(L);
@@ -428,15 +432,16 @@ void set_ptrs(mci::Axis1D &ax, void *base, const std::vector<size_t> &offs, size
 
 template <typename T>
 mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *sys, const int64_t *null_bins,
-                     int n_null, unsigned flags) {
+                     int n_null, unsigned flags, int64_t K1 = K1_DEFAULT) {
     std::vector<T> blob;
     std::vector<size_t> offs;
     const bool analytic = flags & MCI_OUT_HILBERT;
     mci::Axis1D ax;
     ax.dtype = p->dtype;
     mci_status s;
-    if (use_anylen(M, N, L)) {  // arbitrary lengths / odd band
-        s = build_axis_any<T>(ax, M, N, L, sys, null_bins, n_null, analytic, blob, offs, p->cond_max);
+    const bool cplx = flags & MCI_COMPLEX;
+    if (cplx || use_anylen(M, N, L)) {  // arbitrary lengths / odd band / complex output
+        s = build_axis_any<T>(ax, M, N, L, sys, null_bins, n_null, analytic, blob, offs, p->cond_max, K1, cplx);
         if (s != MCI_OK) return s;
         if (!mci::anylen_supported(ax)) return MCI_E_SIZE;
         p->path = mci::PATH_FUSED;
@@ -635,13 +640,38 @@ mci_status create_sisr(mci_plan p, int64_t H, int64_t W, int s) {
 
 extern "C" {
 
+mci_status mci_plan_create_band(mci_plan *out, int M, int64_t N, int64_t L, int64_t K1, const mci_system *sys,
+                                const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags) {
+    if (!out) return MCI_E_ARG;
+    *out = nullptr;
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID | MCI_COMPLEX)) ||
+        n_null < 0 || (n_null > 0 && !null_bins))
+        return MCI_E_ARG;
+    if ((flags & MCI_COMPLEX) && (flags & (MCI_OUT_HILBERT | MCI_OFFGRID))) return MCI_E_UNSUPPORTED;
+    // real output: the Hermitian assembly of the paths needs the default band
+    if (!(flags & MCI_COMPLEX) && K1 != K1_DEFAULT && K1 != -(((int64_t)M * N) / 2)) return MCI_E_UNSUPPORTED;
+    mci_plan p = new (std::nothrow) mci_plan_s();
+    if (!p) return MCI_E_ARG;
+    p->dtype = dtype;
+    p->flags = flags;
+    mci_status s = dtype == MCI_F64 ? create_1d<double>(p, M, N, L, sys, null_bins, n_null, flags, K1)
+                                    : create_1d<float>(p, M, N, L, sys, null_bins, n_null, flags, K1);
+    if (s != MCI_OK) {
+        mci_plan_destroy(p);
+        return s;
+    }
+    *out = p;
+    return MCI_OK;
+}
+
 mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci_system *sys,
                            const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags) {
     if (!out) return MCI_E_ARG;
     *out = nullptr;
-    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID)) || n_null < 0 ||
-        (n_null > 0 && !null_bins))
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID | MCI_COMPLEX)) ||
+        n_null < 0 || (n_null > 0 && !null_bins))
         return MCI_E_ARG;
+    if ((flags & MCI_COMPLEX) && (flags & (MCI_OUT_HILBERT | MCI_OFFGRID))) return MCI_E_UNSUPPORTED;
     mci_plan p = new (std::nothrow) mci_plan_s();
     if (!p) return MCI_E_ARG;
     p->dtype = dtype;
@@ -757,8 +787,9 @@ static mci_status exec_host(mci_plan p, int64_t units, const void *g, void *f, v
         in_u = (size_t)p->My * p->Mx * p->Ny * p->Nx * es;
         out_u = (size_t)p->Ly * p->Lx * es;
     } else {
-        in_u = (size_t)p->ax.M * p->ax.N * es;
-        out_u = (size_t)p->ax.L * es;
+        const size_t cf = (p->flags & MCI_COMPLEX) ? 2 : 1;  // complex: two scalars per value
+        in_u = (size_t)p->ax.M * p->ax.N * es * cf;
+        out_u = (size_t)p->ax.L * es * cf;
         nout = (p->flags & MCI_OUT_HILBERT) ? 2 : 1;
     }
     int64_t chunk = std::max<int64_t>(1, (int64_t)((64u << 20) / (out_u * nout)));

@@ -524,3 +524,53 @@ def test_cfg8_full_batch_sampled():
     got = np.clip(out[0].double().cpu().numpy(), 0, 255)
     psnr = 10 * np.log10(255.0 ** 2 / np.mean((got - hrs[0]) ** 2))
     assert psnr > 20.0, psnr
+
+
+# -------------------------------------------------------------------------- NEXT-3: complex output
+@pytest.mark.parametrize("M,N,L,bank,K1,dtype", [
+    (2, 10, 40, [("identity",), ("hilbert",)], -9, "f32"),      # Example 5 (N = 9: band -9..10)
+    (2, 64, 256, [("identity",), ("derivative", 1)], -20, "f32"),
+    (3, 30, 180, [("delay", 0.0), ("delay", 0.37), ("delay", 1.3)], -41, "f64"),
+    (2, 128, 256, [("identity",), ("derivative", 1)], None, "f32"),  # L = MN, default band
+])
+def test_complex_output_vs_oracle(M, N, L, bank, K1, dtype):
+    """complex channel samples -> complex T_N f on any band
+    (Example 5, PAPER.md:466-520) vs the oracle's complex direct formula (pinned P12);
+    a bandlimited complex signal is reconstructed exactly."""
+    m = mci()
+    cdt = torch.complex128 if dtype == "f64" else torch.complex64
+    rng = np.random.default_rng(N + M)
+    g = rng.standard_normal((3, M, N)) + 1j * rng.standard_normal((3, M, N))
+    plan = m.Plan(M, N, L, bank, dtype=dtype, complex=True, K1=K1)
+    gt = torch.from_numpy(g).to("cuda", dtype=cdt)
+    f = plan.execute(gt)
+    torch.cuda.synchronize()
+    assert f.dtype == cdt and f.shape == (3, L)
+    P = oracle.OraclePlan(M, N, L, bank, K1=K1)
+    ref = P.eval_complex(gt.cpu().numpy().astype(np.complex128))
+    got = f.cpu().numpy().astype(np.complex128)
+    tol = F64_TOL if dtype == "f64" else F32_TOL
+    assert row_rel(got.view(np.float64), ref.view(np.float64)).max() < tol
+
+
+def test_example3_hilbert_channel_null_bin():
+    """Example 3: M = 1, b(n) = -i sgn n on the odd band -N'..N' (2N'+1
+    samples), singular at n = 0; with 0 declared a null bin (Remark 1)
+    the samples of Hf reconstruct f for a(0) = 0 -- vs the oracle and the exact signal."""
+    m = mci()
+    Np = 16
+    N, L = 2 * Np + 1, 4 * (2 * Np + 1)
+    rng = np.random.default_rng(3)
+    k = np.arange(-Np, Np + 1)
+    a = rng.standard_normal(len(k)) + 1j * rng.standard_normal(len(k))
+    a = (a + np.conj(a[::-1])) / 2          # real signal
+    a[Np] = 0.0                              # a(0) = 0
+    tn = 2 * np.pi * np.arange(N) / N
+    hf = np.real((a * (-1j) * np.sign(k)) @ np.exp(1j * np.outer(k, tn)))
+    tp = 2 * np.pi * np.arange(L) / L
+    truth = np.real(a @ np.exp(1j * np.outer(k, tp)))
+    plan = m.Plan(1, N, L, [("hilbert",)], null_bins=[0], dtype="f64")
+    out = run_plan(plan, hf[None, None, :], torch.float64)[0]
+    ref = oracle.OraclePlan(1, N, L, [("hilbert",)], null_bins=[0]).eval(hf[None, None, :])[0]
+    assert row_rel(out, ref) < F64_TOL
+    assert row_rel(out, truth) < 1e-12

@@ -389,3 +389,40 @@ def test_p11_sisr_consistency_constant_and_smooth():
     truth = f(yf, xf)
     err = np.linalg.norm(out - truth) / np.linalg.norm(truth)
     assert err < 5e-3, err
+
+
+# ---------------------------------------------------------------- P12: complex output, general band
+@pytest.mark.parametrize("bank,K1", [
+    ([("identity",), ("hilbert",)], -11),                  # Example 5's band -N..N+1 (N = 11)
+    ([("identity",), ("derivative", 1)], -3),              # shifted band
+    ([("delay", 0.0), ("delay", 0.4), ("delay", 1.1)], -20),
+])
+def test_p12_complex_exact_reconstruction(bank, K1):
+    """Theorem 1 for complex f: any complex trig polynomial on the
+    band [K1, K1 + MN) is reproduced exactly from its channel samples by eval_complex."""
+    M = len(bank)
+    N = 12
+    L = 2 * M * N
+    P = oracle.OraclePlan(M, N, L, bank, K1=K1)
+    rng = np.random.default_rng(abs(K1) + M)
+    k = np.arange(K1, K1 + M * N)
+    a = rng.standard_normal(len(k)) + 1j * rng.standard_normal(len(k))
+    tn = 2 * np.pi * np.arange(N) / N
+    g = np.stack([(a * np.array([P.multiplier(m, kk) for kk in k])) @ np.exp(1j * np.outer(k, tn))
+                  for m in range(M)])[None]
+    tp = 2 * np.pi * np.arange(L) / L
+    truth = a @ np.exp(1j * np.outer(k, tp))
+    out = P.eval_complex(g)[0]
+    assert np.linalg.norm(out - truth) / np.linalg.norm(truth) < 1e-11
+
+
+def test_p12_example5_printed_kernel():
+    """Example 5 (PAPER.md:466-500): M = 2, b = (1, -i sgn n), band -N..N+1, N + 1 samples;
+    the paper prints y_1(t) = (cos((N+1)t) - cos(Nt) + cos t - 1) / (2 cos t - 2)."""
+    Np = 9
+    P = oracle.OraclePlan(2, Np + 1, 4 * (Np + 1), [("identity",), ("hilbert",)], K1=-Np)
+    t = np.linspace(0.1, 6.0, 37)
+    k = np.arange(-Np, Np + 2)
+    y1 = (P.r[0] @ np.exp(1j * np.outer(k, t)))
+    printed = (np.cos((Np + 1) * t) - np.cos(Np * t) + np.cos(t) - 1) / (2 * np.cos(t) - 2)
+    assert np.max(np.abs(y1 - printed)) < 1e-12
