@@ -6,7 +6,7 @@ M=3 channels (f, f', f''), N=1024 samples each -> L=16384 outputs, fp32.
 A step is one pass of the whole hot path (forward DFTs, per-class solves,
 assembly, inverse FFTs, stores) over the batch, i.e. one mci_execute_1d.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..8] [--impl mci|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..9] [--impl mci|reference]
 
 N > 1: one process per GPU (torchrun), each rank runs its own batch (rows are
 independent: weak scaling, no collective on the data path); time = max over
@@ -59,6 +59,10 @@ def workload(cfg):
         return dict(name=f"cfg8: {c['batch']} images {H}x{W} -> {s * H}x{s * W} (SISR x{s}: centred differences, "
                          f"bank 1, ik, -k^2, rows then columns; NEXT-2)",
                     units=c["batch"], outs_per_unit=s * H * s * W, in_per_unit=H * W, out_floats_per_unit=s * H * s * W)
+    if cfg == 9:
+        return dict(name=f"cfg9: eps(f, N) of {c['batch']} spectra x {c['nfreq']} coefficients, M={c['M']}, "
+                         f"N={c['N']}, bank 1, ik, -k^2 (NEXT-4; unit = spectral coefficients)",
+                    units=c["batch"], outs_per_unit=c["nfreq"], in_per_unit=2 * c["nfreq"], out_floats_per_unit=3)
     if cfg == 7:
         return dict(name=f"cfg7: {c['batch']} x (M={c['M']}, N={c['N']}) -> {c['npts']} arbitrary points x 1 out, "
                          f"bank 1, ik, -k^2 (NEXT-3 off-grid)",
@@ -86,6 +90,8 @@ def make_inputs(cfg, rank):
         return synth.cfg2_batch_fast(c["batch"], seed=6 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
     if cfg == 7:
         return synth.cfg2_batch_fast(c["batch"], seed=7 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
+    if cfg == 9:
+        return synth.error_spectra(c["batch"], -(c["M"] * c["N"]) * 2, c["nfreq"], seed=9 + 1000 * rank)
     if cfg == 8:  # 4 distinct images tiled to the batch (content does not change the arithmetic)
         lr, _ = synth.sisr_images(range(4 * rank, 4 * rank + 4))
         return np.ascontiguousarray(np.tile(lr, (c["batch"] // 4, 1, 1)))
@@ -105,6 +111,8 @@ def algorithmic_flops(cfg):
         n, L = c["N"], c["N"] * c["scale"]
         line = 2 * 2.5 * n * lg(n) + 8 * 4 * (n // 2 + 1) + 2.5 * L * lg(L)
         return (2 * n + L) * line  # per image: column pass Mx*Nx = 2n lines, row pass Ly = L lines
+    if cfg == 9:  # per coefficient: M^2 complex multiply-adds (fp64) + norms
+        return c["nfreq"] * (8 * c["M"] ** 2 + 6 * c["M"])
     if cfg == 8:  # per image: H row lines (3 channels, N = W -> sW), then sW column lines
         H, W, s = c["H"], c["W"], c["scale"]
 
@@ -133,6 +141,8 @@ def make_plan(cfg):
         return mci.Plan2D(2, c["N"], c["bank"], 2, c["N"], c["bank"], c["scale"])
     if cfg == 8:
         return mci.SisrPlan(c["H"], c["W"], c["scale"])
+    if cfg == 9:
+        return mci.Plan(c["M"], c["N"], c["L"], c["bank"], analysis=True)
     return mci.Plan(c["M"], c["N"], c["L"], c["bank"], dtype="f64" if cfg == 1 else "f32",
                     hilbert=bool(c.get("hilbert")), offgrid=cfg == 7)
 
@@ -212,6 +222,18 @@ def oracle_sample(cfg, budget_s=12.0, max_steps=None):
                 break
         dt = time.perf_counter() - t0
         return n / dt, f"signal 0, {n} output points (closed-form delay kernel), M*N={M*N} terms each", threads
+    if cfg == 9:
+        P9 = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
+        s9 = make_inputs(9, 0)[:8]
+        t0 = time.perf_counter()
+        n = 0
+        while n < len(s9):
+            oracle.averaged_error(P9, s9[n].astype(np.complex128), -(c["M"] * c["N"]) * 2)
+            n += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return n * c["nfreq"] / dt, f"{n} spectra x {c['nfreq']} coefficients (direct loops)", threads
     if cfg == 8:
         lr, _ = synth.sisr_images([0])
         t0 = time.perf_counter()
@@ -307,6 +329,14 @@ def run_reference(args, rank, world):
             oracle.delay_eval_points(c["M"], c["N"], c["L"], gg[0], pts, threads=threads)
             return len(pts)
         sample = "64 output points of signal 0 per step (closed-form delay kernel)"
+    elif cfg == 9:
+        P9 = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
+        s9 = make_inputs(9, 0)[:4]
+
+        def step(i):
+            oracle.averaged_error(P9, s9[i % 4].astype(np.complex128), -(c["M"] * c["N"]) * 2)
+            return c["nfreq"]
+        sample = "one spectrum per step (direct loops of Eq. averageerror)"
     elif cfg == 8:
         lr8, _ = synth.sisr_images([0])
 
@@ -365,7 +395,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6, 7, 8])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5, 6, 7, 8, 9])
     ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -395,7 +425,7 @@ def main():
 
     g_host = make_inputs(cfg, rank)
     plan = make_plan(cfg)
-    g = torch.from_numpy(g_host).to("cuda", dtype=tdt)
+    g = torch.from_numpy(g_host).to("cuda", dtype=torch.complex64 if cfg == 9 else tdt)
     units = w["units"]
     c = synth.CONFIGS[cfg]
     hilbert = bool(c.get("hilbert"))
@@ -405,6 +435,9 @@ def main():
         hf = None
     elif cfg == 8:
         out = torch.empty((units, c["scale"] * c["H"], c["scale"] * c["W"]), dtype=tdt, device="cuda")
+        hf = None
+    elif cfg == 9:
+        out = torch.empty((units, 3), dtype=tdt, device="cuda")
         hf = None
     elif cfg == 7:
         t_host = synth.offgrid_points(c["npts"], seed=7 + 1000 * rank).astype(np.float32)
@@ -421,6 +454,8 @@ def main():
             plan.execute(g, out)
         elif cfg == 7:
             plan.execute_offgrid(g, tpts, out)
+        elif cfg == 9:
+            plan.averaged_error(g, -(c["M"] * c["N"]) * 2, out)
         else:
             plan.execute(g, out, hf)
 
@@ -478,7 +513,7 @@ def main():
     # end-to-end through the host-buffer C-ABI call (H2D + compute + D2H inside)
     e2e = None
     if not args.no_e2e:
-        gh = torch.from_numpy(g_host).to(tdt).pin_memory()
+        gh = torch.from_numpy(g_host).to(torch.complex64 if cfg == 9 else tdt).pin_memory()
         oh = torch.empty(out.shape, dtype=tdt).pin_memory()
         hh = torch.empty(out.shape, dtype=tdt).pin_memory() if hilbert else None
         e_steps = max(3, min(args.steps, 10))
@@ -489,6 +524,10 @@ def main():
         def estep():
             if cfg == 5:
                 plan.execute_host(gh, oh)
+            elif cfg == 9:  # public device API with the host copies inside the timed step
+                oh.copy_(plan.averaged_error(gh.to("cuda", non_blocking=True), -(c["M"] * c["N"]) * 2),
+                         non_blocking=True)
+                torch.cuda.synchronize()
             elif cfg == 8:  # public device API with the host copies inside the timed step
                 oh.copy_(plan.execute(gh.to("cuda", non_blocking=True)), non_blocking=True)
                 torch.cuda.synchronize()

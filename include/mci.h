@@ -78,11 +78,13 @@ enum {
     MCI_OUT_HILBERT = 1u, /* plan also produces Hf                                            */
     MCI_OFFGRID = 2u,     /* plan also evaluates at arbitrary points (mci_execute_offgrid); it is
                              built on the arbitrary-length path                                */
-    MCI_COMPLEX = 4u      /* complex-valued f: complex channel samples
+    MCI_COMPLEX = 4u,     /* complex-valued f: complex channel samples
                              in, T_N f itself out (no real part, no Hermitian assembly); any bank
                              (Hermitian or not) and any band K1 (mci_plan_create_band), e.g.
                              Example 5.  Not combinable with MCI_OUT_HILBERT or
                              MCI_OFFGRID in this build (MCI_E_UNSUPPORTED).                      */
+    MCI_ANALYSIS = 8u     /* plan also supports mci_consistency_residual and mci_averaged_error
+                             (built-in system kinds only: MCI_SYS_TABLE is MCI_E_UNSUPPORTED)     */
 };
 
 /* ---- plans ------------------------------------------------------------------------ */
@@ -148,6 +150,24 @@ mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, voi
  * is a direct sum over the band in fp64 (cost O(n_pts M N) per row). */
 mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t n_pts, const void *t, void *f,
                                void *hf, void *cuda_stream);
+
+/* ---- error analysis, plans created with MCI_ANALYSIS ----------------
+ * Consistency residual (Theorem consistency): per row,
+ *   out[b] = max_{m,n} |(T_N f * h_m)(t_n) - g_m[n]|,
+ * T_N f the complex reconstruction (a^ on the band), resampled through each channel's multiplier.
+ * g: device [batch][M][N]; out: device [batch] (plan dtype). */
+mci_status mci_consistency_residual(mci_plan p, int64_t batch, const void *g, void *out, void *cuda_stream);
+
+/* Averaged error eps(f, N) (Theorem error, Eq. averageerror) of batches of true
+ * spectra a(n), n = k_lo .. k_lo + n_freq - 1 (zero elsewhere), I_k = {K1+(k-1)N .. K1+kN-1}:
+ *   eps^2 = sum_{n not in I^N} |a(n)|^2
+ *         + sum_{k not in 1..M} sum_{n in I_k} |a(n)|^2 sum_{l=1}^M |sum_m r_m(n+(l-k)N) b_m(n)|^2,
+ *   bound^2 = sum_{n not in I^N} |a|^2 + M (sum_m Omega_m) sum_{n not in I^N} sum_m |a(n) b_m(n)|^2,
+ *   Omega_m = sup_{i in I^N} |r_m(i)|^2 (Eq. errorestimate, Cauchy-Schwarz reading).
+ * spec: device [batch][n_freq] complex (plan dtype, interleaved); out: device [batch][3] =
+ * (eps, bound, out-of-band energy), plan dtype; sums accumulated in fp64. */
+mci_status mci_averaged_error(mci_plan p, int64_t batch, const void *spec, int64_t k_lo, int64_t n_freq,
+                              void *out, void *cuda_stream);
 
 /* g: device [n_images][My][Mx][Ny][Nx]; out: device [n_images][Ly][Lx]. */
 mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out,

@@ -284,3 +284,58 @@ def sisr(lr, scale=3):
 def px_py_out_t(out_cols):
     """Column-pass output [sW][sH] -> image [sH][sW]."""
     return np.ascontiguousarray(np.asarray(out_cols).T)
+
+
+# ---------------------------------------------------------------- error analysis (NEXT-4)
+def band_spectrum(P: OraclePlan, g):
+    """Fourier coefficients of T_N f on the band from channel samples g[M][N] (real or complex):
+    a^(k) = (1/N) sum_m r_m(k) sum_p g_m(t_p) e^{-ik t_p}  (Eq. DFTexpression).
+    Returns (k, a^(k)) for k = K1 .. K1 + MN - 1."""
+    g = np.asarray(g, dtype=np.complex128).reshape(P.M, P.N)
+    k = np.arange(P.K1, P.K1 + P.MN)
+    tp = 2 * np.pi * np.arange(P.N) / P.N
+    E = np.exp(-1j * np.outer(k, tp))                       # [MN][N]
+    return k, np.einsum("mk,mk->k", P.r, (g @ E.T)) / P.N  # sum_m r_m(k) G_m(k) / N
+
+
+def consistency_residual(P: OraclePlan, g):
+    """max_{m,n} |(T_N f * h_m)(t_n) - g_m(t_n)| (Theorem consistency, PAPER.md:546-585;
+    SPEC.md:327-335): reconstruct a^, apply each multiplier b_m on the band, resample."""
+    g = np.asarray(g, dtype=np.complex128).reshape(P.M, P.N)
+    k, a = band_spectrum(P, g)
+    tn = 2 * np.pi * np.arange(P.N) / P.N
+    E = np.exp(1j * np.outer(k, tn))
+    res = 0.0
+    for m in range(P.M):
+        b = np.array([P.multiplier(m, kk) for kk in k])
+        res = max(res, float(np.max(np.abs((a * b) @ E - g[m]))))
+    return res
+
+
+def averaged_error(P: OraclePlan, spec, k_lo):
+    """eps(f, N) of Theorem error (Eq. averageerror) for the true spectrum
+    a(n), n = k_lo .. k_lo + len(spec) - 1 (zero elsewhere); I_k = {K1 + (k-1)N .. K1 + kN - 1}:
+      eps^2 = sum_{n not in I^N} |a(n)|^2
+            + sum_{k not in 1..M} sum_{n in I_k} |a(n)|^2 sum_{l=1}^M |sum_m r_m(n + (l-k)N) b_m(n)|^2.
+    bound (Eq. errorestimate; DESIGN.md reading: Cauchy-Schwarz with Omega_m = sup_band |r_m|^2):
+      bound^2 = sum_{n not in I^N} |a(n)|^2 + M (sum_m Omega_m) sum_{n not in I^N} sum_m |a(n) b_m(n)|^2.
+    Returns (eps, bound, out_of_band_energy).  Direct loops (test infrastructure)."""
+    spec = np.asarray(spec, dtype=np.complex128)
+    M, N, K1 = P.M, P.N, P.K1
+    omega = np.max(np.abs(P.r) ** 2, axis=1)
+    e2 = oob = cs = 0.0
+    for i, an in enumerate(spec):
+        n = k_lo + i
+        kb = (n - K1) // N + 1                               # block index of n
+        if 1 <= kb <= M:
+            continue
+        a2 = abs(an) ** 2
+        oob += a2
+        b = np.array([P.multiplier(m, n) for m in range(M)])
+        w = 0.0
+        for l in range(1, M + 1):
+            e = n + (l - kb) * N                             # the class's element in block l
+            w += abs(np.sum(P.r[:, e - K1] * b)) ** 2
+        e2 += a2 * (1.0 + w)
+        cs += a2 * np.sum(np.abs(b) ** 2)
+    return np.sqrt(e2), np.sqrt(oob + M * omega.sum() * cs), oob

@@ -26,6 +26,7 @@ MCI_F32, MCI_F64 = 0, 1
 MCI_OUT_HILBERT = 1
 MCI_OFFGRID = 2
 MCI_COMPLEX = 4
+MCI_ANALYSIS = 8
 K1_DEFAULT = -(2 ** 63)
 _KIND = {"identity": 0, "derivative": 1, "hilbert": 2, "delay": 3, "table": 4}
 PATH_NAMES = {0: "fused", 1: "fourstep", 2: "2d", 3: "sisr"}
@@ -70,6 +71,10 @@ def _lib_handle():
         L.mci_plan_create_sisr.restype = i32
         L.mci_execute_sisr.argtypes = [vp, i64, vp, vp, vp]
         L.mci_execute_sisr.restype = i32
+        L.mci_consistency_residual.argtypes = [vp, i64, vp, vp, vp]
+        L.mci_consistency_residual.restype = i32
+        L.mci_averaged_error.argtypes = [vp, i64, vp, i64, i64, vp, vp]
+        L.mci_averaged_error.restype = i32
         L.mci_execute_2d.argtypes = [vp, i64, vp, vp, vp]
         L.mci_execute_2d.restype = i32
         L.mci_execute_1d_host.argtypes = [vp, i64, vp, vp, vp]
@@ -138,7 +143,7 @@ class Plan:
     """1D MCI plan: M channels x N samples -> L outputs (f, optionally Hf)."""
 
     def __init__(self, M, N, L, bank, null_bins=(), dtype="f32", hilbert=False, offgrid=False,
-                 complex=False, K1=None):
+                 complex=False, K1=None, analysis=False):
         lib = _lib_handle()
         self.M, self.N, self.L = int(M), int(N), int(L)
         self.dtype = dtype
@@ -148,7 +153,8 @@ class Plan:
         sys_arr, self._keep = _systems(bank)
         nb = np.ascontiguousarray(np.asarray(list(null_bins), dtype=np.int64))
         h = ctypes.c_void_p()
-        flags = (MCI_OUT_HILBERT if hilbert else 0) | (MCI_OFFGRID if offgrid else 0) | (MCI_COMPLEX if complex else 0)
+        flags = ((MCI_OUT_HILBERT if hilbert else 0) | (MCI_OFFGRID if offgrid else 0) |
+                 (MCI_COMPLEX if complex else 0) | (MCI_ANALYSIS if analysis else 0))
         st = lib.mci_plan_create_band(ctypes.byref(h), self.M, self.N, self.L,
                                       K1_DEFAULT if K1 is None else int(K1), ctypes.addressof(sys_arr),
                                       nb.ctypes.data if len(nb) else None, len(nb),
@@ -209,6 +215,31 @@ class Plan:
                                                _dptr(hf) if self.hilbert else None, _stream(stream))
         _check(st, "mci_execute_offgrid")
         return (f, hf) if self.hilbert else f
+
+    def consistency_residual(self, g, out=None, stream=None):
+        """max_{m,n} |(T_N f * h_m)(t_n) - g_m[n]| per row (plan created with analysis=True)."""
+        import torch
+        assert g.is_cuda and g.is_contiguous() and g.dtype == self.torch_dtype()
+        batch = g.numel() // (self.M * self.N)
+        if out is None:
+            out = torch.empty((batch,), dtype=g.dtype, device=g.device)
+        _check(_lib_handle().mci_consistency_residual(self._h, batch, _dptr(g), _dptr(out), _stream(stream)),
+               "mci_consistency_residual")
+        return out
+
+    def averaged_error(self, spec, k_lo, out=None, stream=None):
+        """eps(f, N), its bound and the out-of-band energy per spectrum: spec complex CUDA tensor
+        [batch][n_freq] holding a(k_lo .. k_lo + n_freq - 1).  Returns [batch][3]."""
+        import torch
+        assert spec.is_cuda and spec.is_contiguous() and spec.is_complex()
+        batch, nf = spec.shape
+        rdt = torch.float64 if spec.dtype == torch.complex128 else torch.float32
+        assert rdt == (torch.float64 if self.dtype == "f64" else torch.float32)
+        if out is None:
+            out = torch.empty((batch, 3), dtype=rdt, device=spec.device)
+        _check(_lib_handle().mci_averaged_error(self._h, batch, _dptr(spec), int(k_lo), nf, _dptr(out),
+                                                _stream(stream)), "mci_averaged_error")
+        return out
 
     def execute_host(self, g, f, hf=None):
         """Host buffers (numpy arrays or CPU tensors, ideally pinned): H2D, compute, D2H inside."""

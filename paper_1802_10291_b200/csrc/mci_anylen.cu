@@ -28,6 +28,10 @@
 
 namespace mci {
 
+struct AnyErrSys {
+    SysDev s[8];
+};
+
 template <typename T> struct AnyArgs {
     int M, N, L, K1, Kmax, MN, analytic;
     AnyRadix rn, rl;  // radix plans of the forward (N) and inverse (L) transforms
@@ -41,11 +45,28 @@ template <typename T> struct AnyArgs {
     int qsm;           // Q~ copied to shared memory (else read through L1)
     int offgrid;       // evaluate at the points tp[0 .. npts) instead of the L grid (NEXT-3)
     int cplx;          // complex f (NEXT-3 C2C): g, f complex (V), T_N f without real part
+    int resid;         // consistency residual per row into f[row] (NEXT-4)
+    SysDev sys[8];
     const T *tp;
     int npts;
 };
 
 namespace anyk {
+
+// b_m(k) of a built-in system (fp64): 1, (ik)^order, -i sgn k, e^{ik tau} (mci_plan.cpp sys_multiplier)
+__device__ __forceinline__ double2 bmul(const SysDev &s, int64_t k) {
+    if (s.kind == MCI_SYS_IDENTITY) return make_double2(1.0, 0.0);
+    if (s.kind == MCI_SYS_DERIVATIVE) {
+        double2 v = make_double2(1.0, 0.0);
+        const double kd = (double)k;
+        for (int i = 0; i < s.order; ++i) v = make_double2(-v.y * kd, v.x * kd);
+        return v;
+    }
+    if (s.kind == MCI_SYS_HILBERT) return make_double2(0.0, k > 0 ? -1.0 : (k < 0 ? 1.0 : 0.0));
+    double sn, cs;  // delay
+    sincos(fmod((double)k * s.tau, 6.283185307179586476925286766559), &sn, &cs);
+    return make_double2(cs, sn);
+}
 
 template <typename V> __device__ __forceinline__ V crot(V a, int s) {  // a * (s i)
     return s > 0 ? V{-a.y, a.x} : V{a.y, -a.x};
@@ -309,7 +330,7 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
     using namespace anyk;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int M = a.M, N = a.N, L = a.L, MN = a.MN, K1 = a.K1, Kmax = a.Kmax;
-    const int RP = (a.analytic || a.offgrid || a.cplx) ? 1 : 2;
+    const int RP = (a.analytic || a.offgrid || a.cplx || a.resid) ? 1 : 2;
     const int bl = max((a.cplx ? M : (RP * M + 1) / 2) * N, L);
     V *twN = reinterpret_cast<V *>(smem_raw);
     V *twL = twN + N;
@@ -453,6 +474,43 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
             const V p = af(rl, k), m = cconj(af(rl, -k));
             return V{(T)0.5 * (p.x + m.x), (T)0.5 * (p.y + m.y)};
         };
+        if (a.resid) {
+            // ---- consistency residual (Theorem consistency): for every channel m,
+            //      F_m(q) = sum_l a(j_q + lN) b_m(j_q + lN) (a^ b_m folded mod N); the inverse DFT
+            //      y_m(n) = sum_q F_m(q) e^{2 pi i q n / N} (conj trick through the forward plan) is
+            //      (T_N f * h_m)(t_n); out[row] = max_{m,n} |y_m(n) - g_m[n]|.  All M channels are
+            //      folded first (A is overwritten by the transform's Bluestein buffers).
+            const int q0r = (int)((((int64_t)-K1) % N + N) % N);
+            for (int m = 0; m < M; ++m)
+                for (int q = lane; q < N; q += G) {
+                    int t = q + q0r;
+                    if (t >= N) t -= N;
+                    const int jq = K1 + t;
+                    double fr = 0.0, fi = 0.0;
+                    for (int l = 0; l < M; ++l) {
+                        const V x = A[jq + l * N - K1];
+                        const double2 b = bmul(a.sys[m], (int64_t)jq + (int64_t)l * N);
+                        fr += (double)x.x * b.x - (double)x.y * b.y;
+                        fi += (double)x.x * b.y + (double)x.y * b.x;
+                    }
+                    b0[m * N + q] = V{(T)fr, (T)-fi};  // conj
+                }
+            gsync<G>();
+            V *Y = fft_any<T, G>(b0, b1, N, M, a.rn, -1, twN, blN, lane);
+            T best = 0;
+            for (int m = 0; m < M; ++m) {
+                const T *gm = chan(m);
+                for (int n = lane; n < N; n += G) {
+                    const V y = Y[m * N + n];
+                    const T gv = gm[(int64_t)n * ra.ss];
+                    best = fmax(best, sqrt((y.x - gv) * (y.x - gv) + y.y * y.y));  // y = conj(Y)
+                }
+            }
+            best = group_max<T, G>(best, red);
+            if (lane == 0) a.f[row0] = best;
+            gsync<G>();
+            continue;
+        }
         if (a.offgrid) {
             // ---- off-grid evaluation (Eq. drictexpression / Lemma 2):
             //      f(t) = Xf(0) + 2 sum_{k=1}^{Kmax} Re(Xf(k) e^{ikt}),  Hf(t) = 2 sum_k Im(Xf(k) e^{ikt});
@@ -564,8 +622,10 @@ template <typename T, int G, int GPB>
 static cudaError_t anylen_launch_t(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                                    cudaStream_t st, const void *tp = nullptr, int64_t npts = 0) {
     AnyArgs<T> a;
-    a.offgrid = tp != nullptr;
+    a.offgrid = tp != nullptr && npts > 0;
+    a.resid = tp != nullptr && npts < 0;
     a.cplx = ax.cplx;
+    for (int m = 0; m < 8; ++m) a.sys[m] = ax.sys[m];
     a.tp = (const T *)tp;
     a.npts = (int)npts;
     a.M = ax.M; a.N = (int)ax.N; a.L = (int)ax.L; a.MN = (int)(ax.M * ax.N);
@@ -612,6 +672,83 @@ cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, con
     if (rows <= 0) return cudaSuccess;
     if (n_launches) *n_launches += 1;
     return anylen_dispatch(ax, ra, rows, g, f, hf, st, nullptr, 0);
+}
+
+cudaError_t launch_anylen_residual(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *out,
+                                   cudaStream_t st) {
+    if (rows <= 0) return cudaSuccess;
+    static const int marker = 0;  // residual mode: tp set, npts < 0
+    return anylen_dispatch(ax, ra, rows, g, out, nullptr, st, &marker, -1);
+}
+
+// eps(f, N) of a batch of spectra: one warp per signal, sums in fp64 (Eq. averageerror)
+template <typename T>
+__global__ void mci_avg_error_kernel(const cv<T> *__restrict__ spec, int64_t k_lo, int nf, int64_t batch, int M,
+                                     int N, int64_t K1, const cv<T> *__restrict__ Q, double omega_sum, AnyErrSys sy,
+                                     T *__restrict__ out) {
+    using namespace anyk;
+    const int lane = threadIdx.x & 31;
+    const int64_t sig = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (sig >= batch) return;
+    const cv<T> *a = spec + sig * (int64_t)nf;
+    double e2 = 0, oob = 0, cs = 0;
+    for (int i = lane; i < nf; i += 32) {
+        const int64_t n = k_lo + i;
+        const int64_t d = n - K1;
+        const int64_t kb = (d >= 0 ? d / N : -((-d + N - 1) / N)) + 1;  // block index of n
+        if (kb >= 1 && kb <= M) continue;
+        const cv<T> an = a[i];
+        const double a2 = (double)an.x * an.x + (double)an.y * an.y;
+        const int64_t j = n - (kb - 1) * N;        // the class element of I_1
+        const int q = (int)(((j % N) + N) % N);
+        double2 b[8];
+        double bsum = 0;
+        for (int m = 0; m < M; ++m) {
+            b[m] = bmul(sy.s[m], n);
+            bsum += b[m].x * b[m].x + b[m].y * b[m].y;
+        }
+        double w = 0;
+        for (int l = 0; l < M; ++l) {  // S_l = sum_m r_m(j + lN) b_m(n), r_m(j + lN) = N Q~_q[m][l]
+            double sr = 0, si = 0;
+            for (int m = 0; m < M; ++m) {
+                const cv<T> r = Q[((int64_t)q * M + m) * M + l];
+                const double rr = (double)r.x * N, ri = (double)r.y * N;
+                sr += rr * b[m].x - ri * b[m].y;
+                si += rr * b[m].y + ri * b[m].x;
+            }
+            w += sr * sr + si * si;
+        }
+        e2 += a2 * (1.0 + w);
+        oob += a2;
+        cs += a2 * bsum;
+    }
+    for (int o = 16; o; o >>= 1) {
+        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+        oob += __shfl_xor_sync(0xffffffffu, oob, o);
+        cs += __shfl_xor_sync(0xffffffffu, cs, o);
+    }
+    if (lane == 0) {
+        out[sig * 3 + 0] = (T)sqrt(e2);
+        out[sig * 3 + 1] = (T)sqrt(oob + M * omega_sum * cs);
+        out[sig * 3 + 2] = (T)oob;
+    }
+}
+
+cudaError_t launch_averaged_error(const Axis1D &ax, int64_t batch, const void *spec, int64_t k_lo, int64_t n_freq,
+                                  void *out, cudaStream_t st) {
+    if (batch <= 0) return cudaSuccess;
+    AnyErrSys sy;
+    for (int m = 0; m < 8; ++m) sy.s[m] = ax.sys[m];
+    const unsigned grid = (unsigned)((batch + 7) / 8);
+    if (ax.dtype == MCI_F64)
+        mci_avg_error_kernel<double><<<grid, 256, 0, st>>>((const cv<double> *)spec, k_lo, (int)n_freq, batch, ax.M,
+                                                           (int)ax.N, ax.K1, (const cv<double> *)ax.Qt, ax.omega_sum,
+                                                           sy, (double *)out);
+    else
+        mci_avg_error_kernel<float><<<grid, 256, 0, st>>>((const cv<float> *)spec, k_lo, (int)n_freq, batch, ax.M,
+                                                          (int)ax.N, ax.K1, (const cv<float> *)ax.Qt, ax.omega_sum, sy,
+                                                          (float *)out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,

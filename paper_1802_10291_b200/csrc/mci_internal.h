@@ -10,6 +10,12 @@
 
 namespace mci {
 
+// A built-in channel system for device-side multiplier evaluation (error analysis).
+struct SysDev {
+    int kind = 0, order = 0;
+    double tau = 0.0;
+};
+
 // Radix plan of a mixed-radix transform (arbitrary-length path): n passes, radices r[].
 struct AnyRadix {
     int n = 0;
@@ -44,6 +50,8 @@ struct Axis1D {
                       //   twLhi = e^{+2 pi i m/L} [L], band K1 = -floor(MN/2))
     int64_t K1 = 0;   // lowest band frequency (arbitrary-length path)
     int cplx = 0;     // complex f: complex channels in, T_N f out (arbitrary-length path, MCI_COMPLEX)
+    SysDev sys[8];        // the bank (built-in kinds), for device-side b_m(k) (MCI_ANALYSIS)
+    double omega_sum = 0;  // sum_m Omega_m, Omega_m = sup_{band} |r_m|^2 (Eq. errorestimate)
     AnyRadix radN, radL;
 };
 
@@ -79,6 +87,10 @@ bool anylen_supported(const Axis1D &ax);
 size_t anylen_smem_bytes(const Axis1D &ax);
 cudaError_t launch_anylen(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                           cudaStream_t st, int *n_launches);
+cudaError_t launch_anylen_residual(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *out,
+                                   cudaStream_t st);
+cudaError_t launch_averaged_error(const Axis1D &ax, int64_t batch, const void *spec, int64_t k_lo, int64_t n_freq,
+                                  void *out, cudaStream_t st);
 cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,
                                   const void *t, void *f, void *hf, cudaStream_t st);
 

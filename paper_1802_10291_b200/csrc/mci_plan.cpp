@@ -337,6 +337,12 @@ mci_status build_axis_any(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mc
     }
     ax.M = M; ax.N = N; ax.L = L; ax.K = -K1; ax.K1 = K1; ax.analytic = analytic ? 1 : 0;
     ax.cplx = cplx ? 1 : 0;
+    for (int m = 0; m < M; ++m) {
+        ax.sys[m].kind = sys[m].kind;
+        ax.sys[m].order = sys[m].order;
+        ax.sys[m].tau = sys[m].tau;
+    }
+    std::vector<double> omega(M, 0.0);
     ax.S = L; ax.R = 1;
     ax.radN = radix_plan(N);
     ax.radL = radix_plan(L);
@@ -372,8 +378,13 @@ mci_status build_axis_any(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mc
             cond_max = std::max(cond_max, n1 * n2);
         }
         for (int m = 0; m < M; ++m)
-            for (int l = 0; l < M; ++l) push_c(blob, inv[m * M + l] / (double)N);
+            for (int l = 0; l < M; ++l) {
+                push_c(blob, inv[m * M + l] / (double)N);
+                omega[m] = std::max(omega[m], std::norm(inv[m * M + l]));  // |r_m(j_q + l N)|^2
+            }
     }
+    ax.omega_sum = 0;
+    for (double o : omega) ax.omega_sum += o;
     offs.push_back(blob.size());  // twF = e^{-2 pi i m / N}
     push_roots(blob, N, N, 1, -1);
     offs.push_back(blob.size());  // twLhi = e^{+2 pi i m / L}
@@ -463,7 +474,10 @@ mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *
     std::vector<size_t> offs2;
     mci::Axis1D ay;
     ay.dtype = p->dtype;
-    if (flags & MCI_OFFGRID) {
+    if (flags & (MCI_OFFGRID | MCI_ANALYSIS)) {
+        if (flags & MCI_ANALYSIS)
+            for (int m = 0; m < M; ++m)
+                if (sys[m].kind == MCI_SYS_TABLE) return MCI_E_UNSUPPORTED;
         double c2 = 0;
         s = build_axis_any<T>(ay, M, N, (int64_t)M * N, sys, null_bins, n_null, analytic, blob2, offs2, c2);
         if (s != MCI_OK) return s;
@@ -474,7 +488,7 @@ mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *
     if ((s = upload<T>(p, blob)) != MCI_OK) return s;
     set_ptrs(ax, p->tables, offs, sizeof(T));
     p->ax = ax;
-    if (flags & MCI_OFFGRID) {
+    if (flags & (MCI_OFFGRID | MCI_ANALYSIS)) {
         set_ptrs(ay, (char *)p->tables + n1 * sizeof(T), offs2, sizeof(T));
         p->ay = ay;
     }
@@ -644,10 +658,10 @@ mci_status mci_plan_create_band(mci_plan *out, int M, int64_t N, int64_t L, int6
                                 const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags) {
     if (!out) return MCI_E_ARG;
     *out = nullptr;
-    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID | MCI_COMPLEX)) ||
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID | MCI_COMPLEX | MCI_ANALYSIS)) ||
         n_null < 0 || (n_null > 0 && !null_bins))
         return MCI_E_ARG;
-    if ((flags & MCI_COMPLEX) && (flags & (MCI_OUT_HILBERT | MCI_OFFGRID))) return MCI_E_UNSUPPORTED;
+    if ((flags & MCI_COMPLEX) && (flags & (MCI_OUT_HILBERT | MCI_OFFGRID | MCI_ANALYSIS))) return MCI_E_UNSUPPORTED;
     // real output: the Hermitian assembly of the paths needs the default band
     if (!(flags & MCI_COMPLEX) && K1 != K1_DEFAULT && K1 != -(((int64_t)M * N) / 2)) return MCI_E_UNSUPPORTED;
     mci_plan p = new (std::nothrow) mci_plan_s();
@@ -668,10 +682,10 @@ mci_status mci_plan_create(mci_plan *out, int M, int64_t N, int64_t L, const mci
                            const int64_t *null_bins, int n_null, mci_dtype dtype, unsigned flags) {
     if (!out) return MCI_E_ARG;
     *out = nullptr;
-    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID | MCI_COMPLEX)) ||
+    if ((dtype != MCI_F32 && dtype != MCI_F64) || (flags & ~(MCI_OUT_HILBERT | MCI_OFFGRID | MCI_COMPLEX | MCI_ANALYSIS)) ||
         n_null < 0 || (n_null > 0 && !null_bins))
         return MCI_E_ARG;
-    if ((flags & MCI_COMPLEX) && (flags & (MCI_OUT_HILBERT | MCI_OFFGRID))) return MCI_E_UNSUPPORTED;
+    if ((flags & MCI_COMPLEX) && (flags & (MCI_OUT_HILBERT | MCI_OFFGRID | MCI_ANALYSIS))) return MCI_E_UNSUPPORTED;
     mci_plan p = new (std::nothrow) mci_plan_s();
     if (!p) return MCI_E_ARG;
     p->dtype = dtype;
@@ -769,6 +783,29 @@ mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t
     ra.cs = p->ax.N;
     ra.ss = 1;
     return from_cuda(mci::launch_anylen_offgrid(p->ay, ra, batch, g, n_pts, t, f, hf, (cudaStream_t)stream));
+}
+
+mci_status mci_consistency_residual(mci_plan p, int64_t batch, const void *g, void *out, void *stream) {
+    if (!p || p->path == mci::PATH_2D || p->path == mci::PATH_SISR || !(p->flags & MCI_ANALYSIS) ||
+        p->ay.special != 4 || batch < 0)
+        return MCI_E_ARG;
+    if (batch == 0) return MCI_OK;
+    if (!g || !out) return MCI_E_ARG;
+    mci::RowAddr ra;
+    ra.s2 = (int64_t)p->ay.M * p->ay.N;
+    ra.cs = p->ay.N;
+    ra.ss = 1;
+    return from_cuda(mci::launch_anylen_residual(p->ay, ra, batch, g, out, (cudaStream_t)stream));
+}
+
+mci_status mci_averaged_error(mci_plan p, int64_t batch, const void *spec, int64_t k_lo, int64_t n_freq, void *out,
+                              void *stream) {
+    if (!p || p->path == mci::PATH_2D || p->path == mci::PATH_SISR || !(p->flags & MCI_ANALYSIS) ||
+        p->ay.special != 4 || batch < 0 || n_freq < 0 || n_freq > INT32_MAX)
+        return MCI_E_ARG;
+    if (batch == 0) return MCI_OK;
+    if (!spec || !out) return MCI_E_ARG;
+    return from_cuda(mci::launch_averaged_error(p->ay, batch, spec, k_lo, n_freq, out, (cudaStream_t)stream));
 }
 
 mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out, void *stream) {

@@ -168,7 +168,25 @@ CONFIGS = {
     # SURVEY.md §8(f) NEXT-2 measurement line: the paper's x3 SISR on 510 x 510 images
     # (LR 170 x 170, "Baby (510 x 510)"), 64 synthetic images
     8: dict(H=170, W=170, scale=3, batch=64, dtype="f32"),
+    # SURVEY.md §8(f) NEXT-4 measurement line: eps(f, N) of 16,384 spectra on 4x the config-2 band
+    9: dict(M=3, N=1024, L=16384, batch=16384, nfreq=4 * 3 * 1024,
+            bank=[("identity",), ("derivative", 1), ("derivative", 2)], dtype="f32"),
 }
+
+
+def error_spectra(batch: int, k_lo: int, nfreq: int, seed: int = 9, block: int = 1024) -> np.ndarray:
+    """Config 9 inputs: complex64 spectra a(k), k = k_lo .. k_lo + nfreq - 1, Re/Im ~ N(0, 1/2)
+    scaled by 1/(1+|k|/256) (the config-2 decay extended beyond the band); rows drawn in blocks
+    of `block` from default_rng([seed, block index])."""
+    k = np.arange(k_lo, k_lo + nfreq)
+    sc = (1.0 / (1.0 + np.abs(k) / 256.0)).astype(np.float32)
+    out = np.empty((batch, nfreq), dtype=np.complex64)
+    for b0 in range(0, batch, block):
+        nb = min(block, batch - b0)
+        rng = np.random.default_rng([seed, b0 // block])
+        z = rng.standard_normal((nb, 2 * nfreq), dtype=np.float32) * np.float32(math.sqrt(0.5))
+        out[b0:b0 + nb] = (z[:, 0::2] + 1j * z[:, 1::2]) * sc
+    return out
 
 
 def offgrid_points(npts: int, seed: int = 7) -> np.ndarray:

@@ -48,7 +48,7 @@ def test_alias_band_size_errors():
     assert _create(3, 1, 16, [("identity",)] * 3)[0] in (mci.MCI_E_SIZE, mci.MCI_E_BAND)
     assert _create(0, 32, 256, f)[0] == mci.MCI_E_ARG
     assert _create(2, 32, 256, f, dtype=7)[0] == mci.MCI_E_ARG
-    st, h = _create(2, 32, 256, f, flags=8)
+    st, h = _create(2, 32, 256, f, flags=16)
     assert st == mci.MCI_E_ARG and not h.value
 
 

@@ -574,3 +574,62 @@ def test_example3_hilbert_channel_null_bin():
     ref = oracle.OraclePlan(1, N, L, [("hilbert",)], null_bins=[0]).eval(hf[None, None, :])[0]
     assert row_rel(out, ref) < F64_TOL
     assert row_rel(out, truth) < 1e-12
+
+
+# -------------------------------------------------------------------------- NEXT-4: error analysis
+@pytest.mark.parametrize("bank,dtype", [(BANKS["f_df_ddf"], "f64"), (BANKS["f_df"], "f32"),
+                                        (BANKS["f_hf"], "f64"), ([("delay", 0.0), ("delay", 0.3)], "f32")])
+def test_averaged_error_vs_oracle(bank, dtype):
+    """eps(f, N), its bound and the out-of-band energy of batches of
+    spectra (Eq. averageerror / errorestimate) vs oracle.averaged_error
+    (pinned P13 against the brute-force shift-averaged error)."""
+    m = mci()
+    M, N = len(bank), 24
+    P = oracle.OraclePlan(M, N, 4 * M * N, bank)
+    plan = m.Plan(M, N, 4 * M * N, bank, dtype=dtype, analysis=True)
+    rng = np.random.default_rng(M * 7 + N)
+    k_lo = P.K1 - 3 * N - 5
+    nf = M * N + 6 * N
+    kk = np.arange(k_lo, k_lo + nf)
+    spec = (rng.standard_normal((5, nf)) + 1j * rng.standard_normal((5, nf))) / (1 + np.abs(kk) / 8.0) ** 2
+    cdt = torch.complex128 if dtype == "f64" else torch.complex64
+    out = plan.averaged_error(torch.from_numpy(spec).to("cuda", dtype=cdt), k_lo).double().cpu().numpy()
+    tol = 1e-10 if dtype == "f64" else 1e-5
+    for i in range(5):
+        sp = spec[i].astype(np.complex64).astype(np.complex128) if dtype == "f32" else spec[i]
+        ref = np.array(oracle.averaged_error(P, sp, k_lo))
+        assert np.max(np.abs(out[i] - ref) / ref) < tol, (out[i], ref)
+
+
+@pytest.mark.parametrize("bank,N,L,dtype", [(BANKS["f_df_ddf"], 107, 321, "f64"), (BANKS["f_df"], 256, 1024, "f32"),
+                                            (BANKS["f_hf"], 64, 256, "f64")])
+def test_consistency_residual(bank, N, L, dtype):
+    """Theorem consistency: the residual of arbitrary
+    (non-band-limited) data is at rounding level on the GPU, and the oracle agrees on
+    which scale that is."""
+    m = mci()
+    M = len(bank)
+    npdt, tdt = (np.float64, torch.float64) if dtype == "f64" else (np.float32, torch.float32)
+    g = (np.random.default_rng(N).standard_normal((6, M, N)) * (N / 4.0) ** np.arange(M)[None, :, None]).astype(npdt)
+    plan = m.Plan(M, N, L, bank, dtype=dtype, analysis=True)
+    res = plan.consistency_residual(torch.from_numpy(g).cuda()).double().cpu().numpy()
+    scale = np.abs(g).max(axis=(1, 2))
+    eps = 1e-12 if dtype == "f64" else 2e-5
+    assert np.all(res < eps * scale), res / scale
+    P = oracle.OraclePlan(M, N, L, bank)
+    assert oracle.consistency_residual(P, g[0].astype(np.float64)) < 1e-11 * scale[0]
+
+
+def test_cfg9_full_batch_sampled():
+    """Config 9 (NEXT-4 measurement line) in the bench launch: sampled spectra vs
+    oracle.averaged_error."""
+    m = mci()
+    c = synth.CONFIGS[9]
+    k_lo = -(c["M"] * c["N"]) * 2
+    spec = synth.error_spectra(c["batch"], k_lo, c["nfreq"], seed=9)
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"], analysis=True)
+    out = plan.averaged_error(torch.from_numpy(spec).cuda(), k_lo).double().cpu().numpy()
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    for i in (0, c["batch"] - 1):
+        ref = np.array(oracle.averaged_error(P, spec[i].astype(np.complex128), k_lo))
+        assert np.max(np.abs(out[i] - ref) / ref) < 1e-5

@@ -426,3 +426,63 @@ def test_p12_example5_printed_kernel():
     y1 = (P.r[0] @ np.exp(1j * np.outer(k, t)))
     printed = (np.cos((Np + 1) * t) - np.cos(Np * t) + np.cos(t) - 1) / (2 * np.cos(t) - 2)
     assert np.max(np.abs(y1 - printed)) < 1e-12
+
+
+# ---------------------------------------------------------------- P13: error analysis (NEXT-4)
+def _shift_averaged_error(P, spec, k_lo):
+    """(N/2 pi) int_0^{2 pi/N} ||f_tau - T_N f_tau||^2 dtau by brute force:
+    for each tau, the channels of f_tau = f(. - tau) are sampled exactly, T_N f_tau's band
+    coefficients come from oracle.band_spectrum, and Parseval gives the squared error.
+    The integrand is a trig polynomial in tau with period 2 pi / N, so J > (support width)/N
+    uniform points integrate it exactly."""
+    n = np.arange(k_lo, k_lo + len(spec))
+    J = len(spec) // P.N + 3
+    tn = 2 * np.pi * np.arange(P.N) / P.N
+    B = np.array([[P.multiplier(m, nn) for nn in n] for m in range(P.M)])
+    acc = 0.0
+    for j in range(J):
+        tau = 2 * np.pi * j / (P.N * J)
+        at = spec * np.exp(-1j * n * tau)                    # coefficients of f_tau
+        g = (B * at) @ np.exp(1j * np.outer(n, tn))          # [M][N] channel samples
+        k, ah = oracle.band_spectrum(P, g)
+        full = dict(zip(n, at))
+        err = sum(abs(full.get(kk, 0.0) - v) ** 2 for kk, v in zip(k, ah))
+        err += sum(abs(v) ** 2 for nn, v in zip(n, at) if nn < P.K1 or nn >= P.K1 + P.MN)
+        acc += err
+    return np.sqrt(acc / J)
+
+
+@pytest.mark.parametrize("bank", [[("identity",), ("derivative", 1)],
+                                  [("identity",), ("derivative", 1), ("derivative", 2)],
+                                  [("identity",), ("hilbert",)]])
+def test_p13_averaged_error_matches_shift_average(bank):
+    """Theorem error (Eq. averageerror) against the definition it comes
+    from (shift-averaged L2 error), plus eps >= sqrt(oob), eps <= bound,
+    and eps = 0 for band-limited f."""
+    M, N = len(bank), 8
+    P = oracle.OraclePlan(M, N, 4 * M * N, bank)
+    rng = np.random.default_rng(M + 40)
+    k_lo = P.K1 - 2 * N - 3
+    spec = (rng.standard_normal(M * N + 5 * N) + 1j * rng.standard_normal(M * N + 5 * N)) / (
+        1 + np.abs(np.arange(k_lo, k_lo + M * N + 5 * N)) / 4.0)
+    eps, bound, oob = oracle.averaged_error(P, spec, k_lo)
+    brute = _shift_averaged_error(P, spec, k_lo)
+    assert abs(eps - brute) < 1e-9 * brute
+    assert eps >= np.sqrt(oob) - 1e-12 and eps <= bound + 1e-9
+    inband = spec.copy()
+    n = np.arange(k_lo, k_lo + len(spec))
+    inband[(n < P.K1) | (n >= P.K1 + P.MN)] = 0
+    assert oracle.averaged_error(P, inband, k_lo)[0] == 0.0
+
+
+def test_p13_consistency_residual():
+    """Theorem consistency: residual ~0 for band-limited
+    and for arbitrary data; a corrupted inverse entry is detected (> 1e-6)."""
+    bank = [("identity",), ("derivative", 1), ("derivative", 2)]
+    P = oracle.OraclePlan(3, 16, 96, bank)
+    rng = np.random.default_rng(13)
+    g = rng.standard_normal((3, 16)) * np.array([1.0, 4.0, 16.0])[:, None]
+    assert oracle.consistency_residual(P, g) < 1e-10 * np.abs(g).max()
+    P.r = P.r.copy()
+    P.r[1, 5] += 1e-3
+    assert oracle.consistency_residual(P, g) > 1e-6
