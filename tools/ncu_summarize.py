@@ -62,9 +62,9 @@ def main():
     lines = [f"# ncu summary, round {RND[1:]}", "",
              "Captured on a B200 with `tools/profile_round.sh` (bench.py --steps 3 --warmup 3, one GPU);",
              "launch lists use `--metrics gpu__time_duration.sum --clock-control none` (cold, serialised:",
-             "compare shares, not absolutes); full captures use `--set full --clock-control none`.", ""]
+             "compare shares, not absolutes); full captures use `--set full --clock-control none --cache-control none`.", ""]
     traffic = {}
-    for c in (2, 3, 4, 5):
+    for c in (2, 3, 4, 5, 6, 7, 8, 9):
         w = bench.workload(c)
         lines.append(f"## config {c}: {w['name']}")
         lp = os.path.join(SRC, f"launches_c{c}.csv")
