@@ -73,11 +73,13 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
     constexpr int GB = 272 + 1;   // forward buffer stride (4 FFTs of 256, pad4)
     constexpr int IB = 1056 + 4;  // inverse buffer stride (4 FFTs of 1024, pad5); == 4 mod 16
     const int64_t xl = a.K / N1 + 2;
+    // the inverse buffers (phase C) alias the forward buffers (phases A-B), which are dead after
+    // the barrier that follows the solve: 54 KB per CTA, 4 CTAs (16 warps) per SM
     float2 *fb = reinterpret_cast<float2 *>(smem);  // 4 x GB
     float2 *G = fb + 4 * GB;                         // [4][256] natural order
-    float2 *Xl = G + 4 * 256;                        // [2][xl]
-    float2 *ib = Xl + 2 * xl;                        // 4 x IB
-    float2 *tw16 = ib + 4 * IB;                      // [16][16] e^{-2 pi i j b/256}
+    float2 *ib = fb;                                 // 4 x IB (phase C)
+    float2 *Xl = fb + 4 * IB;                        // [2][xl]  (4 IB >= 4 GB + 4 x 256)
+    float2 *tw16 = Xl + 2 * xl;                      // [16][16] e^{-2 pi i j b/256}
     float2 *tw32 = tw16 + 256;                       // [32][32] e^{-2 pi i j i/1024}
     float2 *tw128 = tw32 + 1024;                     // [3][32] e^{2 pi i e j / 128}, e = 1, 2, 3
     float2 *twE = tw128 + 96;                        // [2][32] e^{2 pi i 32 res_r j / S}
@@ -325,7 +327,7 @@ cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t
     using namespace fsf;
     const size_t fa_sm = (size_t)(8 * (1056 + 2) + 1024) * 8;
     const int64_t xl = a.K / N1 + 2;
-    const size_t fb_sm = (size_t)(4 * 273 + 4 * 256 + 2 * xl + 4 * 1060 + 256 + 1024 + 96 + 64) * 8;
+    const size_t fb_sm = (size_t)(4 * 1060 + 2 * xl + 256 + 1024 + 96 + 64) * 8;  // ib aliases fb + G
     const size_t ic_sm = (size_t)(16 * 1057 + 1024) * 8;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
