@@ -137,16 +137,21 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     float2 *fwd = bufB;  // forward spectra (2 x 1024) alias buffer B
     float2 *fw2 = reinterpret_cast<float2 *>(smem + G * C::GROUP_BYTES + C::Q_BYTES);
     float2 *fw3 = fw2, *fw8 = fw2 + 16 * 64;  // 4-warp forward twiddles (alias fw2)
-    float2 *itw = C::SMALL_TAB ? fw2 - 64 : fw2 + C::FW_TAB;  // [64][64] e^{+2 pi i j t / 4096} (j >= 1 used)
-    float2 *wps = itw + 64 * 64;  // e^{+2 pi i p / L}, p = 0..K
+    // inverse pass-2 twiddles w_j(t) = e^{+2 pi i j t / 4096}, j = 1..63, paired for 128-bit loads:
+    // itwp[128 p + 2 t + h] = w_{2p+1+h}(t) for p < 31, itwp[3968 + t] = w_63(t)  (4032 entries)
+    float2 *itwp = C::SMALL_TAB ? fw2 : fw2 + C::FW_TAB;
+    float2 *wps = itwp + 64 * 64;  // e^{+2 pi i p / L}, p = 0..K (layouts with all tables in smem)
     // table reads: shared memory, or L1 (__ldg) in the G = 3 layout
     auto ld_wp = [&](int p) { return C::SMALL_TAB ? __ldg(tb.wp + p) : wps[p]; };
     auto ld_fw3 = [&](int i) { return C::SMALL_TAB ? __ldg(tb.fw3 + i) : fw3[i]; };
     auto ld_fw8 = [&](int i) { return C::SMALL_TAB ? __ldg(tb.fw8 + i) : fw8[i]; };
 
     // ---- one-time setup
+    for (int i = threadIdx.x; i < 31 * 128 + 64; i += G * NT) {
+        const int pp = i >> 7, r = i & 127;
+        itwp[i] = i < 31 * 128 ? tb.itw[(2 * pp + 1 + (r & 1)) * 64 + (r >> 1)] : tb.itw[63 * 64 + (i - 31 * 128)];
+    }
     if constexpr (C::SMALL_TAB) {
-        for (int i = 64 + threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
     } else if constexpr (FW4) {
         for (int i = threadIdx.x; i < 16 * 64; i += G * NT) fw3[i] = tb.fw3[i];
         for (int i = threadIdx.x; i < 8 * 8; i += G * NT) fw8[i] = tb.fw8[i];
@@ -154,7 +159,6 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
         for (int i = threadIdx.x; i < 32 * 32; i += G * NT) fw2[i] = tb.fw2[i];
     }
     if constexpr (!C::SMALL_TAB) {
-        for (int i = threadIdx.x; i < 64 * 64; i += G * NT) itw[i] = tb.itw[i];
         for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
     }
     if (tid == 0) mbar_init(&mbar[grp], 1);
@@ -456,7 +460,12 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
 #pragma unroll
         for (int j = 0; j < 64; ++j) x[j] = mk(buf[swz64(t + 64 * j)]);
 #pragma unroll
-        for (int j = 1; j < 64; ++j) x[j] = pkx::cmul(x[j], mk(itw[j * 64 + t]));
+        for (int p2 = 0; p2 < 31; ++p2) {
+            const float4 w2 = *reinterpret_cast<const float4 *>(itwp + 128 * p2 + 2 * t);
+            x[2 * p2 + 1] = pkx::cmul(x[2 * p2 + 1], mk(w2.x, w2.y));
+            x[2 * p2 + 2] = pkx::cmul(x[2 * p2 + 2], mk(w2.z, w2.w));
+        }
+        x[63] = pkx::cmul(x[63], mk(itwp[31 * 128 + t]));
         pkx::dft<64, 1>(x);
         // outputs p2 = t + 64 j: A -> f[4p2], f[4p2+1]; B -> f[4p2+2], f[4p2+3]
         // (each half-warp store covers 128 contiguous bytes)
