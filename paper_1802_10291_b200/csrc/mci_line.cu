@@ -57,13 +57,15 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
     float *stage = reinterpret_cast<float *>(bufs + WARPS * BUF);  // TILED: [2][WARPS][SP]
     for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
     for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
-    for (int i = threadIdx.x; i < 512; i += WARPS * 32) fwt[i] = tb.fwt[i];
-    for (int i = threadIdx.x; i < 1024; i += WARPS * 32) iw[i] = tb.iw[i];
+    // pass-2 twiddles re-laid as pairs for 128-bit loads (the kernel is MIO-bound):
+    // fwt[32 p + 2 i + h] = fw_{2p+1+h}(i) (p < 15), fwt[480 + i] = fw_31(i); iw likewise with 64 per pair row
+    for (int i = threadIdx.x; i < 15 * 32 + 16; i += WARPS * 32)
+        fwt[i] = i < 480 ? tb.fwt[(2 * (i >> 5) + 1 + (i & 1)) * 16 + ((i & 31) >> 1)] : tb.fwt[31 * 16 + (i - 480)];
+    for (int i = threadIdx.x; i < 15 * 64 + 32; i += WARPS * 32)
+        iw[i] = i < 960 ? tb.iw[(2 * (i >> 6) + 1 + (i & 1)) * 32 + ((i & 63) >> 1)] : tb.iw[31 * 32 + (i - 960)];
     __syncthreads();
     auto ldQ = [&](int i) { return Qs[i]; };
     auto ldwp = [&](int i) { return wps[i]; };
-    auto ldfw = [&](int i) { return fwt[i]; };
-    auto ldiw = [&](int i) { return iw[i]; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2 *buf = bufs + warp * BUF;
 
@@ -148,7 +150,12 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
 #pragma unroll
             for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw3(lane + 16 * j)]);
 #pragma unroll
-            for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(ldfw(j * 16 + lane)));
+            for (int p2 = 0; p2 < 15; ++p2) {
+                const float4 w2 = *reinterpret_cast<const float4 *>(fwt + 32 * p2 + 2 * lane);
+                y[2 * p2 + 1] = pkx::cmul(y[2 * p2 + 1], mk(w2.x, w2.y));
+                y[2 * p2 + 2] = pkx::cmul(y[2 * p2 + 2], mk(w2.z, w2.w));
+            }
+            y[31] = pkx::cmul(y[31], mk(fwt[480 + lane]));
             dft<32, -1>(y);
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[sw3(lane + 16 * j)] = f2(y[j]);
@@ -215,7 +222,12 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
 #pragma unroll
-        for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(ldiw(j * 32 + lane)));
+        for (int p2 = 0; p2 < 15; ++p2) {
+            const float4 w2 = *reinterpret_cast<const float4 *>(iw + 64 * p2 + 2 * lane);
+            y[2 * p2 + 1] = pkx::cmul(y[2 * p2 + 1], mk(w2.x, w2.y));
+            y[2 * p2 + 2] = pkx::cmul(y[2 * p2 + 2], mk(w2.z, w2.w));
+        }
+        y[31] = pkx::cmul(y[31], mk(iw[960 + lane]));
         dft<32, 1>(y);
         float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
 #pragma unroll
