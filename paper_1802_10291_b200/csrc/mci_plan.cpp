@@ -552,7 +552,10 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
     return MCI_OK;
 }
 
-mci_status from_cuda(cudaError_t e) { return e == cudaSuccess ? MCI_OK : MCI_E_CUDA; }
+mci_status from_cuda(cudaError_t e) {
+    if (e != cudaSuccess && getenv("MCI_DEBUG")) fprintf(stderr, "mci: CUDA error: %s\n", cudaGetErrorString(e));
+    return e == cudaSuccess ? MCI_OK : MCI_E_CUDA;
+}
 
 mci_status exec_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf, cudaStream_t st, int *nl) {
     if (p->path == mci::PATH_FUSED) {

@@ -83,6 +83,80 @@ __device__ __forceinline__ int sw3(int a) { return a ^ ((a >> 3) & 15); }
 // 2^e as an exact float (|e| <= 100)
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 
+// ---- tensor memory (TMEM) as per-thread read-only tables.  Every table entry the
+// kernel reads is a fixed function of the thread's index within its row group, and
+// thread tid of every group maps to TMEM lane tid (warp w of a group accesses lanes
+// 32 (w % 4) ..), so one copy serves the three groups.  tcgen05.ld runs beside the
+// shared-memory pipe (tools/microbench/tmem_ld.cu: >= 370 B/clk/SM at 16 warps),
+// which is the kernel's most loaded data path.
+constexpr int TM_COLS = 512;
+// TM flags (template parameter): which per-thread data live in TMEM
+constexpr int TM_SMALL = 1;   // forward-pass and pre-twiddle tables (read through L1 otherwise)
+constexpr int TM_ITWF = 2;    // inverse pass-2 twiddles (shared memory otherwise)
+constexpr int TM_NEXT = 4;    // the group's next input row (loaded early, parked in TMEM)
+constexpr int TM_STORE = 8;   // outputs, drained by a fourth (store) warpgroup
+// column map; with TM_STORE the outputs take columns 0..383 and the tables move up by 256
+constexpr int TM_ITW = 0;    // 126 cols: w_j(t) = e^{+2 pi i j t / 4096}, j = 1..63 (inverse pass 2)
+constexpr int TM_FW8 = 128;  // 14 cols: e^{-2 pi i j k / 64}, j = 1..7, k = tid & 7 (forward pass 2)
+constexpr int TM_FW3 = 144;  // 30 cols: e^{-2 pi i j bb / 1024}, j = 1..15, bb = tid & 63 (forward pass 3)
+constexpr int TM_WP = 176;   // 24 cols: e^{+2 pi i p / L} for p = N - q, q, q + N, q = tid + 128 u (solve)
+constexpr int TM_IN = 200;   // 24 cols per row group: the group's next input row, g_m[b + 128 j] at 3 j + m
+__device__ __forceinline__ void tm_st8(uint32_t ta, const float *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+// load 8 consecutive columns (4 complex entries) and wait; the wait names the
+// destination registers so no use can be scheduled before it
+__device__ __forceinline__ void tm_ld8(uint32_t ta, float2 *w) {
+    float v0, v1, v2, v3, v4, v5, v6, v7;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v0), "=f"(v1), "=f"(v2), "=f"(v3), "=f"(v4), "=f"(v5), "=f"(v6), "=f"(v7)
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v0), "+f"(v1), "+f"(v2), "+f"(v3), "+f"(v4), "+f"(v5), "+f"(v6), "+f"(v7)::"memory");
+    w[0] = make_float2(v0, v1);
+    w[1] = make_float2(v2, v3);
+    w[2] = make_float2(v4, v5);
+    w[3] = make_float2(v6, v7);
+}
+__device__ __forceinline__ void tm_st32(uint32_t ta, const float *v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tm_ld8f(uint32_t ta, float *v) {
+    float2 w[4];
+    tm_ld8(ta, w);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = w[i].x;
+        v[2 * i + 1] = w[i].y;
+    }
+}
+__device__ __forceinline__ void tm_ld16(uint32_t ta, float2 *w) {
+    float v[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+          "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+        : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                   "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                   "+f"(v[15])::"memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = make_float2(v[2 * i], v[2 * i + 1]);
+}
+
 }  // namespace rowk
 
 // Device tables built by the plan (fp64-rounded), see mci_plan.cpp.
@@ -96,7 +170,7 @@ struct RowTables {
     int deriv;          // 1: bank is (1, ik, -k^2) -> closed-form Q (Example 2)
 };
 
-template <int G, bool QTAB, bool FW4 = false>
+template <int G, bool QTAB, bool FW4 = false, int TM = 0>
 struct RowCfg {
     static constexpr int M = 3, N = 1024, S = 4096, K = 1536, L = 16384;
     static constexpr int NQ = N / 2 + 1;
@@ -110,21 +184,34 @@ struct RowCfg {
     // G = 3 (12 warps) fits 227 KB only with the inverse twiddles (rows j >= 1) alone in
     // shared memory; the pre-twiddle and forward tables are then read through L1
     static constexpr bool SMALL_TAB = G >= 3;
-    static constexpr int TAB_BYTES = SMALL_TAB ? 63 * 64 * 8 : (FW_TAB + 64 * 64 + K + 2) * 8;
+    static constexpr int TAB_BYTES = (TM & rowk::TM_ITWF) ? 0 : SMALL_TAB ? 63 * 64 * 8 : (FW_TAB + 64 * 64 + K + 2) * 8;
     static constexpr int SMEM = G * GROUP_BYTES + Q_BYTES + TAB_BYTES;
+    // TM = 3: a fourth warpgroup streams the outputs out of tensor memory
+    static constexpr int THREADS = G * 128 + ((TM & rowk::TM_STORE) ? 128 : 0);
 };
 
-template <int G, bool QTAB, bool FW4>
-__global__ void __launch_bounds__(G * rowk::NT, 1)
+template <int G, bool QTAB, bool FW4, int TM = 0>
+__global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
     mci_row_kernel(const float *__restrict__ g, float *__restrict__ f, int64_t rows, RowTables tb) {
     using namespace rowk;
-    using C = RowCfg<G, QTAB, FW4>;
+    using C = RowCfg<G, QTAB, FW4, TM>;
     static_assert(!C::SMALL_TAB || FW4, "G = 3 uses the 4-warp forward");
+    static_assert(!TM || (FW4 && G == 3), "TMEM tables: 3 groups, 4-warp forward");
+    constexpr bool TMS = TM & TM_SMALL, TMI = TM & TM_ITWF, TMN = TM & TM_NEXT, STW = TM & TM_STORE;
+    static_assert(!(STW && (TMI || TMN)), "the outputs leave no TMEM room for these");
+    constexpr int TB = STW ? 256 : 0;  // table column shift
     constexpr int M = C::M, N = C::N, S = C::S, K = C::K, L = C::L;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t mbar[G];
     __shared__ float ssup[G][4];
     __shared__ float smx[G][4][3];  // per-warp channel maxima (4-warp forward)
+    __shared__ uint32_t tm_base;
+    // TM = 3: output hand-off barriers of group gg, kept in the 64-byte gap between its
+    // buffers A and B (the 227 KB budget has no room for them in static shared memory)
+    auto tm_full = [&](int gg) {
+        return reinterpret_cast<uint64_t *>(smem + gg * C::GROUP_BYTES + C::STAGE_BYTES + C::BUF_ELEMS * 8);
+    };
+    auto tm_empty = [&](int gg) { return tm_full(gg) + 1; };
 
     const int grp = threadIdx.x / NT;
     const int tid = threadIdx.x % NT;
@@ -147,7 +234,71 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     auto ld_fw8 = [&](int i) { return C::SMALL_TAB ? __ldg(tb.fw8 + i) : fw8[i]; };
 
     // ---- one-time setup
-    for (int i = threadIdx.x; i < 31 * 128 + 64; i += G * NT) {
+    if constexpr (TM) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tm_base)),
+                         "n"(TM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if ((TMS || TMI) && threadIdx.x < NT) {  // group 0 writes lane tid of the shared tables
+            const int tt = threadIdx.x;
+            const uint32_t ta = tm_base + ((uint32_t)(32 * (tt >> 5)) << 16);
+            const int t2 = 16 * (tt >> 5) + ((tt & 31) >> 1);  // inverse butterfly of this lane
+            float v[8];
+#pragma unroll 1
+            for (int c = 0; TMI && c < 128; c += 8) {  // inverse pass-2 twiddles, j = 1 + c/2 ..
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;
+                    const float2 w = j <= 63 ? tb.itw[j * 64 + t2] : make_float2(0.f, 0.f);
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tm_st8(ta + TM_ITW + c, v);
+            }
+#pragma unroll 1
+            for (int c = 0; TMS && c < 16; c += 8) {  // forward pass-2 twiddles
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;
+                    const float2 w = j <= 7 ? tb.fw8[j * 8 + (tt & 7)] : make_float2(0.f, 0.f);
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tm_st8(ta + TB + TM_FW8 + c, v);
+            }
+#pragma unroll 1
+            for (int c = 0; TMS && c < 32; c += 8) {  // forward pass-3 twiddles
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;
+                    const float2 w = j <= 15 ? tb.fw3[j * 64 + (tt & 63)] : make_float2(0.f, 0.f);
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tm_st8(ta + TB + TM_FW3 + c, v);
+            }
+#pragma unroll 1
+            for (int c = 0; TMS && c < 32; c += 8) {  // pre-twiddles of the solve outputs (entry 3u + e)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int idx = c / 2 + i, u = idx / 3, e = idx % 3;
+                    const int q = tt + 128 * u;
+                    const int pp = e == 0 ? (N - q) & (2 * N - 1) : e == 1 ? q : q + N;  // q = 0: e = 0 -> p = N
+                    const float2 w = u < 4 ? tb.wp[pp] : make_float2(0.f, 0.f);
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tm_st8(ta + TB + TM_WP + c, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+    }
+    for (int i = threadIdx.x; !TMI && i < 31 * 128 + 64; i += G * NT) {
         const int pp = i >> 7, r = i & 127;
         itwp[i] = i < 31 * 128 ? tb.itw[(2 * pp + 1 + (r & 1)) * 64 + (r >> 1)] : tb.itw[63 * 64 + (i - 31 * 128)];
     }
@@ -161,13 +312,40 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     if constexpr (!C::SMALL_TAB) {
         for (int i = threadIdx.x; i <= K; i += G * NT) wps[i] = tb.wp[i];
     }
-    if (tid == 0) mbar_init(&mbar[grp], 1);
+    if (tid == 0 && grp < G) mbar_init(&mbar[grp], 1);
+    if (STW && threadIdx.x < G) {
+        mbar_init(tm_full(threadIdx.x), NT);
+        mbar_init(tm_empty(threadIdx.x), NT);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if constexpr (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmA = TM ? tm_base + ((uint32_t)(32 * warp) << 16) : 0u;  // this thread's TMEM lane
+    // TM = 2: the group's next input row is loaded into registers early in the forward
+    // phase and parked in TMEM (24 columns per thread) until the next row's pass 1
+    float nx[24];
+    auto in_load = [&](int64_t r) {
+        const float *src = g + r * (int64_t)(M * N);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+            for (int m = 0; m < 3; ++m) nx[3 * j + m] = __ldcs(src + m * N + tid + 128 * j);
+    };
+    auto in_park = [&]() {
+#pragma unroll
+        for (int c = 0; c < 24; c += 8) tm_st8(tmA + TM_IN + 24 * grp + c, nx + c);
+    };
 
     const int64_t gid = (int64_t)blockIdx.x * G + grp;
     const int64_t gstride = (int64_t)gridDim.x * G;
     uint32_t phase = 0;
+    if constexpr (TMN) {
+        if (gid < rows) {
+            in_load(gid);
+            in_park();
+        }
+    }
     if (C::STAGED && tid == 0 && gid < rows) {
         mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
         tma_load_1d(stage, g + gid * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
@@ -182,6 +360,37 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
     const int h = lane & 1;
     const int t = 16 * warp + (lane >> 1);
 
+    uint32_t opar = 0;  // TM = 3: parity of this group's output hand-off
+    if (STW && grp == G) {
+        // ---- store warpgroup: drains each group's finished row from TMEM (lane = the
+        //      computing thread, columns 128 g + 2 j, 2 j + 1 = its output j) with the
+        //      compute warps' coalesced store pattern, so output stores never stall them
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
+        const uint32_t ta = tm_base + ((uint32_t)(32 * warp) << 16);
+        for (int64_t it = 0;; ++it) {
+            bool any = false;
+#pragma unroll 1
+            for (int gg = 0; gg < G; ++gg) {
+                const int64_t r = (int64_t)blockIdx.x * G + gg + it * gstride;
+                if (r >= rows) continue;
+                any = true;
+                mbar_wait(tm_full(gg), (uint32_t)(it & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                float2 *fo = reinterpret_cast<float2 *>(f + r * (int64_t)L);
+#pragma unroll 1
+                for (int c = 0; c < 16; ++c) {
+                    float2 w[4];
+                    tm_ld8(ta + 128 * gg + 8 * c, w);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) __stcs(fo + 2 * (t + 64 * (4 * c + i)) + h, w[i]);
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mbar_arrive(tm_empty(gg));
+            }
+            if (!any) break;
+        }
+    } else {
+    if constexpr (STW) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
     for (int64_t row = gid; row < rows; row += gstride) {
         using namespace pkx;
         if constexpr (C::STAGED) {
@@ -197,10 +406,21 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             {  // pass 1: radix 8, Ls = 1, butterfly b of both FFTs
                 pk x0[8], x1[8];
                 float m0 = 0.f, m1 = 0.f, m2 = 0.f;
+                float cur[24];
+                if constexpr (TMN) {
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tm_ld8f(tmA + TM_IN + 24 * grp, cur);
+                    tm_ld8f(tmA + TM_IN + 24 * grp + 8, cur + 8);
+                    tm_ld8f(tmA + TM_IN + 24 * grp + 16, cur + 16);
+                }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     float a0, a1, a2;
-                    if constexpr (C::STAGED) {
+                    if constexpr (TMN) {
+                        a0 = cur[3 * j];
+                        a1 = cur[3 * j + 1];
+                        a2 = cur[3 * j + 2];
+                    } else if constexpr (C::STAGED) {
                         a0 = stage[b + 128 * j];
                         a1 = stage[N + b + 128 * j];
                         a2 = stage[2 * N + b + 128 * j];
@@ -260,15 +480,20 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
                 mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
                 tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
             }
+            if constexpr (TMN) {
+                if (row + gstride < rows) in_load(row + gstride);
+            }
             {  // pass 2: radix 8, Ls = 8, B -> A
                 const int k = b & 7;
+                float2 w8[8];
+                if constexpr (TMS) tm_ld16(tmA + TB + TM_FW8, w8);
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     pk x[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) x[j] = mk(bufB[c * 1024 + sw3(b + 128 * j)]);
 #pragma unroll
-                    for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(ld_fw8(j * 8 + k)));
+                    for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(TMS ? w8[j - 1] : ld_fw8(j * 8 + k)));
                     pkx::dft<8, -1>(x);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) bufA[c * 1024 + sw3(8 * (b - k) + k + 8 * j)] = f2(x[j]);
@@ -280,8 +505,13 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
                 pk x[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) x[j] = mk(bufA[c * 1024 + sw3(bb + 64 * j)]);
+                float2 w3[16];
+                if constexpr (TMS) {
+                    tm_ld16(tmA + TB + TM_FW3, w3);
+                    tm_ld16(tmA + TB + TM_FW3 + 16, w3 + 8);
+                }
 #pragma unroll
-                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(ld_fw3(j * 64 + bb)));
+                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(TMS ? w3[j - 1] : ld_fw3(j * 64 + bb)));
                 pkx::dft<16, -1>(x);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) bufB[c * 1024 + sw3(bb + 64 * j)] = f2(x[j]);
@@ -375,8 +605,14 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
         for (int m = 0; m < 3; ++m) hs[m] = 0.5f * ssup[grp][m];
         group_bar(barid);  // forward spectra read: buffer B may now be overwritten
 
-        auto emit = [&](int p, pk X) {
-            const pk a = mk(ld_wp(p));
+        float2 wq[12];  // TMEM mode: pre-twiddles of this thread's solve outputs (entry 3u + e)
+        if constexpr (TMS) {
+            tm_ld8(tmA + TB + TM_WP, wq);
+            tm_ld8(tmA + TB + TM_WP + 8, wq + 4);
+            tm_ld8(tmA + TB + TM_WP + 16, wq + 8);
+        }
+        auto emit = [&](int p, pk X, float2 wa) {
+            const pk a = mk(TMS ? wa : ld_wp(p));
             const pk P1 = pkx::cmul(X, a);
             const pk P2 = pkx::cmul(P1, a);
             const pk P3 = pkx::cmul(P2, a);
@@ -423,22 +659,25 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
             pk v[3];
             solve(zq[u], zm[u], q, v);
             if (q != 0) {
-                emit(N - q, pkx::conj(v[0]));
-                emit(q, v[1]);
-                emit(q + N, v[2]);
+                emit(N - q, pkx::conj(v[0]), wq[3 * u]);
+                emit(q, v[1], wq[3 * u + 1]);
+                emit(q + N, v[2], wq[3 * u + 2]);
             } else {  // q = 0: elements -N, 0, N; X[0] = Re a(0), X[N] = (a(N) + conj a(-N))/2
-                emit(0, mk(f2(v[1]).x, 0.f));
-                emit(N, pkx::mul(add(v[2], pkx::conj(v[0])), bc(0.5f)));
+                emit(0, mk(f2(v[1]).x, 0.f), wq[3 * u + 1]);
+                emit(N, pkx::mul(add(v[2], pkx::conj(v[0])), bc(0.5f)), wq[3 * u + 2]);
             }
         }
         if (tid == 0) {  // q* = N/2: elements -3N/2 = -K, -N/2, N/2
             pk v[3];
             solve(zq[4], zm[4], N / 2, v);
-            emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)));
-            emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)));
+            emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)), __ldg(tb.wp + K));
+            emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)), __ldg(tb.wp + N / 2));
         }
         group_bar(barid);
 
+        if constexpr (TMN) {
+            if (row + gstride < rows) in_park();
+        }
         // ---- inverse pass 1: radix 64, Ls = 1.  Lane pair (2s, 2s+1) runs FFTs A and B
         //      on butterfly t; zero-padding inputs k' in (K, S-K) are not read.
         float2 *buf = h ? bufB : bufA;
@@ -459,38 +698,80 @@ __global__ void __launch_bounds__(G * rowk::NT, 1)
         // ---- inverse pass 2: radix 64, Ls = 64; twiddles w4096^{j t} = it1[j&7] * it2[j>>3]
 #pragma unroll
         for (int j = 0; j < 64; ++j) x[j] = mk(buf[swz64(t + 64 * j)]);
+        if constexpr (TMI) {
 #pragma unroll
-        for (int p2 = 0; p2 < 31; ++p2) {
-            const float4 w2 = *reinterpret_cast<const float4 *>(itwp + 128 * p2 + 2 * t);
-            x[2 * p2 + 1] = pkx::cmul(x[2 * p2 + 1], mk(w2.x, w2.y));
-            x[2 * p2 + 2] = pkx::cmul(x[2 * p2 + 2], mk(w2.z, w2.w));
+            for (int c = 0; c < 16; ++c) {  // twiddles j = 4c+1 .. 4c+4 (j <= 63)
+                float2 w[4];
+                tm_ld8(tmA + TM_ITW + 8 * c, w);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (4 * c + 1 + i <= 63) x[4 * c + 1 + i] = pkx::cmul(x[4 * c + 1 + i], mk(w[i]));
+            }
+        } else {
+#pragma unroll
+            for (int p2 = 0; p2 < 31; ++p2) {
+                const float4 w2 = *reinterpret_cast<const float4 *>(itwp + 128 * p2 + 2 * t);
+                x[2 * p2 + 1] = pkx::cmul(x[2 * p2 + 1], mk(w2.x, w2.y));
+                x[2 * p2 + 2] = pkx::cmul(x[2 * p2 + 2], mk(w2.z, w2.w));
+            }
+            x[63] = pkx::cmul(x[63], mk(itwp[31 * 128 + t]));
         }
-        x[63] = pkx::cmul(x[63], mk(itwp[31 * 128 + t]));
         pkx::dft<64, 1>(x);
         // outputs p2 = t + 64 j: A -> f[4p2], f[4p2+1]; B -> f[4p2+2], f[4p2+3]
         // (each half-warp store covers 128 contiguous bytes)
         float2 *fo = reinterpret_cast<float2 *>(f + row * (int64_t)L);
 #pragma unroll
-        for (int j = 0; j < 64; ++j) __stcs(fo + 2 * (t + 64 * j) + h, f2(x[j]));
+        if constexpr (STW) {  // hand the row to the store warpgroup through TMEM
+            mbar_wait(tm_empty(grp), opar ^ 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float2 xv = f2(x[16 * c + i]);
+                    v[2 * i] = xv.x;
+                    v[2 * i + 1] = xv.y;
+                }
+                tm_st32(tmA + 128 * grp + 32 * c, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(tm_full(grp));
+            opar ^= 1u;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) {
+                    __stcs(fo + 2 * (t + 64 * j) + h, f2(x[j]));
+            }
+        }
+    }
+    }  // compute warpgroups
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base), "n"(TM_COLS)
+                         : "memory");
     }
 }
 
 // ---------------------------------------------------------------------------------------
-template <int G, bool QTAB, bool FW4>
+template <int G, bool QTAB, bool FW4, int TM = 0>
 static cudaError_t row_launch_t(const RowTables &tb, int64_t rows, const float *g, float *f, cudaStream_t st) {
-    using C = RowCfg<G, QTAB, FW4>;
-    auto kern = mci_row_kernel<G, QTAB, FW4>;
+    using C = RowCfg<G, QTAB, FW4, TM>;
+    auto kern = mci_row_kernel<G, QTAB, FW4, TM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G * rowk::NT, C::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, C::THREADS, C::SMEM);
     if (occ < 1) occ = 1;
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (rows + G - 1) / G;
     if (grid > need) grid = need;
-    kern<<<(unsigned)grid, G * rowk::NT, C::SMEM, st>>>(g, f, rows, tb);
+    kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(g, f, rows, tb);
     return cudaGetLastError();
 }
 
@@ -521,9 +802,21 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     case 2:  // 2 groups, 4-warp forward, all tables in shared memory
         return tb.deriv ? row_launch_t<2, false, true>(tb, rows, gg, ff, st)
                         : row_launch_t<2, true, true>(tb, rows, gg, ff, st);
-    default:  // 3 groups (12 warps), 4-warp forward, untiled inputs, inverse twiddles in shared memory
+    case 3:  // 3 groups, 4-warp forward, all per-thread twiddle tables in tensor memory
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_SMALL | rowk::TM_ITWF>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_SMALL | rowk::TM_ITWF>(tb, rows, gg, ff, st);
+    case 5:  // 3 compute groups + a store warpgroup draining the outputs from tensor memory
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_STORE>(tb, rows, gg, ff, st);
+    case 7:  // variant 0 with the forward and pre-twiddle tables in tensor memory
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_SMALL>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_SMALL>(tb, rows, gg, ff, st);
+    case 8:  // 3 groups (12 warps), 4-warp forward, untiled inputs, inverse twiddles in shared memory
         return tb.deriv ? row_launch_t<3, false, true>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true>(tb, rows, gg, ff, st);
+    default:  // 3 compute groups + the store warpgroup; forward and pre-twiddle tables in TMEM
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st);
     }
 }
 
