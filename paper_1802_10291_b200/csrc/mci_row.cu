@@ -93,14 +93,13 @@ constexpr int TM_COLS = 512;
 // TM flags (template parameter): which per-thread data live in TMEM
 constexpr int TM_SMALL = 1;   // forward-pass and pre-twiddle tables (read through L1 otherwise)
 constexpr int TM_ITWF = 2;    // inverse pass-2 twiddles (shared memory otherwise)
-constexpr int TM_NEXT = 4;    // the group's next input row (loaded early, parked in TMEM)
+constexpr int TM_L2PF = 4;    // the store warpgroup prefetches each group's input two rows ahead into L2
 constexpr int TM_STORE = 8;   // outputs, drained by a fourth (store) warpgroup
 // column map; with TM_STORE the outputs take columns 0..383 and the tables move up by 256
 constexpr int TM_ITW = 0;    // 126 cols: w_j(t) = e^{+2 pi i j t / 4096}, j = 1..63 (inverse pass 2)
 constexpr int TM_FW8 = 128;  // 14 cols: e^{-2 pi i j k / 64}, j = 1..7, k = tid & 7 (forward pass 2)
 constexpr int TM_FW3 = 144;  // 30 cols: e^{-2 pi i j bb / 1024}, j = 1..15, bb = tid & 63 (forward pass 3)
 constexpr int TM_WP = 176;   // 24 cols: e^{+2 pi i p / L} for p = N - q, q, q + N, q = tid + 128 u (solve)
-constexpr int TM_IN = 200;   // 24 cols per row group: the group's next input row, g_m[b + 128 j] at 3 j + m
 __device__ __forceinline__ void tm_st8(uint32_t ta, const float *v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
                  "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
@@ -132,15 +131,6 @@ __device__ __forceinline__ void tm_st32(uint32_t ta, const float *v) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void tm_ld8f(uint32_t ta, float *v) {
-    float2 w[4];
-    tm_ld8(ta, w);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        v[2 * i] = w[i].x;
-        v[2 * i + 1] = w[i].y;
-    }
 }
 __device__ __forceinline__ void tm_ld16(uint32_t ta, float2 *w) {
     float v[16];
@@ -197,8 +187,9 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
     using C = RowCfg<G, QTAB, FW4, TM>;
     static_assert(!C::SMALL_TAB || FW4, "G = 3 uses the 4-warp forward");
     static_assert(!TM || (FW4 && G == 3), "TMEM tables: 3 groups, 4-warp forward");
-    constexpr bool TMS = TM & TM_SMALL, TMI = TM & TM_ITWF, TMN = TM & TM_NEXT, STW = TM & TM_STORE;
-    static_assert(!(STW && (TMI || TMN)), "the outputs leave no TMEM room for these");
+    constexpr bool TMS = TM & TM_SMALL, TMI = TM & TM_ITWF, PF2 = TM & TM_L2PF, STW = TM & TM_STORE;
+    static_assert(!(STW && TMI), "the outputs leave no TMEM room for the inverse twiddles");
+    static_assert(!PF2 || STW, "the L2 prefetch is issued by the store warpgroup");
     constexpr int TB = STW ? 256 : 0;  // table column shift
     constexpr int M = C::M, N = C::N, S = C::S, K = C::K, L = C::L;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -322,30 +313,9 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
     __syncthreads();
     if constexpr (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmA = TM ? tm_base + ((uint32_t)(32 * warp) << 16) : 0u;  // this thread's TMEM lane
-    // TM = 2: the group's next input row is loaded into registers early in the forward
-    // phase and parked in TMEM (24 columns per thread) until the next row's pass 1
-    float nx[24];
-    auto in_load = [&](int64_t r) {
-        const float *src = g + r * (int64_t)(M * N);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-#pragma unroll
-            for (int m = 0; m < 3; ++m) nx[3 * j + m] = __ldcs(src + m * N + tid + 128 * j);
-    };
-    auto in_park = [&]() {
-#pragma unroll
-        for (int c = 0; c < 24; c += 8) tm_st8(tmA + TM_IN + 24 * grp + c, nx + c);
-    };
-
     const int64_t gid = (int64_t)blockIdx.x * G + grp;
     const int64_t gstride = (int64_t)gridDim.x * G;
     uint32_t phase = 0;
-    if constexpr (TMN) {
-        if (gid < rows) {
-            in_load(gid);
-            in_park();
-        }
-    }
     if (C::STAGED && tid == 0 && gid < rows) {
         mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
         tma_load_1d(stage, g + gid * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
@@ -367,6 +337,14 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
         //      compute warps' coalesced store pattern, so output stores never stall them
         asm volatile("setmaxnreg.dec.sync.aligned.u32 32;" ::: "memory");
         const uint32_t ta = tm_base + ((uint32_t)(32 * warp) << 16);
+        // TM_L2PF: 96 lanes x 128 B = one 12 KB input row into L2, two rows ahead of its group
+        auto l2pf = [&](int64_t r) {
+            if (r < rows && tid < M * N * 4 / 128)
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(g + r * (int64_t)(M * N) + 32 * tid));
+        };
+        if constexpr (PF2) {
+            for (int gg = 0; gg < G; ++gg) l2pf((int64_t)blockIdx.x * G + gg + gstride);
+        }
         for (int64_t it = 0;; ++it) {
             bool any = false;
 #pragma unroll 1
@@ -386,6 +364,7 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(tm_empty(gg));
+                if constexpr (PF2) l2pf(r + 2 * gstride);
             }
             if (!any) break;
         }
@@ -406,21 +385,10 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             {  // pass 1: radix 8, Ls = 1, butterfly b of both FFTs
                 pk x0[8], x1[8];
                 float m0 = 0.f, m1 = 0.f, m2 = 0.f;
-                float cur[24];
-                if constexpr (TMN) {
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-                    tm_ld8f(tmA + TM_IN + 24 * grp, cur);
-                    tm_ld8f(tmA + TM_IN + 24 * grp + 8, cur + 8);
-                    tm_ld8f(tmA + TM_IN + 24 * grp + 16, cur + 16);
-                }
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     float a0, a1, a2;
-                    if constexpr (TMN) {
-                        a0 = cur[3 * j];
-                        a1 = cur[3 * j + 1];
-                        a2 = cur[3 * j + 2];
-                    } else if constexpr (C::STAGED) {
+                    if constexpr (C::STAGED) {
                         a0 = stage[b + 128 * j];
                         a1 = stage[N + b + 128 * j];
                         a2 = stage[2 * N + b + 128 * j];
@@ -479,9 +447,6 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_expect_tx(&mbar[grp], C::STAGE_BYTES);
                 tma_load_1d(stage, g + (row + gstride) * (int64_t)(M * N), C::STAGE_BYTES, &mbar[grp]);
-            }
-            if constexpr (TMN) {
-                if (row + gstride < rows) in_load(row + gstride);
             }
             {  // pass 2: radix 8, Ls = 8, B -> A
                 const int k = b & 7;
@@ -675,9 +640,6 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
         }
         group_bar(barid);
 
-        if constexpr (TMN) {
-            if (row + gstride < rows) in_park();
-        }
         // ---- inverse pass 1: radix 64, Ls = 1.  Lane pair (2s, 2s+1) runs FFTs A and B
         //      on butterfly t; zero-padding inputs k' in (K, S-K) are not read.
         float2 *buf = h ? bufB : bufA;
@@ -808,15 +770,19 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     case 5:  // 3 compute groups + a store warpgroup draining the outputs from tensor memory
         return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true, rowk::TM_STORE>(tb, rows, gg, ff, st);
+    case 6:  // 3 compute groups + the store warpgroup, no L2 prefetch
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st);
     case 7:  // variant 0 with the forward and pre-twiddle tables in tensor memory
         return tb.deriv ? row_launch_t<3, false, true, rowk::TM_SMALL>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true, rowk::TM_SMALL>(tb, rows, gg, ff, st);
     case 8:  // 3 groups (12 warps), 4-warp forward, untiled inputs, inverse twiddles in shared memory
         return tb.deriv ? row_launch_t<3, false, true>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true>(tb, rows, gg, ff, st);
-    default:  // 3 compute groups + the store warpgroup; forward and pre-twiddle tables in TMEM
-        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st)
-                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st);
+    default:  // 3 compute groups + the store warpgroup (outputs from TMEM, input rows into L2
+              // two rows ahead); forward and pre-twiddle tables in TMEM
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF>(tb, rows, gg, ff, st);
     }
 }
 
