@@ -37,7 +37,8 @@ constexpr int ITW_LD = 65;              // row stride of the [32][65] twiddle ta
 __device__ __forceinline__ int pad6(int a) { return a + (a >> 6); }
 __device__ __forceinline__ int pad4(int a) { return a + (a >> 4); }  // forward 4096-point buffer
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
-__device__ __forceinline__ void bar() { __syncthreads(); }
+// compute-thread barrier (named, so a store warpgroup can run beside the 8 compute warps)
+__device__ __forceinline__ void bar() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 // next row's input arrives by TMA bulk copy (cp.async.bulk + mbarrier) while this row is transformed
 __device__ __forceinline__ void stage_row(float *dst, const float *src, uint64_t *mb) {
@@ -46,6 +47,26 @@ __device__ __forceinline__ void stage_row(float *dst, const float *src, uint64_t
                      su32(dst)),
                  "l"(src), "r"(M * N * 4), "r"(su32(mb))
                  : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t *mb) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(mb)) : "memory");
+}
+__device__ __forceinline__ void tm_st32(uint32_t ta, const float *v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(ta),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+        "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+        "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+        "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t ta, float *v) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7])::"memory");
 }
 __device__ __forceinline__ void stage_wait(uint64_t *mb, uint32_t parity) {
     uint32_t done = 0;
@@ -65,7 +86,12 @@ struct HilbertTables {
     int deriv;          // 1: bank is (1, ik) -> closed-form inverse
 };
 
-__global__ void __launch_bounds__(hilk::NT, 1)
+// STW: a fourth... (ninth to twelfth) warp set -- a store warpgroup -- takes each round's 64 outputs
+// per thread out of tensor memory (lane = compute thread, 128 columns per compute warpgroup,
+// double-buffered by round) and writes them with the compute threads' sector-aligned pattern,
+// so the output stores never stall the transform.
+template <bool STW>
+__global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
     mci_hilbert_kernel(const float *__restrict__ g, float *__restrict__ f, float *__restrict__ hf, int64_t rows,
                        HilbertTables tb) {
     using namespace hilk;
@@ -81,6 +107,21 @@ __global__ void __launch_bounds__(hilk::NT, 1)
     __shared__ __align__(8) uint64_t mbar;
     __shared__ float smx[8][2];
     __shared__ float ssc[2];
+    __shared__ uint32_t tm_base;
+    __shared__ __align__(8) uint64_t tfull[2], tempty[2];  // STW: per TMEM buffer (round parity)
+    if (STW) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tm_base))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        if (threadIdx.x == 32) {
+            for (int i = 0; i < 2; ++i) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&tfull[i])), "n"(NT) : "memory");
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(su32(&tempty[i])) : "memory");
+            }
+        }
+    }
     for (int i = threadIdx.x; i < 256; i += NT) {
         whi[i] = tb.whi[i];
         wlo[i] = tb.wlo[i];
@@ -91,9 +132,47 @@ __global__ void __launch_bounds__(hilk::NT, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (blockIdx.x < rows) stage_row(stage, g + blockIdx.x * (int64_t)(M * N), &mbar);
     }
+    if (STW) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if (STW) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     uint32_t parity = 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    if (STW && threadIdx.x >= NT) {
+        // ---- store warpgroup: warp k drains TMEM lane quarter k of both compute warpgroups
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+        const int k = warp - NT / 32;
+        const uint32_t ta = tm_base + ((uint32_t)(32 * k) << 16);
+        uint32_t rc = 0;  // global round count
+        for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+            for (int r = 0; r < 4; ++r, ++rc) {
+                const uint32_t b = rc & 1;
+                stage_wait(&tfull[b], (rc >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+                for (int wg = 0; wg < 2; ++wg) {
+                    const int ctid = 128 * wg + 32 * k + lane;  // the compute thread of this lane
+                    const int c = ctid & 7, bt = ctid >> 3, p1 = 8 * r + c;
+                    float *fr = f + row * (int64_t)L + p1, *hr = hf + row * (int64_t)L + p1;
+#pragma unroll 1
+                    for (int cc = 0; cc < 16; ++cc) {  // 8 columns = outputs (hh, j), 4 per chunk
+                        float v[8];
+                        tm_ld8(ta + 256 * b + 128 * wg + 8 * cc, v);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int e = 4 * cc + i, hh = e >> 5, j = e & 31;
+                            const int64_t o = (int64_t)R * (bt + 32 * hh + 64 * j);
+                            __stcs(fr + o, v[2 * i]);
+                            __stcs(hr + o, v[2 * i + 1]);
+                        }
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mb_arrive(&tempty[b]);
+            }
+        }
+    } else {
+    if (STW) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
+    uint32_t rcc = 0;  // STW: global round count of the compute side
     // w = e^{+2 pi i m / L}, m in [0, L)
     auto wL = [&](int m) { return pkx::cmul(mk(whi[m >> 8]), mk(wlo[m & 255])); };
 
@@ -230,6 +309,13 @@ __global__ void __launch_bounds__(hilk::NT, 1)
             bar();
             // pass 2 (Ls = 64): radix 32 on butterflies t = bt and bt + 32; outputs p2 = t + 64 j
             float *fr = f + row * (int64_t)L + p1, *hr = hf + row * (int64_t)L + p1;
+            const uint32_t tb_ = STW ? tm_base + ((uint32_t)(32 * (warp & 3)) << 16) + 256 * (rcc & 1) +
+                                           128 * (warp >> 2)
+                                     : 0u;
+            if (STW) {  // the store warpgroup has drained this TMEM buffer (two rounds ago)
+                stage_wait(&tempty[rcc & 1], ((rcc >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 const int t = bt + 32 * hh;
@@ -239,15 +325,42 @@ __global__ void __launch_bounds__(hilk::NT, 1)
 #pragma unroll
                 for (int j = 1; j < 32; ++j) y[j] = pkx::cmul(y[j], mk(itw[j * ITW_LD + t]));
                 dft<32, 1>(y);
+                if (STW) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float2 z = f2(y[j]);
-                    const int64_t o = (int64_t)R * (t + 64 * j);
-                    __stcs(fr + o, z.x);
-                    __stcs(hr + o, z.y);
+                    for (int cc = 0; cc < 2; ++cc) {
+                        float v[32];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float2 z = f2(y[16 * cc + i]);
+                            v[2 * i] = z.x;
+                            v[2 * i + 1] = z.y;
+                        }
+                        tm_st32(tb_ + 64 * hh + 32 * cc, v);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float2 z = f2(y[j]);
+                        const int64_t o = (int64_t)R * (t + 64 * j);
+                        __stcs(fr + o, z.x);
+                        __stcs(hr + o, z.y);
+                    }
                 }
             }
+            if (STW) {
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                mb_arrive(&tfull[rcc & 1]);
+                ++rcc;
+            }
         }
+    }
+    }  // compute warps
+    if (STW) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base) : "memory");
     }
 }
 
@@ -267,7 +380,11 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     tb.itw = base + 512;
     tb.deriv = ax.bank_deriv01;
     const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4;
-    cudaError_t e = cudaFuncSetAttribute(mci_hilbert_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // MCI_HILBERT_VARIANT=1: the 8-warp layout storing directly (A/B); default: store warpgroup
+    const int variant = getenv("MCI_HILBERT_VARIANT") ? atoi(getenv("MCI_HILBERT_VARIANT")) : 0;
+    const bool stw = variant != 1;
+    auto kern = stw ? mci_hilbert_kernel<true> : mci_hilbert_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148;
     cudaGetDevice(&dev);
@@ -275,7 +392,7 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     int64_t grid = nsm;
     if (grid > rows) grid = rows;
     if (n_launches) *n_launches += 1;
-    mci_hilbert_kernel<<<(unsigned)grid, NT, smem, st>>>((const float *)g, (float *)f, (float *)hf, rows, tb);
+    kern<<<(unsigned)grid, NT + (stw ? 128 : 0), smem, st>>>((const float *)g, (float *)f, (float *)hf, rows, tb);
     return cudaGetLastError();
 }
 

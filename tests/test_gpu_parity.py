@@ -158,12 +158,14 @@ def test_cfg3_shape_hilbert():
     assert row_rel(f[0], fr) < 1e-5 and row_rel(hf[0], hr) < 1e-5
 
 
-@pytest.mark.parametrize("qtab", [False, True])
-def test_hilbert_kernel_vs_oracle_and_generic(qtab, monkeypatch):
+@pytest.mark.parametrize("qtab,variant", [(False, 0), (True, 0), (False, 1), (True, 1)])
+def test_hilbert_kernel_vs_oracle_and_generic(qtab, variant, monkeypatch):
     """The specialised config-3 kernel (mci_hilbert.cu; closed-form (1, ik) inverse or
-    the Q table) on a batch larger than the persistent grid, with non-bandlimited
-    rows: within tolerance of the oracle (sampled rows) and of the generic fused
-    kernel (all rows), and bit-for-bit independent of batch size."""
+    the Q table; variant 0 = store warpgroup draining the outputs from tensor memory,
+    1 = direct stores) on a batch larger than the persistent grid, with
+    non-bandlimited rows: within tolerance of the oracle (sampled rows) and of the
+    generic fused kernel (all rows), and bit-for-bit independent of batch size."""
+    monkeypatch.setenv("MCI_HILBERT_VARIANT", str(variant))
     m = mci()
     c = synth.CONFIGS[3]
     rows = 157
