@@ -95,15 +95,32 @@ constexpr int TM_SMALL = 1;   // forward-pass and pre-twiddle tables (read throu
 constexpr int TM_ITWF = 2;    // inverse pass-2 twiddles (shared memory otherwise)
 constexpr int TM_L2PF = 4;    // the store warpgroup prefetches each group's input two rows ahead into L2
 constexpr int TM_STORE = 8;   // outputs, drained by a fourth (store) warpgroup
+constexpr int TM_A2 = 32;     // squared pre-twiddles e^{2 pi i 2p / L}: FFT B's inputs = a^2 x FFT A's
 // column map; with TM_STORE the outputs take columns 0..383 and the tables move up by 256
 constexpr int TM_ITW = 0;    // 126 cols: w_j(t) = e^{+2 pi i j t / 4096}, j = 1..63 (inverse pass 2)
 constexpr int TM_FW8 = 128;  // 14 cols: e^{-2 pi i j k / 64}, j = 1..7, k = tid & 7 (forward pass 2)
 constexpr int TM_FW3 = 144;  // 30 cols: e^{-2 pi i j bb / 1024}, j = 1..15, bb = tid & 63 (forward pass 3)
 constexpr int TM_WP = 176;   // 24 cols: e^{+2 pi i p / L} for p = N - q, q, q + N, q = tid + 128 u (solve)
+constexpr int TM_WP2 = 200;  // 24 cols: e^{+2 pi i 2p / L} for the same p (TM_A2)
 __device__ __forceinline__ void tm_st8(uint32_t ta, const float *v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
                  "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                  : "memory");
+}
+// Example 2 closed-form inverse for the (f, f', f'') bank, class q of
+// N = 1024, K = 1536, divided by N (d = G/N): r0[l], r1[l] (r2 = (-d2, d1, -d2) is constant).
+// Every numerator is an integer < 2^24 and every denominator a power of two: exact in fp32.
+__device__ __forceinline__ void ex2_coeffs(int q, float *r0, float *r1) {
+    constexpr int N = 1024, K = 1536;
+    const float n = (float)(-K + ((q + K) % N));
+    const float Nf = (float)N;
+    const float d2 = 1.f / (2.f * Nf * Nf * Nf), d1 = 1.f / (Nf * Nf * Nf);
+    r0[0] = (2.f * Nf * Nf + 3.f * Nf * n + n * n) * d2;
+    r0[1] = -(n * (2.f * Nf + n)) * d1;
+    r0[2] = (n * (Nf + n)) * d2;
+    r1[0] = (3.f * Nf + 2.f * n) * d2;
+    r1[1] = -2.f * (Nf + n) * d1;
+    r1[2] = (Nf + 2.f * n) * d2;
 }
 // load 8 consecutive columns (4 complex entries) and wait; the wait names the
 // destination registers so no use can be scheduled before it
@@ -285,6 +302,20 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                     v[2 * i + 1] = w.y;
                 }
                 tm_st8(ta + TB + TM_WP + c, v);
+            }
+#pragma unroll 1
+            for (int c = 0; (TM & TM_A2) && c < 24; c += 8) {  // their squares, in double precision
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int idx = c / 2 + i, u = idx / 3, e = idx % 3;
+                    const int q = tt + 128 * u;
+                    const int pp = e == 0 ? (N - q) & (2 * N - 1) : e == 1 ? q : q + N;
+                    double sn, cs;
+                    sincospi(4.0 * pp / L, &sn, &cs);
+                    v[2 * i] = (float)cs;
+                    v[2 * i + 1] = (float)sn;
+                }
+                tm_st8(ta + TB + TM_WP2 + c, v);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
@@ -576,16 +607,36 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             tm_ld8(tmA + TB + TM_WP + 8, wq + 4);
             tm_ld8(tmA + TB + TM_WP + 16, wq + 8);
         }
-        auto emit = [&](int p, pk X, float2 wa) {
+        float2 wq2[12];  // TM_A2: a^2 for the same outputs
+        if constexpr ((TM & TM_A2) != 0) {
+            tm_ld8(tmA + TB + TM_WP2, wq2);
+            tm_ld8(tmA + TB + TM_WP2 + 8, wq2 + 4);
+            tm_ld8(tmA + TB + TM_WP2 + 16, wq2 + 8);
+        }
+        auto emit = [&](int p, pk X, float2 wa, float2 wa2) {
             const pk a = mk(TMS ? wa : ld_wp(p));
             const pk P1 = pkx::cmul(X, a);
-            const pk P2 = pkx::cmul(P1, a);
-            const pk P3 = pkx::cmul(P2, a);
-            bufA[swz64(p)] = f2(add_rot<1>(X, P1));  // X + i P1
-            bufB[swz64(p)] = f2(add_rot<1>(P2, P3));
-            if (p > 0) {  // k' = S - p: conj(X) + i conj(P1)
-                bufA[swz64(S - p)] = f2(add_rot<1>(pkx::conj(X), pkx::conj(P1)));
-                bufB[swz64(S - p)] = f2(add_rot<1>(pkx::conj(P2), pkx::conj(P3)));
+            if constexpr ((TM & TM_A2) != 0) {
+                // FFT B's inputs are a^2 times FFT A's: P2 + i P3 = a^2 (X + i P1), and the
+                // mirrored conj(P2) + i conj(P3) = conj(a^2) (conj X + i conj P1)
+                const pk a2 = mk(wa2);
+                const pk A = add_rot<1>(X, P1);
+                bufA[swz64(p)] = f2(A);
+                bufB[swz64(p)] = f2(pkx::cmul(A, a2));
+                if (p > 0) {
+                    const pk Am = add_rot<1>(pkx::conj(X), pkx::conj(P1));
+                    bufA[swz64(S - p)] = f2(Am);
+                    bufB[swz64(S - p)] = f2(pkx::cmul(Am, pkx::conj(a2)));
+                }
+            } else {
+                const pk P2 = pkx::cmul(P1, a);
+                const pk P3 = pkx::cmul(P2, a);
+                bufA[swz64(p)] = f2(add_rot<1>(X, P1));  // X + i P1
+                bufB[swz64(p)] = f2(add_rot<1>(P2, P3));
+                if (p > 0) {  // k' = S - p: conj(X) + i conj(P1)
+                    bufA[swz64(S - p)] = f2(add_rot<1>(pkx::conj(X), pkx::conj(P1)));
+                    bufB[swz64(S - p)] = f2(add_rot<1>(pkx::conj(P2), pkx::conj(P3)));
+                }
             }
         };
         auto solve = [&](const pk *zqu, const pk *zmu, int q, pk *v) {
@@ -605,12 +656,10 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                 // Example 2, paper's L = N, n = j_q; divided by N (d = G/N).
                 // Every numerator is an integer < 2^24 and every denominator a power of
                 // two, so these entries are exact in fp32.
-                const float n = (float)(-K + ((q + K) % N));
                 const float Nf = (float)N;
                 const float d2 = 1.f / (2.f * Nf * Nf * Nf), d1 = 1.f / (Nf * Nf * Nf);
-                const float r0[3] = {(2.f * Nf * Nf + 3.f * Nf * n + n * n) * d2, -(n * (2.f * Nf + n)) * d1,
-                                     (n * (Nf + n)) * d2};
-                const float r1[3] = {(3.f * Nf + 2.f * n) * d2, -2.f * (Nf + n) * d1, (Nf + 2.f * n) * d2};
+                float r0[3], r1[3];
+                ex2_coeffs(q, r0, r1);
                 const float r2[3] = {-d2, d1, -d2};
                 const pk ig1 = rot<1>(g1);  // i G1
 #pragma unroll
@@ -624,19 +673,20 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             pk v[3];
             solve(zq[u], zm[u], q, v);
             if (q != 0) {
-                emit(N - q, pkx::conj(v[0]), wq[3 * u]);
-                emit(q, v[1], wq[3 * u + 1]);
-                emit(q + N, v[2], wq[3 * u + 2]);
+                emit(N - q, pkx::conj(v[0]), wq[3 * u], wq2[3 * u]);
+                emit(q, v[1], wq[3 * u + 1], wq2[3 * u + 1]);
+                emit(q + N, v[2], wq[3 * u + 2], wq2[3 * u + 2]);
             } else {  // q = 0: elements -N, 0, N; X[0] = Re a(0), X[N] = (a(N) + conj a(-N))/2
-                emit(0, mk(f2(v[1]).x, 0.f), wq[3 * u + 1]);
-                emit(N, pkx::mul(add(v[2], pkx::conj(v[0])), bc(0.5f)), wq[3 * u + 2]);
+                emit(0, mk(f2(v[1]).x, 0.f), wq[3 * u + 1], wq2[3 * u + 1]);
+                emit(N, pkx::mul(add(v[2], pkx::conj(v[0])), bc(0.5f)), wq[3 * u + 2], wq2[3 * u + 2]);
             }
         }
         if (tid == 0) {  // q* = N/2: elements -3N/2 = -K, -N/2, N/2
             pk v[3];
             solve(zq[4], zm[4], N / 2, v);
-            emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)), __ldg(tb.wp + K));
-            emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)), __ldg(tb.wp + N / 2));
+            const float2 aK = __ldg(tb.wp + K), aH = __ldg(tb.wp + N / 2);
+            emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)), aK, f2(pkx::cmul(mk(aK), mk(aK))));
+            emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)), aH, f2(pkx::cmul(mk(aH), mk(aH))));
         }
         group_bar(barid);
 
@@ -770,6 +820,9 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     case 5:  // 3 compute groups + a store warpgroup draining the outputs from tensor memory
         return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true, rowk::TM_STORE>(tb, rows, gg, ff, st);
+    case 4:  // the default without the a^2 form of FFT B's inputs
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF>(tb, rows, gg, ff, st);
     case 6:  // 3 compute groups + the store warpgroup, no L2 prefetch
         return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL>(tb, rows, gg, ff, st);
@@ -780,9 +833,9 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
         return tb.deriv ? row_launch_t<3, false, true>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true>(tb, rows, gg, ff, st);
     default:  // 3 compute groups + the store warpgroup (outputs from TMEM, input rows into L2
-              // two rows ahead); forward and pre-twiddle tables in TMEM
-        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF>(tb, rows, gg, ff, st)
-                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF>(tb, rows, gg, ff, st);
+              // two rows ahead); forward and pre-twiddle tables in TMEM; FFT B's inputs = a^2 x A's
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF | rowk::TM_A2>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF | rowk::TM_A2>(tb, rows, gg, ff, st);
     }
 }
 
