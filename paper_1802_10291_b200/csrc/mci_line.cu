@@ -41,6 +41,7 @@ struct LineTables {
     const float2 *wp;   // [K+1] e^{+2 pi i p / L}
     const float2 *fwt;  // [32][16] e^{-2 pi i j k / 512}
     const float2 *iw;   // [32][32] e^{+2 pi i j k / 1024}
+    int deriv;          // 1: bank is (1, ik) -> closed-form inverse, no Q~ reads
 };
 
 template <int WARPS, bool TILED>
@@ -177,9 +178,19 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         auto solve = [&](int u, int q, pk &v0, pk &v1) {
             const pk G0 = mul(add(zq[u], pkx::conj(zm[u])), bc(h0));
             const pk G1 = mul(rot<-1>(sub(zq[u], pkx::conj(zm[u]))), bc(h1));
-            const int Qq = q * 4;  // [m][l]
-            v0 = add(pkx::cmul(G0, mk(ldQ(Qq + 0))), pkx::cmul(G1, mk(ldQ(Qq + 2))));
-            v1 = add(pkx::cmul(G0, mk(ldQ(Qq + 1))), pkx::cmul(G1, mk(ldQ(Qq + 3))));
+            if (tb.deriv) {
+                // (1, ik): H_j = [[1, ij], [1, i(j+N)]], det = iN, so with d = G/N
+                // a(j) = ((j+N) G0 + i G1)/N^2, a(j+N) = (-j G0 - i G1)/N^2, j = q - N
+                // (integers times 2^-18: exact in fp32)
+                const float jn = (float)(q - N), inv = 1.f / ((float)N * (float)N);
+                const pk iG1 = rot<1>(G1);
+                v0 = add(mul(G0, bc((jn + (float)N) * inv)), mul(iG1, bc(inv)));
+                v1 = sub(mul(G0, bc(-jn * inv)), mul(iG1, bc(inv)));
+            } else {
+                const int Qq = q * 4;  // [m][l]
+                v0 = add(pkx::cmul(G0, mk(ldQ(Qq + 0))), pkx::cmul(G1, mk(ldQ(Qq + 2))));
+                v1 = add(pkx::cmul(G0, mk(ldQ(Qq + 1))), pkx::cmul(G1, mk(ldQ(Qq + 3))));
+            }
         };
         // inverse input (p1 = 0, 1 share one FFT): Zin(k) = Y(k)(1 + i w^k), w = e^{2 pi i/L}
         auto emit = [&](int p, pk X) {
@@ -250,6 +261,7 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     tb.wp = base;
     tb.fwt = tb.wp + (ax.K + 1);
     tb.iw = tb.fwt + 512;
+    tb.deriv = ax.bank_deriv01;
     const bool tiled = ra.s0 == 1 && ra.ss != 1 && ra.D0 % 16 == 0 &&
                        (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 && ra.s1 % 4 == 0 &&
                        ra.s2 % 4 == 0;

@@ -230,6 +230,10 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             ax.row_variant = getenv("MCI_ROW_VARIANT") ? atoi(getenv("MCI_ROW_VARIANT")) : 0;
             ax.special = 1;
         } else if (mci::line_supported(ax)) {
+            // (1, ik) bank with no null bins: closed-form inverse instead of the Q~ table
+            ax.bank_deriv01 = (M == 2 && n_null == 0 && sys[0].kind == MCI_SYS_IDENTITY &&
+                               sys[1].kind == MCI_SYS_DERIVATIVE && sys[1].order == 1 && !getenv("MCI_ROW_QTAB"))
+                                  ? 1 : 0;
             // line kernel tables: [wp: K+1][fwt: 32x16][iw: 32x32]
             offs.push_back(blob.size());
             push_roots(blob, L, K + 1, 1, +1);
