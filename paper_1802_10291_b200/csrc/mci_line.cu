@@ -18,8 +18,12 @@
 // (TILED) a CTA's 16 lines are adjacent in memory: the next tile [2][16][512] is
 // copied by 4-byte cp.async (transposed into a conflict-free [2][16][516] stage)
 // while the current one is transformed (one 16-warp CTA per SM: warp buffers,
-// stage and tables fill the 227 KB).
+// stage and tables fill the 227 KB).  The per-lane pre-twiddles and inverse
+// pass-2 twiddles are read from tensor memory (a copy per lane quarter), off the
+// shared-memory pipe that bounds the kernel; for the (1, ik) bank the solve uses
+// the closed-form inverse instead of the Q~ table.
 #include <cstdint>
+#include <cstdlib>
 
 #include "mci_internal.h"
 #include "mci_pk.cuh"
@@ -34,6 +38,31 @@ __device__ __forceinline__ int sw5(int a) { return a + (a >> 5); }  // inverse 1
 constexpr int BUF = S + S / 32;
 constexpr int SP = N + 4;  // stage row stride: = 4 (mod 32) -> conflict-free transposed cp.async
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+// TM: per-lane tables in tensor memory (the kernel is bound by the shared-memory pipe).
+// Every warp's lane l reads the same values, so each lane quarter holds a copy:
+// columns 0..31: pre-twiddles e^{2 pi i p / L} for p = N - q, q (q = lane + 32 u, entry 2u + e);
+// columns 32..93: inverse pass-2 twiddles e^{2 pi i j lane / 1024}, j = 1..31.
+constexpr int TM_COLS = 128, TMW = 0, TMI = 32;
+__device__ __forceinline__ uint32_t s32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tst8(uint32_t ta, const float *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
+                 "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tld16(uint32_t ta, float2 *w) {
+    float v[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+          "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+        : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                   "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12]), "+f"(v[13]), "+f"(v[14]),
+                   "+f"(v[15])::"memory");
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = make_float2(v[2 * i], v[2 * i + 1]);
+}
 }  // namespace linek
 
 struct LineTables {
@@ -44,7 +73,7 @@ struct LineTables {
     int deriv;          // 1: bank is (1, ik) -> closed-form inverse, no Q~ reads
 };
 
-template <int WARPS, bool TILED>
+template <int WARPS, bool TILED, bool TM = false>
 __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
                                                               int64_t lines, RowAddr ra, LineTables tb) {
     using namespace linek;
@@ -64,11 +93,54 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         fwt[i] = i < 480 ? tb.fwt[(2 * (i >> 5) + 1 + (i & 1)) * 16 + ((i & 31) >> 1)] : tb.fwt[31 * 16 + (i - 480)];
     for (int i = threadIdx.x; i < 15 * 64 + 32; i += WARPS * 32)
         iw[i] = i < 960 ? tb.iw[(2 * (i >> 6) + 1 + (i & 1)) * 32 + ((i & 63) >> 1)] : tb.iw[31 * 32 + (i - 960)];
+    __shared__ uint32_t tm_base;
+    if (TM) {
+        if (threadIdx.x < 32) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(&tm_base)),
+                         "n"(TM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (threadIdx.x < 128) {  // warps 0-3 fill their lane quarter (all quarters identical)
+            const int ln = threadIdx.x & 31;
+            const uint32_t ta = tm_base + ((uint32_t)(32 * (threadIdx.x >> 5)) << 16);
+            float v[8];
+#pragma unroll 1
+            for (int c = 0; c < 32; c += 8) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int idx = c / 2 + i, u = idx >> 1, e = idx & 1, q = ln + 32 * u;
+                    const float2 w = tb.wp[e ? q : N - q];
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tst8(ta + TMW + c, v);
+            }
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;
+                    const float2 w = j <= 31 ? tb.iw[j * 32 + ln] : make_float2(0.f, 0.f);
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tst8(ta + TMI + c, v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     __syncthreads();
+    if (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     auto ldQ = [&](int i) { return Qs[i]; };
     auto ldwp = [&](int i) { return wps[i]; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2 *buf = bufs + warp * BUF;
+    const uint32_t tmA = TM ? tm_base + ((uint32_t)(32 * (warp & 3)) << 16) : 0u;
 
     // TILED (2D passes): WARPS consecutive lines are adjacent in memory (s0 = 1) while
     // samples are strided.  Tile tl = [2][WARPS][N] is fetched by 4-byte cp.async: element
@@ -193,8 +265,13 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
             }
         };
         // inverse input (p1 = 0, 1 share one FFT): Zin(k) = Y(k)(1 + i w^k), w = e^{2 pi i/L}
-        auto emit = [&](int p, pk X) {
-            const pk P = pkx::cmul(X, mk(ldwp(p)));
+        float2 wq[16];  // TM: pre-twiddles of this lane's solve outputs (entry 2u + e)
+        if constexpr (TM) {
+            tld16(tmA + TMW, wq);
+            tld16(tmA + TMW + 16, wq + 8);
+        }
+        auto emit = [&](int p, pk X, float2 wa) {
+            const pk P = pkx::cmul(X, mk(TM ? wa : ldwp(p)));
             buf[sw5(p)] = f2(add_rot<1>(X, P));
             buf[sw5(S - p)] = f2(add_rot<1>(pkx::conj(X), pkx::conj(P)));
         };
@@ -204,20 +281,20 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
             pk v0, v1;
             solve(u, q, v0, v1);
             if (q != 0) {  // elements q - N (-> X[N - q] = conj v0) and q (-> X[q] = v1)
-                emit(N - q, pkx::conj(v0));
-                emit(q, v1);
+                emit(N - q, pkx::conj(v0), wq[2 * u]);
+                emit(q, v1, wq[2 * u + 1]);
             } else {  // q = 0: X[0] = Re a(0); position K = N aliases +-K at k' = K
                 const float2 a0 = f2(v1);
                 buf[sw5(0)] = make_float2(a0.x, a0.x);  // X + iX, X real
                 const pk XK = mul(pkx::conj(v0), bc(0.5f));  // X[K] = conj a(-K)/2
-                const pk P = pkx::cmul(XK, mk(ldwp(K)));
+                const pk P = pkx::cmul(XK, mk(TM ? wq[2 * u] : ldwp(K)));
                 buf[sw5(K)] = f2(add(add_rot<1>(XK, P), add_rot<1>(pkx::conj(XK), pkx::conj(P))));
             }
         }
         if (lane == 0) {  // q = N/2: elements -N/2, N/2 -> X[N/2] = (a(N/2) + conj a(-N/2))/2
             pk v0, v1;
             solve(8, N / 2, v0, v1);
-            emit(N / 2, mul(add(v1, pkx::conj(v0)), bc(0.5f)));
+            emit(N / 2, mul(add(v1, pkx::conj(v0)), bc(0.5f)), ldwp(N / 2));
         }
         __syncwarp();
 
@@ -232,17 +309,35 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         // ---- pass 2 (Ls = 32)
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
+        if constexpr (TM) {
 #pragma unroll
-        for (int p2 = 0; p2 < 15; ++p2) {
-            const float4 w2 = *reinterpret_cast<const float4 *>(iw + 64 * p2 + 2 * lane);
-            y[2 * p2 + 1] = pkx::cmul(y[2 * p2 + 1], mk(w2.x, w2.y));
-            y[2 * p2 + 2] = pkx::cmul(y[2 * p2 + 2], mk(w2.z, w2.w));
+            for (int c = 0; c < 4; ++c) {  // twiddles j = 8c+1 .. 8c+8 (j <= 31)
+                float2 w[8];
+                tld16(tmA + TMI + 16 * c, w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (8 * c + 1 + i <= 31) y[8 * c + 1 + i] = pkx::cmul(y[8 * c + 1 + i], mk(w[i]));
+            }
+        } else {
+#pragma unroll
+            for (int p2 = 0; p2 < 15; ++p2) {
+                const float4 w2 = *reinterpret_cast<const float4 *>(iw + 64 * p2 + 2 * lane);
+                y[2 * p2 + 1] = pkx::cmul(y[2 * p2 + 1], mk(w2.x, w2.y));
+                y[2 * p2 + 2] = pkx::cmul(y[2 * p2 + 2], mk(w2.z, w2.w));
+            }
+            y[31] = pkx::cmul(y[31], mk(iw[960 + lane]));
         }
-        y[31] = pkx::cmul(y[31], mk(iw[960 + lane]));
         dft<32, 1>(y);
         float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
 #pragma unroll
         for (int j = 0; j < 32; ++j) __stcs(fo + lane + 32 * j, f2(y[j]));
+    }
+    if (TM) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x < 32)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm_base), "n"(TM_COLS)
+                         : "memory");
     }
 }
 
@@ -266,7 +361,11 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
                        (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 && ra.s1 % 4 == 0 &&
                        ra.s2 % 4 == 0;
     const int WARPS = tiled ? 16 : 8;  // tiled: one 16-warp CTA per SM; else two 8-warp CTAs
-    auto kern = tiled ? mci_line_kernel<16, true> : mci_line_kernel<8, false>;
+    // default: per-lane pre-twiddle and inverse pass-2 twiddle tables in tensor memory;
+    // MCI_LINE_VARIANT=1: all tables in shared memory (A/B)
+    const bool tm = !(getenv("MCI_LINE_VARIANT") && atoi(getenv("MCI_LINE_VARIANT")) == 1);
+    auto kern = tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
+                      : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
     const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
                         (tiled ? (size_t)2 * WARPS * linek::SP * 4 : 0);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -277,13 +277,15 @@ def test_2d_small_vs_oracle():
         assert np.linalg.norm(out[i] - ref) / np.linalg.norm(ref) < F32_TOL
 
 
-@pytest.mark.parametrize("qtab", [False, True])
-def test_cfg5_full_size_sampled(qtab, monkeypatch):
+@pytest.mark.parametrize("qtab,variant", [(False, 0), (True, 0), (False, 1), (True, 1)])
+def test_cfg5_full_size_sampled(qtab, variant, monkeypatch):
     """configs[4] shape: 2 synthetic 2048^2 images, sampled columns vs oracle; PSNR sane.
     The line kernel evaluates the (1, ik) closed-form inverse, or reads the Q~ table
-    (MCI_ROW_QTAB)."""
+    (MCI_ROW_QTAB); variant 0 keeps its per-lane twiddle tables in tensor memory,
+    variant 1 in shared memory."""
     if qtab:
         monkeypatch.setenv("MCI_ROW_QTAB", "1")
+    monkeypatch.setenv("MCI_LINE_VARIANT", str(variant))
     m = mci()
     g, truths = synth.cfg5_images([0, 1])
     plan = m.Plan2D(2, 512, BANKS["f_df"], 2, 512, BANKS["f_df"], 4)
