@@ -42,7 +42,8 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // Every warp's lane l reads the same values, so each lane quarter holds a copy:
 // columns 0..31: pre-twiddles e^{2 pi i p / L} for p = N - q, q (q = lane + 32 u, entry 2u + e);
 // columns 32..93: inverse pass-2 twiddles e^{2 pi i j lane / 1024}, j = 1..31.
-constexpr int TM_COLS = 128, TMW = 0, TMI = 32;
+// columns 96..157: forward pass-2 twiddles e^{-2 pi i j lane / 512}, j = 1..31 (lanes < 16).
+constexpr int TM_COLS = 256, TMW = 0, TMI = 32, TMF = 96;
 __device__ __forceinline__ uint32_t s32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void tst8(uint32_t ta, const float *v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
@@ -129,6 +130,17 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
                     v[2 * i + 1] = w.y;
                 }
                 tst8(ta + TMI + c, v);
+            }
+#pragma unroll 1
+            for (int c = 0; c < 64; c += 8) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;
+                    const float2 w = (j <= 31 && ln < 16) ? tb.fwt[j * 16 + ln] : make_float2(0.f, 0.f);
+                    v[2 * i] = w.x;
+                    v[2 * i + 1] = w.y;
+                }
+                tst8(ta + TMF + c, v);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
@@ -219,7 +231,25 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         }
         __syncwarp();
         pk y[32];
-        if (lane < 16) {  // ---- pass 2 (radix 32, Ls = 16): butterfly i = lane < 16, in place
+        if constexpr (TM) {  // ---- pass 2 (radix 32, Ls = 16): butterfly i = lane < 16, in place;
+            // all lanes run the arithmetic (converged for tcgen05.ld), lanes >= 16 neither load nor store
+            const bool act = lane < 16;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) y[j] = act ? mk(buf[sw3(lane + 16 * j)]) : mk(0.f, 0.f);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {  // twiddles j = 8c+1 .. 8c+8 (j <= 31)
+                float2 w[8];
+                tld16(tmA + TMF + 16 * c, w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (8 * c + 1 + i <= 31) y[8 * c + 1 + i] = pkx::cmul(y[8 * c + 1 + i], mk(w[i]));
+            }
+            dft<32, -1>(y);
+            if (act) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) buf[sw3(lane + 16 * j)] = f2(y[j]);
+            }
+        } else if (lane < 16) {  // ---- pass 2 (radix 32, Ls = 16): butterfly i = lane < 16, in place
 #pragma unroll
             for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw3(lane + 16 * j)]);
 #pragma unroll
