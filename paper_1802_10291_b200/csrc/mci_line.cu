@@ -163,7 +163,23 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         return (l0 / (ra.D0 * ra.D1)) * ra.s2 + ((l0 / ra.D0) % ra.D1) * ra.s1 + (l0 % ra.D0) * ra.s0;
     };
     auto fetch_tile = [&](int64_t t) {
-        if (t < ntiles) {
+        if (t < ntiles && WARPS * 32 == 32 * 16) {
+            // 32 elements per thread: line l = tid & 15, samples n = (tid >> 4) + 32 i, channel m;
+            // addresses advance by constant strides (no per-element index arithmetic)
+            const int l = threadIdx.x & 15, n0 = threadIdx.x >> 4;
+            const float *s0 = g + tile_base(t) + l + (int64_t)n0 * ra.ss;
+            const int64_t step = 32 * ra.ss;
+            const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(stage + l * SP + n0);
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                const float *sp = s0 + m * ra.cs;
+                const uint32_t dm = d0 + (uint32_t)(m * WARPS * SP * 4);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dm + 128u * i), "l"(sp + i * step)
+                                 : "memory");
+            }
+        } else if (t < ntiles) {
             const float *src = g + tile_base(t);
 #pragma unroll 4
             for (int e = threadIdx.x; e < 2 * N * WARPS; e += WARPS * 32) {
