@@ -137,7 +137,9 @@ __device__ __forceinline__ void dft_small(cv<T> *x, int s, const cv<T> *root, in
 // one Stockham pass of radix R over `cnt` transforms of length n stored with stride n:
 // butterfly b in [0, n/R), k = b mod Ls: x_j = in[b + j n/R] w^{j k}, w = root^(n/(Ls R)),
 // out[(b - k) R + k + j Ls] = DFT_R(x)_j.  root(m) = e^{s 2 pi i m / n} (shared memory).
-template <typename T, int R, int G>
+// PAD: the root table is stored padded (entry e at e + e / 16), which spreads the strided
+// twiddle reads k * tws of a warp over the banks (the Bluestein power-of-two transforms)
+template <typename T, int R, int G, bool PAD = false>
 __device__ __forceinline__ void pass_r(const cv<T> *in, cv<T> *out, int n, int cnt, int Ls, int s, const cv<T> *root,
                                        int lane) {
     using V = cv<T>;
@@ -157,7 +159,7 @@ __device__ __forceinline__ void pass_r(const cv<T> *in, cv<T> *out, int n, int c
             if (j) {
                 e += d;
                 if (e >= n) e -= n;
-                if (k) x[j] = cmul(x[j], root[e]);
+                if (k) x[j] = cmul(x[j], root[PAD ? e + (e >> 4) : e]);
             }
         }
         dft_small<T, R>(x, s, root, nb);
@@ -224,10 +226,10 @@ __device__ cv<T> *fft_pow2(cv<T> *a, cv<T> *b, int n, int s, const cv<T> *root, 
     int Ls = 1;
     while (Ls < n) {
         if (n / Ls >= 4) {
-            pass_r<T, 4, G>(a, b, n, 1, Ls, s, root, lane);
+            pass_r<T, 4, G, true>(a, b, n, 1, Ls, s, root, lane);
             Ls *= 4;
         } else {
-            pass_r<T, 2, G>(a, b, n, 1, Ls, s, root, lane);
+            pass_r<T, 2, G, true>(a, b, n, 1, Ls, s, root, lane);
             Ls *= 2;
         }
         gsync<G>();
@@ -345,15 +347,16 @@ __global__ void __launch_bounds__(G * GPB) mci_anylen_kernel(const AnyArgs<T> a)
         q.p = rr[t]->bp;
         q.M = rr[t]->bM;
         if (!q.p) continue;
-        V *c = btab, *H = c + q.p, *wm = H + q.M, *wp = wm + q.M;
+        const int Mp = q.M + q.M / 16 + 1;  // padded root tables (see pass_r)
+        V *c = btab, *H = c + q.p, *wm = H + q.M, *wp = wm + Mp;
         for (int i = threadIdx.x; i < q.p; i += G * GPB) c[i] = ((const V *)rr[t]->bc)[i];
         for (int i = threadIdx.x; i < q.M; i += G * GPB) {
             H[i] = ((const V *)rr[t]->bH)[i];
-            wm[i] = ((const V *)rr[t]->bwm)[i];
-            wp[i] = ((const V *)rr[t]->bwp)[i];
+            wm[i + (i >> 4)] = ((const V *)rr[t]->bwm)[i];
+            wp[i + (i >> 4)] = ((const V *)rr[t]->bwp)[i];
         }
         q.c = c; q.H = H; q.wm = wm; q.wp = wp;
-        btab = wp + q.M;
+        btab = wp + Mp;
     }
     const int bmx = max(blN.M, blL.M);
     const int grp = threadIdx.x / G, lane = threadIdx.x % G;
@@ -594,7 +597,7 @@ static size_t group_elems(const Axis1D &ax) {
     return (size_t)(2 * std::max<int64_t>(nfft * ax.N, ax.L) +
                     std::max<int64_t>(rp * ax.M * ax.N, 2 * std::max(ax.radN.bM, ax.radL.bM)));
 }
-static size_t blue_elems(const AnyRadix &r) { return r.bp ? (size_t)(r.bp + 3 * r.bM) : 0; }
+static size_t blue_elems(const AnyRadix &r) { return r.bp ? (size_t)(r.bp + 3 * r.bM + 2 * (r.bM / 16 + 1)) : 0; }
 static bool q_in_smem(const Axis1D &ax) { return ax.N * ax.M * ax.M <= 4096; }
 static size_t smem_for(const Axis1D &ax, int groups) {
     const size_t vs = ax.dtype == MCI_F64 ? 16 : 8;
