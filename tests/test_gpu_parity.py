@@ -142,6 +142,30 @@ def test_cfg2_shape_subset():
     assert row_rel(out, truth).max() < 1e-5   # vs analytic truth (fp32 input rounding included)
 
 
+def test_cfg2_full_batch_sampled():
+    """configs[1] at full size in the bench launch configuration (65,536 rows, one
+    launch of the default row kernel: store warpgroup, TMEM hand-off, L2 prefetch):
+    sampled rows vs the oracle, and on every row the coarse-site consistency
+    (Theorem consistency: the identity channel is reproduced,
+    f[16 n] = g_0[n])."""
+    m = mci()
+    c = synth.CONFIGS[2]
+    g = synth.cfg2_batch_fast(c["batch"], seed=2)
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"])
+    gt = torch.from_numpy(g).cuda()
+    f = plan.execute(gt)
+    torch.cuda.synchronize()
+    pick = [0, 1, 12345, 32767, 49151, c["batch"] - 1]
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    got = f[torch.tensor(pick).cuda()].double().cpu().numpy()
+    assert row_rel(got, P.eval(g[pick])).max() < F32_TOL
+    step = c["L"] // c["N"]
+    err = (f[:, ::step] - gt[:, 0, :]).abs().amax(dim=1)
+    scale = gt[:, 0, :].abs().amax(dim=1)
+    assert (err <= 1e-5 * scale).all().item()
+    del f
+
+
 # -------------------------------------------------------------------------- config 3
 def test_cfg3_shape_hilbert():
     """configs[2] shape: M=2 (f, f'), N=4096, L=65536, f and Hf."""
@@ -156,6 +180,35 @@ def test_cfg3_shape_hilbert():
     assert row_rel(hf[pick], P.eval(g[pick], hilbert=True)).max() < F32_TOL
     fr, hr = synth.cfg3_reference(0)
     assert row_rel(f[0], fr) < 1e-5 and row_rel(hf[0], hr) < 1e-5
+
+
+def test_cfg3_full_batch_sampled():
+    """configs[2] at full size in the bench launch configuration (4,096 rows, one launch
+    of the Hilbert kernel with its store warpgroup): sampled rows of f and Hf vs the
+    oracle; on every row the coarse-site consistency f[16 n] = g_0[n]
+    and the one-sidedness of the analytic signal f + i Hf (Example 4, PAPER.md:436-464:
+    its negative-frequency energy is zero up to fp32 round-off)."""
+    m = mci()
+    c = synth.CONFIGS[3]
+    g = synth.cfg3_rows(np.arange(c["batch"]), seed=3)
+    plan = m.Plan(c["M"], c["N"], c["L"], c["bank"], hilbert=True)
+    gt = torch.from_numpy(g).cuda()
+    f, hf = plan.execute(gt)
+    torch.cuda.synchronize()
+    pick = [0, 2047, c["batch"] - 1]
+    P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"])
+    idx = torch.tensor(pick).cuda()
+    assert row_rel(f[idx].double().cpu().numpy(), P.eval(g[pick])).max() < F32_TOL
+    assert row_rel(hf[idx].double().cpu().numpy(), P.eval(g[pick], hilbert=True)).max() < F32_TOL
+    step = c["L"] // c["N"]
+    err = (f[:, ::step] - gt[:, 0, :]).abs().amax(dim=1)
+    assert (err <= 1e-5 * gt[:, 0, :].abs().amax(dim=1)).all().item()
+    L = c["L"]
+    for r0 in range(0, c["batch"], 512):
+        z = torch.fft.fft(torch.complex(f[r0:r0 + 512], hf[r0:r0 + 512]).to(torch.complex128), dim=1)
+        neg = z[:, L // 2 + 1:].abs().pow(2).sum(dim=1)
+        tot = z.abs().pow(2).sum(dim=1)
+        assert (neg <= 1e-10 * tot).all().item()
 
 
 @pytest.mark.parametrize("qtab,variant", [(False, 0), (True, 0), (False, 1), (True, 1)])
