@@ -268,6 +268,7 @@ static cudaError_t fs_launch_t(const Axis1D &ax, int64_t batch, const void *g, v
     a.Uw = a.Tw + ws_sig * a.npair * ax.N;
     a.cmax = (decltype(a.cmax))(a.Uw + ws_sig * a.npi * ax.S);
     a.Qt = (const cv<T> *)ax.Qt; a.twF = (const cv<T> *)ax.twF; a.TW = ax.TW;
+    a.fbt = ax.TW == 1024 ? (const cv<T> *)ax.rowtab : nullptr;
     a.Kmod = ax.K % ax.N;
     a.delay_uniform = ax.bank_delay_uniform;
     a.lmn = ax.bank_delay_uniform ? ax.L / ((int64_t)ax.M * ax.N) : 0;

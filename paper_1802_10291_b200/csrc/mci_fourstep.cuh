@@ -38,6 +38,7 @@ template <typename T> struct FSArgs {
     int delay_uniform;  // closed-form solve for the uniform delay bank (Axis1D::bank_delay_uniform)
     int64_t lmn;        // L / (M N): e^{-i j tau_m} = conj(w_L^{j m lmn})
     typename std::conditional<sizeof(T) == 4, unsigned, unsigned long long>::type *cmax;  // [sig][M] |g| max bits
+    const cv<T> *fbt = nullptr;  // packed kernels' tables [tw16 256][tw32 1024][tw128 96] (plan block)
 };
 
 // exponent e with max|g_m| = f 2^e, f in [0.5, 1) (0 for an all-zero channel)

@@ -15,6 +15,26 @@ constexpr int N2 = 256, S2 = 1024;  // N1 = 1024 from mci_fourstep.cuh
 __device__ __forceinline__ int pad5(int a) { return a + (a >> 5); }
 __device__ __forceinline__ int pad4(int a) { return a + (a >> 4); }
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+// one bulk copy (cp.async.bulk + mbarrier transaction count) of a CTA's twiddle tables from
+// the plan block into shared memory; issued by thread 0, awaited by each thread before use
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tab_copy(void *dst, const void *src, uint32_t bytes, uint64_t *mb) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(mb)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(mb)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(mb))
+                 : "memory");
+}
+__device__ __forceinline__ void tab_wait(uint64_t *mb) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(su32(mb))
+                     : "memory");
+}
 }  // namespace fsf
 
 using pkx::pk;
@@ -28,7 +48,12 @@ __global__ void __launch_bounds__(256) mci_fsf_fa(const FSArgs<float> a) {
     constexpr int BS = 1056 + 2;  // per-FFT stride (== 2 mod 16: conflict-free)
     float2 *bufs = reinterpret_cast<float2 *>(smem);
     float2 *tw = bufs + 8 * BS;  // [32][32] e^{-2 pi i j i / 1024}
-    for (int q = threadIdx.x; q < 1024; q += 256) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    __shared__ __align__(8) uint64_t tmb;
+    if (a.fbt) {
+        if (threadIdx.x == 0) tab_copy(tw, a.fbt + 256, 1024 * 8, &tmb);
+    } else {
+        for (int q = threadIdx.x; q < 1024; q += 256) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    }
     __syncthreads();
     const int ntiles = N2 / 8;
     const int tile = blockIdx.x % ntiles;
@@ -54,6 +79,7 @@ __global__ void __launch_bounds__(256) mci_fsf_fa(const FSArgs<float> a) {
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
+    if (a.fbt) tab_wait(&tmb);
 #pragma unroll
     for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], mk(tw[j * 32 + i]));
     dft<32, -1>(x);
@@ -83,12 +109,17 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
     float2 *tw32 = tw16 + 256;                       // [32][32] e^{-2 pi i j i/1024}
     float2 *tw128 = tw32 + 1024;                     // [3][32] e^{2 pi i e j / 128}, e = 1, 2, 3
     float2 *twE = tw128 + 96;                        // [2][32] e^{2 pi i 32 res_r j / S}
-    for (int q = threadIdx.x; q < 256; q += 128) tw16[q] = __ldg(a.twF + ((4 * (q >> 4) * (q & 15)) & 1023));
-    for (int q = threadIdx.x; q < 1024; q += 128) tw32[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    __shared__ __align__(8) uint64_t tmb;
     const int q1 = blockIdx.x % (N1 / 2 + 1);
-    for (int q = threadIdx.x; q < 96; q += 128) {  // e^{+2 pi i e j / 128} = conj(twF[8 e j])
-        const float2 v = __ldg(a.twF + ((8 * ((q >> 5) + 1) * (q & 31)) & 1023));
-        tw128[q] = make_float2(v.x, -v.y);
+    if (a.fbt) {  // tw16, tw32, tw128 are contiguous here and in the plan block
+        if (threadIdx.x == 0) tab_copy(tw16, a.fbt, (256 + 1024 + 96) * 8, &tmb);
+    } else {
+        for (int q = threadIdx.x; q < 256; q += 128) tw16[q] = __ldg(a.twF + ((4 * (q >> 4) * (q & 15)) & 1023));
+        for (int q = threadIdx.x; q < 1024; q += 128) tw32[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+        for (int q = threadIdx.x; q < 96; q += 128) {  // e^{+2 pi i e j / 128} = conj(twF[8 e j])
+            const float2 v = __ldg(a.twF + ((8 * ((q >> 5) + 1) * (q & 31)) & 1023));
+            tw128[q] = make_float2(v.x, -v.y);
+        }
     }
     for (int q = threadIdx.x; q < 64; q += 128) {
         const int rq = (q >> 5) == 0 ? q1 : N1 - q1;
@@ -116,6 +147,7 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
             asm volatile("bar.sync 1, 64;" ::: "memory");
 #pragma unroll
             for (int j = 0; j < 16; ++j) x[j] = mk(buf[pad4(b + 16 * j)]);
+            if (a.fbt) tab_wait(&tmb);
 #pragma unroll
             for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(tw16[j * 16 + b]));
             dft<16, -1>(x);
@@ -211,6 +243,7 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
     //    k' > K (j >= 16) is k = k' - S (negative, Y = conj X[S - k'], w^k = -i w^k'); k' = K
     //    (res = 0, k1 = 512) carries both.  w^{k'} = w^{res + N1 i} e^{2 pi i j / 128}.
     //    Zin(k') = W_{pa}(k) + i W_{pb}(k), W_p(k) = Y(k) w^{k p}, (pa, pb) = (2 ip, 2 ip + 1).
+    if (a.fbt) tab_wait(&tmb);  // complete long ago; every reading thread observes it
     if (tid < 128) {
         const int fi = tid >> 5, i = tid & 31, r = fi >> 1, ip = fi & 1;
         float2 *buf = ib + fi * IB;
@@ -287,7 +320,12 @@ __global__ void __launch_bounds__(512) mci_fsf_ic(const FSArgs<float> a) {
     constexpr int BS = 1056 + 1;  // == 1 mod 16: conflict-free for the 16 FFTs of a half-warp
     float2 *bufs = reinterpret_cast<float2 *>(smem);
     float2 *tw = bufs + 16 * BS;  // [32][32] e^{-2 pi i j i/1024}
-    for (int q = threadIdx.x; q < 1024; q += 512) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    __shared__ __align__(8) uint64_t tmb;
+    if (a.fbt) {
+        if (threadIdx.x == 0) tab_copy(tw, a.fbt + 256, 1024 * 8, &tmb);
+    } else {
+        for (int q = threadIdx.x; q < 1024; q += 512) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+    }
     __syncthreads();
     const int ntiles = S2 / 8;
     const int tile = blockIdx.x % ntiles;
@@ -306,6 +344,7 @@ __global__ void __launch_bounds__(512) mci_fsf_ic(const FSArgs<float> a) {
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
+    if (a.fbt) tab_wait(&tmb);
 #pragma unroll
     for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(tw[j * 32 + i])));
     dft<32, 1>(x);

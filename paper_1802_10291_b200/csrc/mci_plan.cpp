@@ -257,6 +257,19 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
         push_roots(blob, N, ax.LO, 1, -1);
         push_roots(blob, ax.S, ax.S / ax.LO, ax.LO, +1);
         push_roots(blob, ax.S, ax.LO, 1, +1);
+        // packed four-step kernels' shared-memory tables, laid out as they are copied (one bulk
+        // copy per CTA instead of per-entry gathers from twF): [tw16: 256][tw32: 1024][tw128: 96]
+        // tw16[q] = e^{-2 pi i 4 (q >> 4)(q & 15) / 1024}, tw32[q] = e^{-2 pi i (q >> 5)(q & 31) / 1024},
+        // tw128[q] = e^{+2 pi i 8 ((q >> 5) + 1)(q & 31) / 1024}  (the same roots as twF with TW = 1024)
+        offs.push_back(blob.size());
+        auto root1024 = [&](int64_t m, int sign) {
+            m %= 1024;
+            const double a = 2.0 * PI * (double)m / 1024.0;
+            push_c(blob, cd(std::cos(a), sign * std::sin(a)));
+        };
+        for (int q = 0; q < 256; ++q) root1024(4 * (q >> 4) * (q & 15), -1);
+        for (int q = 0; q < 1024; ++q) root1024((q >> 5) * (q & 31), -1);
+        for (int q = 0; q < 96; ++q) root1024(8 * ((q >> 5) + 1) * (q & 31), +1);
     }
     return MCI_OK;
 }
