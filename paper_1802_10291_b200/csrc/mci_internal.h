@@ -75,8 +75,10 @@ bool line_supported(const Axis1D &ax);
 bool hilbert_supported(const Axis1D &ax);
 cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *f, void *hf, cudaStream_t st,
                            int *n_launches);
+// tstore: 2D column pass whose output leaves transposed ([D1-block][L][D0] rows), see mci_line.cu
+bool line_tstore_ok(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, const void *f);
 cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
-                        int *n_launches);
+                        int *n_launches, bool tstore = false);
 // dispatch a fused-path axis to its kernel (specialised when available)
 cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                         cudaStream_t st, int *n_launches);

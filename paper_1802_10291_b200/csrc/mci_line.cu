@@ -35,7 +35,9 @@ constexpr int N = 512, S = 1024, L = 2048, K = 512, NQ = N / 2 + 1;
 // paddings (conflict-free for the access strides used, constant offsets per index)
 __device__ __forceinline__ int sw3(int a) { return a + (a >> 4); }  // forward 512 -> 544
 __device__ __forceinline__ int sw5(int a) { return a + (a >> 5); }  // inverse 1024 -> 1056
-constexpr int BUF = S + S / 32;
+// warp buffer stride: = 2 (mod 32) floats, so the tile write-out of the transposed-store
+// mode (thread (py, c) reads lines 4c..4c+3 at float py) hits 32 distinct banks
+constexpr int BUF = S + S / 32 + 1;
 constexpr int SP = N + 4;  // stage row stride: = 4 (mod 32) -> conflict-free transposed cp.async
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 // TM: per-lane tables in tensor memory (the kernel is bound by the shared-memory pipe).
@@ -74,7 +76,10 @@ struct LineTables {
     int deriv;          // 1: bank is (1, ik) -> closed-form inverse, no Q~ reads
 };
 
-template <int WARPS, bool TILED, bool TM = false>
+// TST (2D column pass, TILED only): the tile's 16 output lines leave transposed, as
+// f[(l0 / D0) L D0 + p D0 + (l0 % D0) + w] (row p of the 16 lines is 64 contiguous bytes),
+// through the warp buffers; the row pass then reads contiguous lines.
+template <int WARPS, bool TILED, bool TM = false, bool TST = false>
 __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
                                                               int64_t lines, RowAddr ra, LineTables tb) {
     using namespace linek;
@@ -158,16 +163,20 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
     // samples are strided.  Tile tl = [2][WARPS][N] is fetched by 4-byte cp.async: element
     // e = (m, n, l) (l fastest: 8 lanes read one 32-byte sector) lands at stage[(m WARPS + l) SP + n].
     const int64_t ntiles = (lines + WARPS - 1) / WARPS;
-    auto tile_base = [&](int64_t t) {
-        const int64_t l0 = t * WARPS;
-        return (l0 / (ra.D0 * ra.D1)) * ra.s2 + ((l0 / ra.D0) % ra.D1) * ra.s1 + (l0 % ra.D0) * ra.s0;
+    // line -> element offset; the launcher guarantees lines < 2^31, so the quotients are
+    // 32-bit (a 64-bit division is a long emulated sequence, measured ~8 % of the issue slots)
+    const uint32_t uD0 = (uint32_t)ra.D0, uD1 = (uint32_t)ra.D1;
+    auto line_base = [&](uint32_t l) -> int64_t {
+        const uint32_t a = l / uD0, r0 = l - a * uD0, b = a / uD1, r1 = a - b * uD1;
+        return (int64_t)b * ra.s2 + (int64_t)r1 * ra.s1 + (int64_t)r0 * ra.s0;
     };
-    auto fetch_tile = [&](int64_t t) {
+    auto tile_base = [&](int64_t t) { return line_base((uint32_t)(t * WARPS)); };
+    auto fetch_tile = [&](int64_t t, int64_t tb0) {
         if (t < ntiles && WARPS * 32 == 32 * 16) {
             // 32 elements per thread: line l = tid & 15, samples n = (tid >> 4) + 32 i, channel m;
             // addresses advance by constant strides (no per-element index arithmetic)
             const int l = threadIdx.x & 15, n0 = threadIdx.x >> 4;
-            const float *s0 = g + tile_base(t) + l + (int64_t)n0 * ra.ss;
+            const float *s0 = g + tb0 + l + (int64_t)n0 * ra.ss;
             const int64_t step = 32 * ra.ss;
             const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(stage + l * SP + n0);
 #pragma unroll
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
                                  : "memory");
             }
         } else if (t < ntiles) {
-            const float *src = g + tile_base(t);
+            const float *src = g + tb0;
 #pragma unroll 4
             for (int e = threadIdx.x; e < 2 * N * WARPS; e += WARPS * 32) {
                 const int l = e % WARPS, n = (e / WARPS) % N, m = e / (WARPS * N);
@@ -192,11 +201,15 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if constexpr (TILED) fetch_tile(blockIdx.x);
+    // TILED: D0 % WARPS == 0, so a tile's lines share the outer indices: base = tile base + warp s0
+    int64_t tbase = 0;
+    if constexpr (TILED) {
+        if ((int64_t)blockIdx.x < ntiles) tbase = tile_base(blockIdx.x);
+        fetch_tile(blockIdx.x, tbase);
+    }
     for (int64_t tl = blockIdx.x; tl < (TILED ? ntiles : (lines + WARPS - 1) / WARPS); tl += gridDim.x) {
         const int64_t line = tl * WARPS + warp;
-        const int64_t base =
-            (line / (ra.D0 * ra.D1)) * ra.s2 + ((line / ra.D0) % ra.D1) * ra.s1 + (line % ra.D0) * ra.s0;
+        const int64_t base = TILED ? tbase + warp * ra.s0 : line_base((uint32_t)line);
         const float *g0 = g + base, *g1 = g + base + ra.cs;
         pk x[16];
         float m0 = 0.f, m1 = 0.f;
@@ -214,7 +227,8 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
                 }
             }
             __syncthreads();  // stage consumed: fetch the CTA's next tile while this one is transformed
-            fetch_tile(tl + gridDim.x);
+            if (tl + gridDim.x < ntiles) tbase = tile_base(tl + gridDim.x);
+            fetch_tile(tl + gridDim.x, tbase);
             if (line >= lines) continue;
             __syncwarp();  // previous line's reads of buf are complete
         } else {
@@ -374,9 +388,31 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
             y[31] = pkx::cmul(y[31], mk(iw[960 + lane]));
         }
         dft<32, 1>(y);
-        float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
+        if constexpr (TST) {
+            // lines % WARPS == 0 (launcher), so every warp of the tile gets here
+            __syncwarp();  // pass-2 reads of buf are complete
 #pragma unroll
-        for (int j = 0; j < 32; ++j) __stcs(fo + lane + 32 * j, f2(y[j]));
+            for (int j = 0; j < 32; ++j) buf[lane + 32 * j] = f2(y[j]);  // f[2 p2 + e] at float 2 p2 + e
+            __syncthreads();  // the tile's 16 lines are in the warp buffers
+            const int64_t l0 = tl * WARPS;
+            float *ob = f + (l0 / ra.D0) * (int64_t)L * ra.D0 + (l0 % ra.D0);
+            const float *bf = reinterpret_cast<const float *>(bufs);
+            const int c = threadIdx.x & 3;
+#pragma unroll 4
+            for (int py = threadIdx.x >> 2; py < L; py += WARPS * 8) {
+                float4 v;
+                v.x = bf[(4 * c + 0) * 2 * BUF + py];
+                v.y = bf[(4 * c + 1) * 2 * BUF + py];
+                v.z = bf[(4 * c + 2) * 2 * BUF + py];
+                v.w = bf[(4 * c + 3) * 2 * BUF + py];
+                __stcs(reinterpret_cast<float4 *>(ob + py * ra.D0) + c, v);
+            }
+            __syncthreads();  // warp buffers free for the next tile
+        } else {
+            float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) __stcs(fo + lane + 32 * j, f2(y[j]));
+        }
     }
     if (TM) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -393,9 +429,18 @@ bool line_supported(const Axis1D &ax) {
 
 size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 512 + 1024; }
 
+bool line_tstore_ok(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, const void *f) {
+    if (getenv("MCI_2D_TSTORE") && atoi(getenv("MCI_2D_TSTORE")) == 0) return false;
+    return line_supported(ax) && ra.s0 == 1 && ra.ss != 1 && ra.D0 % 16 == 0 && lines % 16 == 0 &&
+           (((uintptr_t)g) & 15) == 0 && (((uintptr_t)f) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 &&
+           ra.s1 % 4 == 0 && ra.s2 % 4 == 0;
+}
+
 cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
-                        int *n_launches) {
+                        int *n_launches, bool tstore) {
     if (lines <= 0) return cudaSuccess;
+    if (tstore && !line_tstore_ok(ax, ra, lines, g, f)) return cudaErrorInvalidValue;
+    if (lines >= ((int64_t)1 << 31) - 64) return cudaErrorInvalidValue;  // 32-bit line quotients
     LineTables tb;
     tb.Qt = (const float2 *)ax.Qt;
     const float2 *base = (const float2 *)ax.rowtab;  // [wp K+1][fwt 32x16][iw 32x32]
@@ -410,8 +455,9 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // default: per-lane pre-twiddle and inverse pass-2 twiddle tables in tensor memory;
     // MCI_LINE_VARIANT=1: all tables in shared memory (A/B)
     const bool tm = !(getenv("MCI_LINE_VARIANT") && atoi(getenv("MCI_LINE_VARIANT")) == 1);
-    auto kern = tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
-                      : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
+    auto kern = tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
+                : tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
+                        : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
     const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
                         (tiled ? (size_t)2 * WARPS * linek::SP * 4 : 0);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

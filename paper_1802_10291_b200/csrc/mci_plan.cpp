@@ -597,12 +597,22 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
         mci::RowAddr rc;
         rc.D0 = Nx; rc.D1 = Mx; rc.s0 = 1; rc.s1 = Ny * Nx; rc.s2 = My * Mx * Ny * Nx;
         rc.cs = Mx * Ny * Nx; rc.ss = Nx;
-        cudaError_t e = mci::launch_axis(p->ay, rc, ni * Mx * Nx, gi, p->ws, nullptr, st, nl);
+        // line kernels on both axes: the column pass stores ws transposed, ws[img][mx][py][nx],
+        // so the row pass reads contiguous lines (measured: 0.33 -> 0.25 ms per 65,536 lines)
+        const bool tws = p->ay.special == 2 && p->ax.special == 2 &&
+                         mci::line_tstore_ok(p->ay, rc, ni * Mx * Nx, gi, p->ws);
+        cudaError_t e = tws ? mci::launch_line(p->ay, rc, ni * Mx * Nx, gi, p->ws, st, nl, true)
+                            : mci::launch_axis(p->ay, rc, ni * Mx * Nx, gi, p->ws, nullptr, st, nl);
         if (e != cudaSuccess) return MCI_E_CUDA;
         // row pass (along x, channels mx) on ws -> out[img][py][Lx]
         mci::RowAddr rr;
-        rr.D0 = Ly; rr.D1 = 1; rr.s0 = 1; rr.s1 = 0; rr.s2 = Mx * Nx * Ly;
-        rr.cs = Nx * Ly; rr.ss = Ly;
+        if (tws) {  // ws[img][mx][py][nx]: line py, channel stride Ly Nx, samples contiguous
+            rr.D0 = Ly; rr.D1 = 1; rr.s0 = Nx; rr.s1 = 0; rr.s2 = Mx * Ly * Nx;
+            rr.cs = Ly * Nx; rr.ss = 1;
+        } else {  // ws[img][mx][nx][py]: samples strided by Ly
+            rr.D0 = Ly; rr.D1 = 1; rr.s0 = 1; rr.s1 = 0; rr.s2 = Mx * Nx * Ly;
+            rr.cs = Nx * Ly; rr.ss = Ly;
+        }
         e = mci::launch_axis(p->ax, rr, ni * Ly, p->ws, oi, nullptr, st, nl);
         if (e != cudaSuccess) return MCI_E_CUDA;
     }

@@ -352,6 +352,32 @@ def test_cfg5_full_size_sampled(qtab, variant, monkeypatch):
         assert 10 * np.log10(255 ** 2 / mse) > 15.0
 
 
+@pytest.mark.parametrize("ws_mb", ["256", "24"])
+def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
+    """Line kernels on both axes: the column pass stores the workspace transposed
+    (ws[img][mx][py][nx]) so the row pass reads contiguous lines.  Same per-line
+    arithmetic as the strided workspace (MCI_2D_TSTORE=0), so the images agree bit for
+    bit; 24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk)."""
+    m = mci()
+    monkeypatch.setenv("MCI_2D_WS_MB", ws_mb)
+    g = np.random.default_rng(55).standard_normal((5, 2, 2, 512, 512)).astype(np.float32)
+    g[:, 0, 1] *= 64.0
+    g[:, 1, 0] *= 64.0
+    g[:, 1, 1] *= 4096.0
+    gt = torch.from_numpy(g).cuda()
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MCI_2D_TSTORE", flag)
+        plan = m.Plan2D(2, 512, BANKS["f_df"], 2, 512, BANKS["f_df"], 4)
+        outs.append(plan.execute(gt).cpu().numpy())
+        del plan
+    assert np.array_equal(outs[0], outs[1])
+    px = oracle.OraclePlan(2, 512, 2048, BANKS["f_df"])
+    cols = [3, 1000, 2046]
+    ref = oracle.eval_2d_columns(g[4], px, px, cols)
+    assert np.linalg.norm(outs[0][4][:, cols] - ref) / np.linalg.norm(ref) < F32_TOL
+
+
 # -------------------------------------------------------------------------- host API
 def test_host_execute_matches_device():
     m = mci()
