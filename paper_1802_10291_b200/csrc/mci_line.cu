@@ -79,7 +79,9 @@ struct LineTables {
 // TST (2D column pass, TILED only): the tile's 16 output lines leave transposed, as
 // f[(l0 / D0) L D0 + p D0 + (l0 % D0) + w] (row p of the 16 lines is 64 contiguous bytes),
 // through the warp buffers; the row pass then reads contiguous lines.
-template <int WARPS, bool TILED, bool TM = false, bool TST = false>
+// PF (contiguous lines, untiled): the next line's two channel rows are copied by 16-byte
+// cp.async into the warp's own buffer while the current line's inverse finishes.
+template <int WARPS, bool TILED, bool TM = false, bool TST = false, bool PF = false>
 __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
                                                               int64_t lines, RowAddr ra, LineTables tb) {
     using namespace linek;
@@ -201,6 +203,22 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    // PF: stage = floats [0, 2N) of the warp buffer, 16-byte aligned (BUF is odd)
+    float *pstage = reinterpret_cast<float *>(buf + (warp & 1));
+    auto prefetch_line = [&](int64_t ln) {
+        if (ln < lines) {
+            const float *src = g + line_base((uint32_t)ln);
+            const uint32_t d = (uint32_t)__cvta_generic_to_shared(pstage);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int c = lane + 32 * i, m = c >> 7, n = 4 * (c & 127);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16u * c), "l"(src + m * ra.cs + n)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (PF) prefetch_line((int64_t)blockIdx.x * WARPS + warp);
     // TILED: D0 % WARPS == 0, so a tile's lines share the outer indices: base = tile base + warp s0
     int64_t tbase = 0;
     if constexpr (TILED) {
@@ -231,6 +249,19 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
             fetch_tile(tl + gridDim.x, tbase);
             if (line >= lines) continue;
             __syncwarp();  // previous line's reads of buf are complete
+        } else if constexpr (PF) {
+            if (line >= lines) continue;
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            __syncwarp();  // this line's rows have landed in the warp buffer
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int n = lane + 32 * j;
+                const float a = pstage[n], b = pstage[N + n];
+                m0 = fmaxf(m0, fabsf(a));
+                m1 = fmaxf(m1, fabsf(b));
+                x[j] = mk(a, b);
+            }
+            __syncwarp();  // stage read: the forward pass may overwrite the buffer
         } else {
             if (line >= lines) continue;
             __syncwarp();  // previous line's reads of buf are complete
@@ -369,6 +400,10 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         // ---- pass 2 (Ls = 32)
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
+        if constexpr (PF) {
+            __syncwarp();  // buffer read: the next line's rows may land in it
+            prefetch_line(line + (int64_t)gridDim.x * WARPS);
+        }
         if constexpr (TM) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) {  // twiddles j = 8c+1 .. 8c+8 (j <= 31)
@@ -451,12 +486,16 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     const bool tiled = ra.s0 == 1 && ra.ss != 1 && ra.D0 % 16 == 0 &&
                        (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 && ra.s1 % 4 == 0 &&
                        ra.s2 % 4 == 0;
+    // contiguous 16-byte-aligned lines: cp.async prefetch of the next line (MCI_LINE_PF=0: direct loads)
+    const bool pf = !tiled && ra.ss == 1 && (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.s0 % 4 == 0 &&
+                    ra.s1 % 4 == 0 && ra.s2 % 4 == 0 && !(getenv("MCI_LINE_PF") && atoi(getenv("MCI_LINE_PF")) == 0);
     const int WARPS = tiled ? 16 : 8;  // tiled: one 16-warp CTA per SM; else two 8-warp CTAs
     // default: per-lane pre-twiddle and inverse pass-2 twiddle tables in tensor memory;
     // MCI_LINE_VARIANT=1: all tables in shared memory (A/B)
     const bool tm = !(getenv("MCI_LINE_VARIANT") && atoi(getenv("MCI_LINE_VARIANT")) == 1);
     auto kern = tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
                 : tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
+                : pf    ? (tm ? mci_line_kernel<8, false, true, false, true> : mci_line_kernel<8, false, false, false, true>)
                         : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
     const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
                         (tiled ? (size_t)2 * WARPS * linek::SP * 4 : 0);

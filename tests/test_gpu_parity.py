@@ -378,6 +378,34 @@ def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
     assert np.linalg.norm(outs[0][4][:, cols] - ref) / np.linalg.norm(ref) < F32_TOL
 
 
+def test_line_kernel_prefetch_rows(monkeypatch):
+    """Contiguous 1D lines of the 2D-pass shape (M=2, N=512, L=2048): the cp.async
+    next-line prefetch path agrees bit for bit with direct loads (MCI_LINE_PF=0) and
+    with an input 4 bytes off 16-byte alignment (prefetch off); 5,003 rows make every
+    warp run several lines (persistent loop, ragged tail); sampled rows vs the oracle."""
+    m = mci()
+    bank = BANKS["f_df"]
+    rows = 5003
+    g = np.random.default_rng(77).standard_normal((rows, 2, 512)).astype(np.float32)
+    g[:, 1] *= 300.0
+    gt = torch.from_numpy(g).cuda()
+    outs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("MCI_LINE_PF", flag)
+        plan = m.Plan(2, 512, 2048, bank)
+        outs.append(plan.execute(gt).cpu().numpy())
+    raw = torch.empty(rows * 1024 + 1, device="cuda")
+    raw[1:].copy_(gt.reshape(-1))
+    mis = raw[1:].view(rows, 2, 512)
+    assert mis.data_ptr() % 16 == 4
+    monkeypatch.setenv("MCI_LINE_PF", "1")
+    outs.append(plan.execute(mis).cpu().numpy())
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+    P = oracle.OraclePlan(2, 512, 2048, bank)
+    pick = [0, 1, 2367, 2368, rows - 1]
+    assert row_rel(outs[0][pick].astype(np.float64), P.eval(g[pick])).max() < F32_TOL
+
+
 # -------------------------------------------------------------------------- host API
 def test_host_execute_matches_device():
     m = mci()
