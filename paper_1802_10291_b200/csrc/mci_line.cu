@@ -23,6 +23,7 @@
 // shared-memory pipe that bounds the kernel; for the (1, ik) bank the solve uses
 // the closed-form inverse instead of the Q~ table.
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "mci_internal.h"
@@ -76,13 +77,13 @@ struct LineTables {
     int deriv;          // 1: bank is (1, ik) -> closed-form inverse, no Q~ reads
 };
 
-// TST (2D column pass, TILED only): the tile's 16 output lines leave transposed, as
+// TST (2D passes; TILED, or untiled with PF): the tile's 16 output lines leave transposed, as
 // f[(l0 / D0) L D0 + p D0 + (l0 % D0) + w] (row p of the 16 lines is 64 contiguous bytes),
 // through the warp buffers; the row pass then reads contiguous lines.
 // PF (contiguous lines, untiled): the next line's two channel rows are copied by 16-byte
 // cp.async into the warp's own buffer while the current line's inverse finishes.
 template <int WARPS, bool TILED, bool TM = false, bool TST = false, bool PF = false>
-__global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
+__global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
                                                               int64_t lines, RowAddr ra, LineTables tb) {
     using namespace linek;
     using namespace pkx;
@@ -91,8 +92,12 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
     float2 *wps = Qs + NQ * 4;                      // K+1 (+1 pad)
     float2 *fwt = wps + K + 2;                      // 512
     float2 *iw = fwt + 512;                         // 1024
-    float2 *bufs = iw + 1024;                       // WARPS x BUF
-    float *stage = reinterpret_cast<float *>(bufs + WARPS * BUF);  // TILED: [2][WARPS][SP]
+    // (measured: running the untiled TST CTA as two independent 8-warp halves with 8-line
+    // tiles and named barriers was slower, 0.33 -> 0.39 ms per 65,536 lines)
+    constexpr int TW = WARPS;  // lines per tile
+    constexpr int BUFS = BUF;
+    float2 *bufs = iw + 1024;                       // WARPS x BUFS
+    float *stage = reinterpret_cast<float *>(bufs + WARPS * BUFS);  // TILED: [2][WARPS][SP]
     for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
     for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
     // pass-2 twiddles re-laid as pairs for 128-bit loads (the kernel is MIO-bound):
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
     auto ldQ = [&](int i) { return Qs[i]; };
     auto ldwp = [&](int i) { return wps[i]; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float2 *buf = bufs + warp * BUF;
+    float2 *buf = bufs + warp * BUFS;
     const uint32_t tmA = TM ? tm_base + ((uint32_t)(32 * (warp & 3)) << 16) : 0u;
 
     // TILED (2D passes): WARPS consecutive lines are adjacent in memory (s0 = 1) while
@@ -203,8 +208,9 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // PF: stage = floats [0, 2N) of the warp buffer, 16-byte aligned (BUF is odd)
-    float *pstage = reinterpret_cast<float *>(buf + (warp & 1));
+    // PF: stage = floats [0, 2N) of the warp buffer, 16-byte aligned (BUF is odd); with TST
+    // the buffer carries the outputs, so the stage is a separate [WARPS][2N] region
+    float *pstage = (TST && !TILED) ? stage + warp * 2 * N : reinterpret_cast<float *>(buf + (warp & 1));
     auto prefetch_line = [&](int64_t ln) {
         if (ln < lines) {
             const float *src = g + line_base((uint32_t)ln);
@@ -225,8 +231,12 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         if ((int64_t)blockIdx.x < ntiles) tbase = tile_base(blockIdx.x);
         fetch_tile(blockIdx.x, tbase);
     }
-    for (int64_t tl = blockIdx.x; tl < (TILED ? ntiles : (lines + WARPS - 1) / WARPS); tl += gridDim.x) {
-        const int64_t line = tl * WARPS + warp;
+    // tile tl = lines tl TW .. + TW - 1; warp -> (half, index): line = blockIdx.x WARPS + warp
+    // + k gridDim.x WARPS in every mode
+    constexpr int NH = WARPS / TW;
+    for (int64_t tl = (int64_t)blockIdx.x * NH + warp / TW; tl < (TILED ? ntiles : (lines + TW - 1) / TW);
+         tl += (int64_t)gridDim.x * NH) {
+        const int64_t line = tl * TW + warp % TW;
         const int64_t base = TILED ? tbase + warp * ra.s0 : line_base((uint32_t)line);
         const float *g0 = g + base, *g1 = g + base + ra.cs;
         pk x[16];
@@ -262,6 +272,7 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
                 x[j] = mk(a, b);
             }
             __syncwarp();  // stage read: the forward pass may overwrite the buffer
+            if constexpr (TST) prefetch_line(line + (int64_t)gridDim.x * WARPS);  // separate stage
         } else {
             if (line >= lines) continue;
             __syncwarp();  // previous line's reads of buf are complete
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
         // ---- pass 2 (Ls = 32)
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
-        if constexpr (PF) {
+        if constexpr (PF && !TST) {
             __syncwarp();  // buffer read: the next line's rows may land in it
             prefetch_line(line + (int64_t)gridDim.x * WARPS);
         }
@@ -428,21 +439,23 @@ __global__ void __launch_bounds__(WARPS * 32, TILED ? 1 : 2) mci_line_kernel(con
             __syncwarp();  // pass-2 reads of buf are complete
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[lane + 32 * j] = f2(y[j]);  // f[2 p2 + e] at float 2 p2 + e
-            __syncthreads();  // the tile's 16 lines are in the warp buffers
-            const int64_t l0 = tl * WARPS;
+            const int64_t l0 = tl * TW;
             float *ob = f + (l0 / ra.D0) * (int64_t)L * ra.D0 + (l0 % ra.D0);
-            const float *bf = reinterpret_cast<const float *>(bufs);
-            const int c = threadIdx.x & 3;
+            {
+                __syncthreads();  // the tile's 16 lines are in the warp buffers
+                const float *bf = reinterpret_cast<const float *>(bufs);
+                const int c = threadIdx.x & 3;
 #pragma unroll 4
-            for (int py = threadIdx.x >> 2; py < L; py += WARPS * 8) {
-                float4 v;
-                v.x = bf[(4 * c + 0) * 2 * BUF + py];
-                v.y = bf[(4 * c + 1) * 2 * BUF + py];
-                v.z = bf[(4 * c + 2) * 2 * BUF + py];
-                v.w = bf[(4 * c + 3) * 2 * BUF + py];
-                __stcs(reinterpret_cast<float4 *>(ob + py * ra.D0) + c, v);
+                for (int py = threadIdx.x >> 2; py < L; py += WARPS * 8) {
+                    float4 v;
+                    v.x = bf[(4 * c + 0) * 2 * BUFS + py];
+                    v.y = bf[(4 * c + 1) * 2 * BUFS + py];
+                    v.z = bf[(4 * c + 2) * 2 * BUFS + py];
+                    v.w = bf[(4 * c + 3) * 2 * BUFS + py];
+                    __stcs(reinterpret_cast<float4 *>(ob + py * ra.D0) + c, v);
+                }
+                __syncthreads();  // warp buffers free for the next tile
             }
-            __syncthreads();  // warp buffers free for the next tile
         } else {
             float2 *fo = reinterpret_cast<float2 *>(f + line * (int64_t)L);
 #pragma unroll
@@ -466,9 +479,11 @@ size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 512 + 1024; }
 
 bool line_tstore_ok(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, const void *f) {
     if (getenv("MCI_2D_TSTORE") && atoi(getenv("MCI_2D_TSTORE")) == 0) return false;
-    return line_supported(ax) && ra.s0 == 1 && ra.ss != 1 && ra.D0 % 16 == 0 && lines % 16 == 0 &&
-           (((uintptr_t)g) & 15) == 0 && (((uintptr_t)f) & 15) == 0 && ra.cs % 4 == 0 && ra.ss % 4 == 0 &&
-           ra.s1 % 4 == 0 && ra.s2 % 4 == 0;
+    const bool tiled_in = ra.s0 == 1 && ra.ss != 1 && ra.ss % 4 == 0;  // adjacent lines, strided samples
+    const bool contig_in = ra.ss == 1 && ra.s0 % 4 == 0;               // contiguous lines (prefetched)
+    return line_supported(ax) && (tiled_in || contig_in) && ra.D0 % 16 == 0 && lines % 16 == 0 &&
+           (((uintptr_t)g) & 15) == 0 && (((uintptr_t)f) & 15) == 0 && ra.cs % 4 == 0 && ra.s1 % 4 == 0 &&
+           ra.s2 % 4 == 0;
 }
 
 cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, void *f, cudaStream_t st,
@@ -489,22 +504,40 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // contiguous 16-byte-aligned lines: cp.async prefetch of the next line (MCI_LINE_PF=0: direct loads)
     const bool pf = !tiled && ra.ss == 1 && (((uintptr_t)g) & 15) == 0 && ra.cs % 4 == 0 && ra.s0 % 4 == 0 &&
                     ra.s1 % 4 == 0 && ra.s2 % 4 == 0 && !(getenv("MCI_LINE_PF") && atoi(getenv("MCI_LINE_PF")) == 0);
-    const int WARPS = tiled ? 16 : 8;  // tiled: one 16-warp CTA per SM; else two 8-warp CTAs
+    // tiled or transposed-store: one 16-warp CTA per SM (a tile = 16 lines); else two 8-warp CTAs
+    const bool tstore_c = tstore && !tiled;  // untiled transposed store (prefetched contiguous lines)
+    if (tstore_c && !pf) return cudaErrorInvalidValue;
+    const int WARPS = (tiled || tstore) ? 16 : 8;
     // default: per-lane pre-twiddle and inverse pass-2 twiddle tables in tensor memory;
     // MCI_LINE_VARIANT=1: all tables in shared memory (A/B)
-    const bool tm = !(getenv("MCI_LINE_VARIANT") && atoi(getenv("MCI_LINE_VARIANT")) == 1);
-    auto kern = tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
+    const int lv = getenv("MCI_LINE_VARIANT") ? atoi(getenv("MCI_LINE_VARIANT")) : 2;
+    const bool tm = lv == 0 || (lv == 2 && tiled);
+    auto kern = tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
+                : tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
                 : tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
                 : pf    ? (tm ? mci_line_kernel<8, false, true, false, true> : mci_line_kernel<8, false, false, false, true>)
                         : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
     const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
-                        (tiled ? (size_t)2 * WARPS * linek::SP * 4 : 0);
+                        (tiled ? (size_t)2 * WARPS * linek::SP * 4 : tstore_c ? (size_t)WARPS * 2 * linek::N * 4 : 0);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
+    if (getenv("MCI_DEBUG")) {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, kern);
+        int occ0 = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ0, kern, WARPS * 32, 0);
+        size_t avail = 0;
+        const cudaError_t ea = cudaOccupancyAvailableDynamicSMemPerBlock(&avail, kern, 2, WARPS * 32);
+        if (ea != cudaSuccess) fprintf(stderr, "mci: avail query: %s\n", cudaGetErrorString(ea));
+        cudaGetLastError();
+        fprintf(stderr, "mci: line kernel warps=%d tiled=%d tstore=%d pf=%d smem=%zu occ=%d occ(smem0)=%d regs=%d static=%zu local=%zu avail2=%zu\n",
+                WARPS, (int)tiled, (int)tstore, (int)pf, smem, occ, occ0, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, avail);
+    }
     if (occ < 1) occ = 1;
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (lines + WARPS - 1) / WARPS;

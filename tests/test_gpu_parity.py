@@ -354,10 +354,13 @@ def test_cfg5_full_size_sampled(qtab, variant, monkeypatch):
 
 @pytest.mark.parametrize("ws_mb", ["256", "24"])
 def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
-    """Line kernels on both axes: the column pass stores the workspace transposed
-    (ws[img][mx][py][nx]) so the row pass reads contiguous lines.  Same per-line
-    arithmetic as the strided workspace (MCI_2D_TSTORE=0), so the images agree bit for
-    bit; 24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk)."""
+    """Line kernels on both axes.  Default: column pass first, storing the workspace
+    transposed (ws[img][mx][py][nx]) so the row pass reads contiguous lines.
+    MCI_2D_TSTORE=0: column first with a strided workspace (same per-line arithmetic:
+    bit-identical).  MCI_2D_ORDER=1: row pass first on contiguous input lines, storing
+    ws[img][my][px][ny], then the column pass on contiguous lines storing the image
+    transposed: the other pass order (order-independent), equal to fp32
+    rounding.  24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk)."""
     m = mci()
     monkeypatch.setenv("MCI_2D_WS_MB", ws_mb)
     g = np.random.default_rng(55).standard_normal((5, 2, 2, 512, 512)).astype(np.float32)
@@ -366,16 +369,23 @@ def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
     g[:, 1, 1] *= 4096.0
     gt = torch.from_numpy(g).cuda()
     outs = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("MCI_2D_TSTORE", flag)
+    for env in ({}, {"MCI_2D_ORDER": "1"}, {"MCI_2D_TSTORE": "0"}):
+        for k in ("MCI_2D_ORDER", "MCI_2D_TSTORE"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
         plan = m.Plan2D(2, 512, BANKS["f_df"], 2, 512, BANKS["f_df"], 4)
         outs.append(plan.execute(gt).cpu().numpy())
         del plan
-    assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
+    for i in range(5):
+        a, b = outs[1][i].astype(np.float64), outs[0][i].astype(np.float64)
+        assert np.linalg.norm(a - b) / np.linalg.norm(b) < F32_TOL
     px = oracle.OraclePlan(2, 512, 2048, BANKS["f_df"])
     cols = [3, 1000, 2046]
     ref = oracle.eval_2d_columns(g[4], px, px, cols)
-    assert np.linalg.norm(outs[0][4][:, cols] - ref) / np.linalg.norm(ref) < F32_TOL
+    for o in outs[:2]:
+        assert np.linalg.norm(o[4][:, cols] - ref) / np.linalg.norm(ref) < F32_TOL
 
 
 def test_line_kernel_prefetch_rows(monkeypatch):
