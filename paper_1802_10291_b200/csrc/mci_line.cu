@@ -39,7 +39,7 @@ __device__ __forceinline__ int sw5(int a) { return a + (a >> 5); }  // inverse 1
 // warp buffer stride: = 2 (mod 32) floats, so the tile write-out of the transposed-store
 // mode (thread (py, c) reads lines 4c..4c+3 at float py) hits 32 distinct banks
 constexpr int BUF = S + S / 32 + 1;
-constexpr int SP = N + 4;  // stage row stride: = 4 (mod 32) -> conflict-free transposed cp.async
+constexpr int SP = N + 2;  // stage row stride = 2 (mod 32): the transposed cp.async (lines l, l + 8 of a warp) hits 32 banks
 __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
 // TM: per-lane tables in tensor memory (the kernel is bound by the shared-memory pipe).
 // Every warp's lane l reads the same values, so each lane quarter holds a copy:
