@@ -80,7 +80,7 @@ struct LineTables {
 // TST (2D passes; TILED, or untiled with PF): the tile's 16 output lines leave transposed, as
 // f[(l0 / D0) L D0 + p D0 + (l0 % D0) + w] (row p of the 16 lines is 64 contiguous bytes),
 // through the warp buffers; the row pass then reads contiguous lines.
-// PF (contiguous lines, untiled): the next line's two channel rows are copied by 16-byte
+// PF (contiguous lines, untiled; with TILED it selects the G16 gather below): the next line's two channel rows are copied by 16-byte
 // cp.async into the warp's own buffer while the current line's inverse finishes.
 template <int WARPS, bool TILED, bool TM = false, bool TST = false, bool PF = false>
 __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
@@ -178,8 +178,24 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         return (int64_t)b * ra.s2 + (int64_t)r1 * ra.s1 + (int64_t)r0 * ra.s0;
     };
     auto tile_base = [&](int64_t t) { return line_base((uint32_t)(t * WARPS)); };
+    // G16 (TILED with PF set): the tile is gathered by 16-byte cp.async into [m][n][16 lines]
+    // rows of 64 B whose 16-byte chunks are XOR-swizzled by (n >> 1) & 3 (8 copies per
+    // thread instead of 32); a warp's column reads are then 4-way bank conflicted
+    constexpr bool G16 = TILED && PF;
+    auto g16_idx = [](int m, int n, int l) { return ((m * N + n) << 4) + ((((l >> 2) ^ (n >> 1)) & 3) << 2) + (l & 3); };
     auto fetch_tile = [&](int64_t t, int64_t tb0) {
-        if (t < ntiles && WARPS * 32 == 32 * 16) {
+        if (G16) {
+            if (t < ntiles) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int q = threadIdx.x + WARPS * 32 * i, c = q & 3, n = (q >> 2) & (N - 1), m = q >> 11;
+                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + g16_idx(m, n, 4 * c));
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
+                                 "l"(g + tb0 + m * ra.cs + (int64_t)n * ra.ss + 4 * c)
+                                 : "memory");
+                }
+            }
+        } else if (t < ntiles && WARPS * 32 == 32 * 16) {
             // 32 elements per thread: line l = tid & 15, samples n = (tid >> 4) + 32 i, channel m;
             // addresses advance by constant strides (no per-element index arithmetic)
             const int l = threadIdx.x & 15, n0 = threadIdx.x >> 4;
@@ -224,7 +240,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    if constexpr (PF) prefetch_line((int64_t)blockIdx.x * WARPS + warp);
+    if constexpr (PF && !TILED) prefetch_line((int64_t)blockIdx.x * WARPS + warp);
     // TILED: D0 % WARPS == 0, so a tile's lines share the outer indices: base = tile base + warp s0
     int64_t tbase = 0;
     if constexpr (TILED) {
@@ -248,7 +264,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const int n = lane + 32 * j;
-                    const float a = stage[warp * SP + n], b = stage[(WARPS + warp) * SP + n];
+                    const float a = G16 ? stage[g16_idx(0, n, warp)] : stage[warp * SP + n];
+                    const float b = G16 ? stage[g16_idx(1, n, warp)] : stage[(WARPS + warp) * SP + n];
                     m0 = fmaxf(m0, fabsf(a));
                     m1 = fmaxf(m1, fabsf(b));
                     x[j] = mk(a, b);
@@ -411,7 +428,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         // ---- pass 2 (Ls = 32)
 #pragma unroll
         for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw5(lane + 32 * j)]);
-        if constexpr (PF && !TST) {
+        if constexpr (PF && !TILED && !TST) {
             __syncwarp();  // buffer read: the next line's rows may land in it
             prefetch_line(line + (int64_t)gridDim.x * WARPS);
         }
@@ -508,12 +525,17 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     const bool tstore_c = tstore && !tiled;  // untiled transposed store (prefetched contiguous lines)
     if (tstore_c && !pf) return cudaErrorInvalidValue;
     const int WARPS = (tiled || tstore) ? 16 : 8;
+    // tiled passes: 16-byte gather into a swizzled [m][n][16] stage (config 5: 0.808 -> 0.775
+    // ms); MCI_LINE_G16=0: 4-byte transposing cp.async into [m][l][SP] (A/B)
+    const bool g16 = tiled && !(getenv("MCI_LINE_G16") && atoi(getenv("MCI_LINE_G16")) == 0);
     // default: per-lane pre-twiddle and inverse pass-2 twiddle tables in tensor memory;
     // MCI_LINE_VARIANT=1: all tables in shared memory (A/B)
     const int lv = getenv("MCI_LINE_VARIANT") ? atoi(getenv("MCI_LINE_VARIANT")) : 2;
     const bool tm = lv == 0 || (lv == 2 && tiled);
     auto kern = tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
+                : (tstore && g16) ? (tm ? mci_line_kernel<16, true, true, true, true> : mci_line_kernel<16, true, false, true, true>)
                 : tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
+                : (tiled && g16) ? (tm ? mci_line_kernel<16, true, true, false, true> : mci_line_kernel<16, true, false, false, true>)
                 : tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
                 : pf    ? (tm ? mci_line_kernel<8, false, true, false, true> : mci_line_kernel<8, false, false, false, true>)
                         : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);

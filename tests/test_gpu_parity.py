@@ -356,8 +356,9 @@ def test_cfg5_full_size_sampled(qtab, variant, monkeypatch):
 def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
     """Line kernels on both axes.  Default: column pass first, storing the workspace
     transposed (ws[img][mx][py][nx]) so the row pass reads contiguous lines.
-    MCI_2D_TSTORE=0: column first with a strided workspace (same per-line arithmetic:
-    bit-identical).  MCI_2D_ORDER=1: row pass first on contiguous input lines, storing
+    MCI_2D_TSTORE=0: column first with a strided workspace; MCI_LINE_G16=0: the tiled
+    gather by 4-byte transposing copies instead of 16-byte copies into a swizzled stage
+    (same per-line arithmetic: bit-identical).  MCI_2D_ORDER=1: row pass first on contiguous input lines, storing
     ws[img][my][px][ny], then the column pass on contiguous lines storing the image
     transposed: the other pass order (order-independent), equal to fp32
     rounding.  24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk)."""
@@ -369,15 +370,17 @@ def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
     g[:, 1, 1] *= 4096.0
     gt = torch.from_numpy(g).cuda()
     outs = []
-    for env in ({}, {"MCI_2D_ORDER": "1"}, {"MCI_2D_TSTORE": "0"}):
-        for k in ("MCI_2D_ORDER", "MCI_2D_TSTORE"):
+    for env in ({}, {"MCI_2D_ORDER": "1"}, {"MCI_2D_TSTORE": "0"}, {"MCI_LINE_G16": "0"},
+                {"MCI_2D_TSTORE": "0", "MCI_LINE_G16": "0"}):
+        for k in ("MCI_2D_ORDER", "MCI_2D_TSTORE", "MCI_LINE_G16"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         plan = m.Plan2D(2, 512, BANKS["f_df"], 2, 512, BANKS["f_df"], 4)
         outs.append(plan.execute(gt).cpu().numpy())
         del plan
-    assert np.array_equal(outs[0], outs[2])
+    for o in outs[2:]:  # gathers (16-byte swizzled / 4-byte transposing) and stores: same arithmetic
+        assert np.array_equal(outs[0], o)
     for i in range(5):
         a, b = outs[1][i].astype(np.float64), outs[0][i].astype(np.float64)
         assert np.linalg.norm(a - b) / np.linalg.norm(b) < F32_TOL
