@@ -460,16 +460,15 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
             float *ob = f + (l0 / ra.D0) * (int64_t)L * ra.D0 + (l0 % ra.D0);
             {
                 __syncthreads();  // the tile's 16 lines are in the warp buffers
-                const float *bf = reinterpret_cast<const float *>(bufs);
+                // thread (c, p2): lines 4c..4c+3 of rows 2 p2, 2 p2 + 1 (one 64-bit read per line;
+                // buffer stride = 1 (mod 16) float2, so a half-warp's reads hit 16 bank pairs)
                 const int c = threadIdx.x & 3;
-#pragma unroll 4
-                for (int py = threadIdx.x >> 2; py < L; py += WARPS * 8) {
-                    float4 v;
-                    v.x = bf[(4 * c + 0) * 2 * BUFS + py];
-                    v.y = bf[(4 * c + 1) * 2 * BUFS + py];
-                    v.z = bf[(4 * c + 2) * 2 * BUFS + py];
-                    v.w = bf[(4 * c + 3) * 2 * BUFS + py];
-                    __stcs(reinterpret_cast<float4 *>(ob + py * ra.D0) + c, v);
+#pragma unroll 2
+                for (int p2 = threadIdx.x >> 2; p2 < L / 2; p2 += WARPS * 8) {
+                    const float2 u0 = bufs[(4 * c + 0) * BUFS + p2], u1 = bufs[(4 * c + 1) * BUFS + p2];
+                    const float2 u2 = bufs[(4 * c + 2) * BUFS + p2], u3 = bufs[(4 * c + 3) * BUFS + p2];
+                    __stcs(reinterpret_cast<float4 *>(ob + (2 * p2) * ra.D0) + c, make_float4(u0.x, u1.x, u2.x, u3.x));
+                    __stcs(reinterpret_cast<float4 *>(ob + (2 * p2 + 1) * ra.D0) + c, make_float4(u0.y, u1.y, u2.y, u3.y));
                 }
                 __syncthreads();  // warp buffers free for the next tile
             }
