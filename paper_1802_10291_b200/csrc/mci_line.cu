@@ -6,7 +6,7 @@
 // zero-padded inverse of Eq. DFTexpression).  One warp owns
 // one line at a time, so there are no block barriers, only __syncwarp:
 //   * forward: one complex 512-point FFT of (g0 + i g1) (channels scaled to unit
-//     range by exact powers of two), radix 16 (all lanes) then radix 32 (16 lanes);
+//     range by exact powers of two), three radix-8 passes (two butterflies per lane);
 //   * solve: 257 classes (j_q = q - N, elements q - N and q; self-mirror
 //     classes q = 0 and N/2), Q~ from shared memory;
 //   * inverse: S = 1024 = 2K (the window [-K, K] aliases only at k' = K),
@@ -45,8 +45,7 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // Every warp's lane l reads the same values, so each lane quarter holds a copy:
 // columns 0..31: pre-twiddles e^{2 pi i p / L} for p = N - q, q (q = lane + 32 u, entry 2u + e);
 // columns 32..93: inverse pass-2 twiddles e^{2 pi i j lane / 1024}, j = 1..31.
-// columns 96..157: forward pass-2 twiddles e^{-2 pi i j lane / 512}, j = 1..31 (lanes < 16).
-constexpr int TM_COLS = 256, TMW = 0, TMI = 32, TMF = 96;
+constexpr int TM_COLS = 256, TMW = 0, TMI = 32;
 __device__ __forceinline__ uint32_t s32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void tst8(uint32_t ta, const float *v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
@@ -100,10 +99,17 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     float *stage = reinterpret_cast<float *>(bufs + WARPS * BUFS);  // TILED: [2][WARPS][SP]
     for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
     for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
-    // pass-2 twiddles re-laid as pairs for 128-bit loads (the kernel is MIO-bound):
-    // fwt[32 p + 2 i + h] = fw_{2p+1+h}(i) (p < 15), fwt[480 + i] = fw_31(i); iw likewise with 64 per pair row
-    for (int i = threadIdx.x; i < 15 * 32 + 16; i += WARPS * 32)
-        fwt[i] = i < 480 ? tb.fwt[(2 * (i >> 5) + 1 + (i & 1)) * 16 + ((i & 31) >> 1)] : tb.fwt[31 * 16 + (i - 480)];
+    // forward 8 x 8 x 8 twiddles, from the plan's e^{+2 pi i p / L} by quarter turns (exact):
+    // fwt[64 (j-1) + b] = W512^{j b} (j = 1..7, b < 64), fwt[448 + 8 (j-1) + k] = W64^{j k} (k < 8)
+    for (int i = threadIdx.x; i < 448 + 56; i += WARPS * 32) {
+        const int r = i < 448 ? ((((i >> 6) + 1) * (i & 63)) & 511) : ((8 * (((i - 448) >> 3) + 1) * ((i - 448) & 7)) & 511);
+        const int q = r >> 7;
+        const float2 w = tb.wp[4 * (r & 127)];  // e^{+2 pi i (r mod 128) / 512}
+        const float2 v = make_float2(w.x, -w.y);
+        fwt[i] = q == 0 ? v : q == 1 ? make_float2(v.y, -v.x) : q == 2 ? make_float2(-v.x, -v.y) : make_float2(-v.y, v.x);
+    }
+    // inverse pass-2 twiddles re-laid as pairs for 128-bit loads:
+    // iw[64 p + 2 i + h] = iw_{2p+1+h}(i) (p < 15), iw[960 + i] = iw_31(i)
     for (int i = threadIdx.x; i < 15 * 64 + 32; i += WARPS * 32)
         iw[i] = i < 960 ? tb.iw[(2 * (i >> 6) + 1 + (i & 1)) * 32 + ((i & 63) >> 1)] : tb.iw[31 * 32 + (i - 960)];
     __shared__ uint32_t tm_base;
@@ -142,17 +148,6 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
                     v[2 * i + 1] = w.y;
                 }
                 tst8(ta + TMI + c, v);
-            }
-#pragma unroll 1
-            for (int c = 0; c < 64; c += 8) {
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int j = 1 + c / 2 + i;
-                    const float2 w = (j <= 31 && ln < 16) ? tb.fwt[j * 16 + ln] : make_float2(0.f, 0.f);
-                    v[2 * i] = w.x;
-                    v[2 * i + 1] = w.y;
-                }
-                tst8(ta + TMF + c, v);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
@@ -310,49 +305,72 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
         const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
         const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));
-        {  // ---- forward pass 1 (radix 16, Ls = 1): butterfly i = lane, inputs n = i + 32 j
+        {  // ---- forward: 512 = 8 x 8 x 8 (Stockham DIT), butterflies b = lane and lane + 32 on
+           // every lane in every pass; pass p reads b + 64 j and writes (b / Ls) 8 Ls + b % Ls + Ls k.
+           // XOR swizzles keep the 64-bit accesses of each half-warp on 16 bank pairs:
+           // s1 (pass-1 output, region buf[512..1023]) for the stride-8 writes and stride-1 reads,
+           // s2 (pass-2 output, buf[0..511]) for the (b / 8, b % 8) writes; pass 3 writes the
+           // natural-order spectrum with sw3 for the solve.
+            auto s1 = [](int a) { return a ^ ((a >> 4) & 15); };
+            auto s2 = [](int a) { return a ^ (((a >> 6) & 1) << 3); };
+            float2 *R1 = buf + 512;
             const pk sc = mk(pow2f(-e0), pow2f(-e1));
+            pk u[8], v[8];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) x[j] = mul(x[j], sc);
-            dft<16, -1>(x);
+            for (int j = 0; j < 8; ++j) {  // n = lane + 64 j (b = lane), lane + 32 + 64 j (b = lane + 32)
+                u[j] = mul(x[2 * j], sc);
+                v[j] = mul(x[2 * j + 1], sc);
+            }
+            dft<8, -1>(u);
+            dft<8, -1>(v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) buf[sw3(16 * lane + j)] = f2(x[j]);
+            for (int k = 0; k < 8; ++k) {  // pass 1 (Ls = 1): outputs 8 b + k
+                R1[s1(8 * lane + k)] = f2(u[k]);
+                R1[s1(8 * (lane + 32) + k)] = f2(v[k]);
+            }
+            __syncwarp();
+            const int k1 = lane & 7;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // pass 2 (Ls = 8): twiddle W64^{j (b % 8)}
+                u[j] = mk(R1[s1(lane + 64 * j)]);
+                v[j] = mk(R1[s1(lane + 32 + 64 * j)]);
+            }
+#pragma unroll
+            for (int j = 1; j < 8; ++j) {
+                const pk w = mk(fwt[448 + 8 * (j - 1) + k1]);
+                u[j] = pkx::cmul(u[j], w);
+                v[j] = pkx::cmul(v[j], w);
+            }
+            dft<8, -1>(u);
+            dft<8, -1>(v);
+            const int o2 = 64 * (lane >> 3) + k1;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                buf[s2(o2 + 8 * k)] = f2(u[k]);
+                buf[s2(256 + o2 + 8 * k)] = f2(v[k]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // pass 3 (Ls = 64): twiddle W512^{j b}, outputs b + 64 k
+                u[j] = mk(buf[s2(lane + 64 * j)]);
+                v[j] = mk(buf[s2(lane + 32 + 64 * j)]);
+            }
+#pragma unroll
+            for (int j = 1; j < 8; ++j) {
+                u[j] = pkx::cmul(u[j], mk(fwt[64 * (j - 1) + lane]));
+                v[j] = pkx::cmul(v[j], mk(fwt[64 * (j - 1) + lane + 32]));
+            }
+            dft<8, -1>(u);
+            dft<8, -1>(v);
+            __syncwarp();  // pass-3 reads done: the natural-order writes overlap them
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                buf[sw3(lane + 64 * k)] = f2(u[k]);
+                buf[sw3(lane + 32 + 64 * k)] = f2(v[k]);
+            }
         }
         __syncwarp();
         pk y[32];
-        if constexpr (TM) {  // ---- pass 2 (radix 32, Ls = 16): butterfly i = lane < 16, in place;
-            // all lanes run the arithmetic (converged for tcgen05.ld), lanes >= 16 neither load nor store
-            const bool act = lane < 16;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) y[j] = act ? mk(buf[sw3(lane + 16 * j)]) : mk(0.f, 0.f);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {  // twiddles j = 8c+1 .. 8c+8 (j <= 31)
-                float2 w[8];
-                tld16(tmA + TMF + 16 * c, w);
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (8 * c + 1 + i <= 31) y[8 * c + 1 + i] = pkx::cmul(y[8 * c + 1 + i], mk(w[i]));
-            }
-            dft<32, -1>(y);
-            if (act) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) buf[sw3(lane + 16 * j)] = f2(y[j]);
-            }
-        } else if (lane < 16) {  // ---- pass 2 (radix 32, Ls = 16): butterfly i = lane < 16, in place
-#pragma unroll
-            for (int j = 0; j < 32; ++j) y[j] = mk(buf[sw3(lane + 16 * j)]);
-#pragma unroll
-            for (int p2 = 0; p2 < 15; ++p2) {
-                const float4 w2 = *reinterpret_cast<const float4 *>(fwt + 32 * p2 + 2 * lane);
-                y[2 * p2 + 1] = pkx::cmul(y[2 * p2 + 1], mk(w2.x, w2.y));
-                y[2 * p2 + 2] = pkx::cmul(y[2 * p2 + 2], mk(w2.z, w2.w));
-            }
-            y[31] = pkx::cmul(y[31], mk(fwt[480 + lane]));
-            dft<32, -1>(y);
-#pragma unroll
-            for (int j = 0; j < 32; ++j) buf[sw3(lane + 16 * j)] = f2(y[j]);
-        }
-        __syncwarp();
 
         // ---- solve: classes q = lane + 32 u (u < 8) and q = N/2 (lane 0)
         pk zq[9], zm[9];
