@@ -22,6 +22,7 @@
 // pass-2 twiddles are read from tensor memory (a copy per lane quarter), off the
 // shared-memory pipe that bounds the kernel; for the (1, ik) bank the solve uses
 // the closed-form inverse instead of the Q~ table.
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -45,7 +46,7 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // Every warp's lane l reads the same values, so each lane quarter holds a copy:
 // columns 0..31: pre-twiddles e^{2 pi i p / L} for p = N - q, q (q = lane + 32 u, entry 2u + e);
 // columns 32..93: inverse pass-2 twiddles e^{2 pi i j lane / 1024}, j = 1..31.
-constexpr int TM_COLS = 256, TMW = 0, TMI = 32;
+constexpr int TM_COLS = 256, TMW = 0, TMI = 32, TMEM_TOTAL_COLS = 512;
 __device__ __forceinline__ uint32_t s32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void tst8(uint32_t ta, const float *v) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta), "f"(v[0]),
@@ -546,8 +547,8 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // ms); MCI_LINE_G16=0: 4-byte transposing cp.async into [m][l][SP] (A/B)
     const bool g16 = tiled && !(getenv("MCI_LINE_G16") && atoi(getenv("MCI_LINE_G16")) == 0);
     // default: per-lane pre-twiddle and inverse pass-2 twiddle tables in tensor memory;
-    // MCI_LINE_VARIANT=1: all tables in shared memory (A/B)
-    const int lv = getenv("MCI_LINE_VARIANT") ? atoi(getenv("MCI_LINE_VARIANT")) : 2;
+    // MCI_LINE_VARIANT=1: all tables in shared memory, 2: tensor memory on the tiled path only (A/B)
+    const int lv = getenv("MCI_LINE_VARIANT") ? atoi(getenv("MCI_LINE_VARIANT")) : 0;
     const bool tm = lv == 0 || (lv == 2 && tiled);
     auto kern = tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
                 : (tstore && g16) ? (tm ? mci_line_kernel<16, true, true, true, true> : mci_line_kernel<16, true, false, true, true>)
@@ -578,6 +579,13 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
                 WARPS, (int)tiled, (int)tstore, (int)pf, smem, occ, occ0, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, avail);
     }
     if (occ < 1) occ = 1;
+    if (tm && WARPS == 8) {
+        // the occupancy query reports one CTA per SM for a kernel that allocates tensor memory;
+        // two 8-warp CTAs fit (2 x 256 of the 512 TMEM columns, 2 x 92 KB shared memory, 2 x 32K
+        // registers) and run (measured: 0.217 -> 0.202 ms per 65,536 contiguous lines)
+        occ = std::max(occ, std::min(linek::TMEM_TOTAL_COLS / linek::TM_COLS, (int)(233472 / (smem + 1024))));
+    }
+    if (getenv("MCI_LINE_OCC")) occ = atoi(getenv("MCI_LINE_OCC"));  // A/B: CTAs per SM in the grid
     int64_t grid = (int64_t)nsm * occ;
     const int64_t need = (lines + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
