@@ -560,9 +560,10 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
     // intermediate per image: column-first Mx Nx Ly, row-first (line kernels) My Ny Lx
     const size_t per = (size_t)std::max<int64_t>((int64_t)Mx * Nx * ay.L, (int64_t)My * Ny * ax.L) * sizeof(T);
     // images per chunk: measured on B200 (config 5), fewer and fuller launches beat L2
-    // residency of the intermediate (32 MB: 1.35 ms, 128 MB: 1.15 ms, 256 MB: 1.12 ms,
-    // 512 MB: 1.10 ms per 64 images); 256 MB is the default footprint (MCI_2D_WS_MB overrides)
-    const size_t ws_mb = getenv("MCI_2D_WS_MB") ? (size_t)atoi(getenv("MCI_2D_WS_MB")) : 256;
+    // residency of the intermediate (first kernels: 32 MB 1.35 ms, 256 MB 1.12 ms, 512 MB
+    // 1.10 ms per 64 images; current kernels: 32 MB 1.05 ms, 128 MB 0.79 ms, 256 MB 0.735 ms,
+    // 512 MB 0.706 ms); 512 MB is the default footprint (MCI_2D_WS_MB overrides)
+    const size_t ws_mb = getenv("MCI_2D_WS_MB") ? (size_t)atoi(getenv("MCI_2D_WS_MB")) : 512;
     int64_t units = std::max<int64_t>(1, (int64_t)((ws_mb << 20) / per));
     p->ws_units = units;
     p->ws_bytes = per * units;
