@@ -886,7 +886,10 @@ static mci_status exec_host(mci_plan p, int64_t units, const void *g, void *f, v
         nout = (p->flags & MCI_OUT_HILBERT) ? 2 : 1;
     }
     int64_t chunk = std::max<int64_t>(1, (int64_t)((64u << 20) / (out_u * nout)));
-    if (p->path == mci::PATH_2D) chunk = std::max<int64_t>(chunk, p->ws_units);
+    // 2D: 256 MB of output per chunk (16 config-5 images), so the copies of neighbouring
+    // chunks overlap (exec_2d splits a chunk by the workspace size itself)
+    if (p->path == mci::PATH_2D)
+        chunk = std::min<int64_t>(p->ws_units, std::max<int64_t>(1, (int64_t)((256u << 20) / (out_u * nout))));
     if (p->path == mci::PATH_FOURSTEP) chunk = std::max<int64_t>(chunk, p->ws_units);
     chunk = std::min(chunk, units);
     if (p->stage_rows < chunk) {
