@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) mci_fsf_fa(const FSArgs<float> a) {
 }
 
 // ---- FB: forward step 2 + solve + assembly + inverse step 1 for the residue pair --------------
-__global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
+__global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
     using namespace fsf;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -100,22 +100,20 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
     constexpr int IB = 1056 + 4;  // inverse buffer stride (4 FFTs of 1024, pad5); == 4 mod 16
     const int64_t xl = a.K / N1 + 2;
     // the inverse buffers (phase C) alias the forward buffers (phases A-B), which are dead after
-    // the barrier that follows the solve: 54 KB per CTA, 4 CTAs (16 warps) per SM
+    // the barrier that follows the solve; the radix-16 / radix-32 twiddles are read through L1
+    // from the plan block (not staged per CTA): 43 KB per CTA, 5 CTAs (20 warps) per SM
     float2 *fb = reinterpret_cast<float2 *>(smem);  // 4 x GB
     float2 *G = fb + 4 * GB;                         // [4][256] natural order
     float2 *ib = fb;                                 // 4 x IB (phase C)
     float2 *Xl = fb + 4 * IB;                        // [2][xl]  (4 IB >= 4 GB + 4 x 256)
-    float2 *tw16 = Xl + 2 * xl;                      // [16][16] e^{-2 pi i j b/256}
-    float2 *tw32 = tw16 + 256;                       // [32][32] e^{-2 pi i j i/1024}
-    float2 *tw128 = tw32 + 1024;                     // [3][32] e^{2 pi i e j / 128}, e = 1, 2, 3
+    const float2 *gt16 = a.fbt, *gt32 = a.fbt + 256;  // plan block: [16][16] e^{-2 pi i j b/256}, [32][32] e^{-2 pi i j i/1024}
+    float2 *tw128 = Xl + 2 * xl;                     // [3][32] e^{2 pi i e j / 128}, e = 1, 2, 3
     float2 *twE = tw128 + 96;                        // [2][32] e^{2 pi i 32 res_r j / S}
     __shared__ __align__(8) uint64_t tmb;
     const int q1 = blockIdx.x % (N1 / 2 + 1);
-    if (a.fbt) {  // tw16, tw32, tw128 are contiguous here and in the plan block
-        if (threadIdx.x == 0) tab_copy(tw16, a.fbt, (256 + 1024 + 96) * 8, &tmb);
+    if (a.fbt) {  // plan block: [tw16 256][tw32 1024][tw128 96]
+        if (threadIdx.x == 0) tab_copy(tw128, a.fbt + 256 + 1024, 96 * 8, &tmb);
     } else {
-        for (int q = threadIdx.x; q < 256; q += 128) tw16[q] = __ldg(a.twF + ((4 * (q >> 4) * (q & 15)) & 1023));
-        for (int q = threadIdx.x; q < 1024; q += 128) tw32[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
         for (int q = threadIdx.x; q < 96; q += 128) {  // e^{+2 pi i e j / 128} = conj(twF[8 e j])
             const float2 v = __ldg(a.twF + ((8 * ((q >> 5) + 1) * (q & 31)) & 1023));
             tw128[q] = make_float2(v.x, -v.y);
@@ -147,9 +145,9 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
             asm volatile("bar.sync 1, 64;" ::: "memory");
 #pragma unroll
             for (int j = 0; j < 16; ++j) x[j] = mk(buf[pad4(b + 16 * j)]);
-            if (a.fbt) tab_wait(&tmb);
 #pragma unroll
-            for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(tw16[j * 16 + b]));
+            for (int j = 1; j < 16; ++j)
+                x[j] = pkx::cmul(x[j], mk(a.fbt ? __ldg(gt16 + j * 16 + b) : __ldg(a.twF + ((4 * j * b) & 1023))));
             dft<16, -1>(x);
 #pragma unroll
             for (int j = 0; j < 16; ++j) G[fi * 256 + b + 16 * j] = f2(x[j]);
@@ -299,7 +297,8 @@ __global__ void __launch_bounds__(128) mci_fsf_fb(const FSArgs<float> a) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) x[j] = mk(buf[pad5(i + 32 * j)]);
 #pragma unroll
-            for (int j = 1; j < 32; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(tw32[j * 32 + i])));
+            for (int j = 1; j < 32; ++j)
+                x[j] = pkx::cmul(x[j], pkx::conj(mk(a.fbt ? __ldg(gt32 + j * 32 + i) : __ldg(a.twF + ((j * i) & 1023)))));
             dft<32, 1>(x);
             // twiddle e^{2 pi i res u / S}, u = i + 32 j: base(i) * E[j], E[j] = e^{2 pi i 32 res j / S}
             const pk B = mk(a.twS((int64_t)res[r] * i));
@@ -366,7 +365,7 @@ cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t
     using namespace fsf;
     const size_t fa_sm = (size_t)(8 * (1056 + 2) + 1024) * 8;
     const int64_t xl = a.K / N1 + 2;
-    const size_t fb_sm = (size_t)(4 * 1060 + 2 * xl + 256 + 1024 + 96 + 64) * 8;  // ib aliases fb + G
+    const size_t fb_sm = (size_t)(4 * 1060 + 2 * xl + 96 + 64) * 8;  // ib aliases fb + G
     const size_t ic_sm = (size_t)(16 * 1057 + 1024) * 8;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
