@@ -123,6 +123,10 @@ struct mci_plan_s {
     size_t stage_bytes[2] = {0, 0};
     int64_t stage_rows = 0;
     cudaStream_t hs[2] = {nullptr, nullptr};
+    // 2D with two workspace halves: odd chunks on a second stream (MCI_2D_STREAMS=2)
+    int ws_halves = 1;
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -566,7 +570,8 @@ mci_status create_2d(mci_plan p, int Mx, int64_t Nx, const mci_system *sx, int M
     const size_t ws_mb = getenv("MCI_2D_WS_MB") ? (size_t)atoi(getenv("MCI_2D_WS_MB")) : 512;
     int64_t units = std::max<int64_t>(1, (int64_t)((ws_mb << 20) / per));
     p->ws_units = units;
-    p->ws_bytes = per * units;
+    p->ws_halves = (getenv("MCI_2D_STREAMS") && atoi(getenv("MCI_2D_STREAMS")) == 2) ? 2 : 1;
+    p->ws_bytes = per * units * p->ws_halves;
     if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
     return MCI_OK;
 }
@@ -591,8 +596,25 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
     const size_t es = esize(p->dtype);
     const int64_t Mx = p->Mx, My = p->My, Nx = p->Nx, Ny = p->Ny, Lx = p->Lx, Ly = p->Ly;
     const int64_t in_img = My * Mx * Ny * Nx, out_img = Ly * Lx;
+    // two workspace halves: chunk c runs on stream c & 1 (the caller's stream or s2), so one
+    // chunk's row pass overlaps the next chunk's column pass; s2 joins the caller's stream
+    const bool two = p->ws_halves == 2 && n > p->ws_units;
+    cudaStream_t st0 = st;
+    if (two) {
+        if (!p->s2 && cudaStreamCreateWithFlags(&p->s2, cudaStreamNonBlocking) != cudaSuccess) return MCI_E_CUDA;
+        for (int k = 0; k < 2; ++k)
+            if (!p->ev[k] && cudaEventCreateWithFlags(&p->ev[k], cudaEventDisableTiming) != cudaSuccess)
+                return MCI_E_CUDA;
+        if (cudaEventRecord(p->ev[0], st0) != cudaSuccess || cudaStreamWaitEvent(p->s2, p->ev[0], 0) != cudaSuccess)
+            return MCI_E_CUDA;
+    }
+    const size_t half_bytes = p->ws_bytes / p->ws_halves;
+    int64_t chunk_id = 0;
     for (int64_t i0 = 0; i0 < n; i0 += p->ws_units) {
         const int64_t ni = std::min<int64_t>(p->ws_units, n - i0);
+        cudaStream_t sc = (two && (chunk_id & 1)) ? p->s2 : st0;
+        void *wsc = (char *)p->ws + (two ? (size_t)(chunk_id & 1) * half_bytes : 0);
+        ++chunk_id;
         const char *gi = (const char *)g + i0 * in_img * es;
         char *oi = (char *)out + i0 * out_img * es;
         if (p->ay.special == 2 && p->ax.special == 2) {
@@ -610,11 +632,11 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
             // opt-in (MCI_2D_ORDER=1): measured slower than column-first on config 5 (0.99 vs
             // 0.81 ms per 64 images): the untiled transposed-store passes issue at ~31 %
             const bool order_rows = getenv("MCI_2D_ORDER") && atoi(getenv("MCI_2D_ORDER")) == 1 &&
-                                    mci::line_tstore_ok(p->ax, ra1, ni * My * Ny, gi, p->ws) &&
-                                    mci::line_tstore_ok(p->ay, ra2, ni * Lx, p->ws, oi);
+                                    mci::line_tstore_ok(p->ax, ra1, ni * My * Ny, gi, wsc) &&
+                                    mci::line_tstore_ok(p->ay, ra2, ni * Lx, wsc, oi);
             if (order_rows) {
-                if (mci::launch_line(p->ax, ra1, ni * My * Ny, gi, p->ws, st, nl, true) != cudaSuccess ||
-                    mci::launch_line(p->ay, ra2, ni * Lx, p->ws, oi, st, nl, true) != cudaSuccess)
+                if (mci::launch_line(p->ax, ra1, ni * My * Ny, gi, wsc, sc, nl, true) != cudaSuccess ||
+                    mci::launch_line(p->ay, ra2, ni * Lx, wsc, oi, sc, nl, true) != cudaSuccess)
                     return MCI_E_CUDA;
                 continue;
             }
@@ -626,9 +648,9 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
         // line kernels on both axes: the column pass stores ws transposed, ws[img][mx][py][nx],
         // so the row pass reads contiguous lines (measured: 0.33 -> 0.25 ms per 65,536 lines)
         const bool tws = p->ay.special == 2 && p->ax.special == 2 &&
-                         mci::line_tstore_ok(p->ay, rc, ni * Mx * Nx, gi, p->ws);
-        cudaError_t e = tws ? mci::launch_line(p->ay, rc, ni * Mx * Nx, gi, p->ws, st, nl, true)
-                            : mci::launch_axis(p->ay, rc, ni * Mx * Nx, gi, p->ws, nullptr, st, nl);
+                         mci::line_tstore_ok(p->ay, rc, ni * Mx * Nx, gi, wsc);
+        cudaError_t e = tws ? mci::launch_line(p->ay, rc, ni * Mx * Nx, gi, wsc, sc, nl, true)
+                            : mci::launch_axis(p->ay, rc, ni * Mx * Nx, gi, wsc, nullptr, sc, nl);
         if (e != cudaSuccess) return MCI_E_CUDA;
         // row pass (along x, channels mx) on ws -> out[img][py][Lx]
         mci::RowAddr rr;
@@ -639,9 +661,11 @@ mci_status exec_2d(mci_plan p, int64_t n, const void *g, void *out, cudaStream_t
             rr.D0 = Ly; rr.D1 = 1; rr.s0 = 1; rr.s1 = 0; rr.s2 = Mx * Nx * Ly;
             rr.cs = Nx * Ly; rr.ss = Ly;
         }
-        e = mci::launch_axis(p->ax, rr, ni * Ly, p->ws, oi, nullptr, st, nl);
+        e = mci::launch_axis(p->ax, rr, ni * Ly, wsc, oi, nullptr, sc, nl);
         if (e != cudaSuccess) return MCI_E_CUDA;
     }
+    if (two && (cudaEventRecord(p->ev[1], p->s2) != cudaSuccess || cudaStreamWaitEvent(st0, p->ev[1], 0) != cudaSuccess))
+        return MCI_E_CUDA;
     return MCI_OK;
 }
 
@@ -811,6 +835,9 @@ void mci_plan_destroy(mci_plan p) {
     if (!p) return;
     for (int i = 0; i < 2; ++i)
         if (p->hs[i]) cudaStreamDestroy(p->hs[i]);
+    if (p->s2) cudaStreamDestroy(p->s2);
+    for (int i = 0; i < 2; ++i)
+        if (p->ev[i]) cudaEventDestroy(p->ev[i]);
     for (int i = 0; i < 4; ++i)
         if (p->stage[i]) cudaFree(p->stage[i]);
     if (p->ws) cudaFree(p->ws);

@@ -352,8 +352,8 @@ def test_cfg5_full_size_sampled(qtab, variant, monkeypatch):
         assert 10 * np.log10(255 ** 2 / mse) > 15.0
 
 
-@pytest.mark.parametrize("ws_mb", ["256", "24"])
-def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
+@pytest.mark.parametrize("ws_mb,streams", [("512", "1"), ("24", "1"), ("24", "2")])
+def test_cfg5_transposed_workspace(ws_mb, streams, monkeypatch):
     """Line kernels on both axes.  Default: column pass first, storing the workspace
     transposed (ws[img][mx][py][nx]) so the row pass reads contiguous lines.
     MCI_2D_TSTORE=0: column first with a strided workspace; MCI_LINE_G16=0: the tiled
@@ -361,9 +361,11 @@ def test_cfg5_transposed_workspace(ws_mb, monkeypatch):
     (same per-line arithmetic: bit-identical).  MCI_2D_ORDER=1: row pass first on contiguous input lines, storing
     ws[img][my][px][ny], then the column pass on contiguous lines storing the image
     transposed: the other pass order (order-independent), equal to fp32
-    rounding.  24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk)."""
+    rounding.  24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk);
+    MCI_2D_STREAMS=2 alternates the chunks over two streams and two workspace halves."""
     m = mci()
     monkeypatch.setenv("MCI_2D_WS_MB", ws_mb)
+    monkeypatch.setenv("MCI_2D_STREAMS", streams)
     g = np.random.default_rng(55).standard_normal((5, 2, 2, 512, 512)).astype(np.float32)
     g[:, 0, 1] *= 64.0
     g[:, 1, 0] *= 64.0
