@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
     float2 *itw = wlo + 256;                        // 32 x 65
     float2 *F = bufs;                               // forward spectrum, pad4 layout (4352 slots)
     float *stage = reinterpret_cast<float *>(itw + 32 * ITW_LD);  // [2][4096] input row
+    // w16[t] = wlo[16 t] = e^{2 pi i 16 t / L}: the forward pass-3 twiddle's low factor, whose
+    // wlo index is a multiple of 16 (one bank pair: 16-way conflicts) -- here 16 consecutive slots
+    float2 *w16 = reinterpret_cast<float2 *>(stage + M * N);
     __shared__ __align__(8) uint64_t mbar;
     __shared__ float smx[8][2];
     __shared__ float ssc[2];
@@ -125,6 +128,7 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
     for (int i = threadIdx.x; i < 256; i += NT) {
         whi[i] = tb.whi[i];
         wlo[i] = tb.wlo[i];
+        if (i < 16) w16[i] = tb.wlo[16 * i];
     }
     for (int i = threadIdx.x; i < 32 * ITW_LD; i += NT) itw[i] = tb.itw[i];
     if (threadIdx.x == 0) {
@@ -240,7 +244,10 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) x[j] = mk(F[pad4(b + 256 * j)]);
 #pragma unroll
-            for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], pkx::conj(wL((16 * j * b) & (L - 1))));
+            for (int j = 1; j < 16; ++j) {  // e^{2 pi i j b / 4096} = whi[(j b) >> 4] w16[(j b) & 15]
+                const int jb = j * b;
+                x[j] = pkx::cmul(x[j], pkx::conj(pkx::cmul(mk(whi[(jb >> 4) & 255]), mk(w16[jb & 15]))));
+            }
             dft<16, -1>(x);
 #pragma unroll
             for (int j = 0; j < 16; ++j) F[pad4(b + 256 * j)] = f2(x[j]);
@@ -379,7 +386,7 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     tb.wlo = base + 256;
     tb.itw = base + 512;
     tb.deriv = ax.bank_deriv01;
-    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4;
+    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4 + 16 * 8;
     // MCI_HILBERT_VARIANT=1: the 8-warp layout storing directly (A/B); default: store warpgroup
     const int variant = getenv("MCI_HILBERT_VARIANT") ? atoi(getenv("MCI_HILBERT_VARIANT")) : 0;
     const bool stw = variant != 1;
