@@ -72,7 +72,7 @@ __device__ __forceinline__ void tld16(uint32_t ta, float2 *w) {
 struct LineTables {
     const float2 *Qt;   // [NQ][2][2] H^{-1}/N per class
     const float2 *wp;   // [K+1] e^{+2 pi i p / L}
-    const float2 *fwt;  // [32][16] e^{-2 pi i j k / 512}
+    const float2 *fwt;  // [32][16] e^{-2 pi i j k / 512} (plan layout; the 8 x 8 x 8 forward derives its twiddles from wp)
     const float2 *iw;   // [32][32] e^{+2 pi i j k / 1024}
     int deriv;          // 1: bank is (1, ik) -> closed-form inverse, no Q~ reads
 };
