@@ -515,7 +515,8 @@ size_t line_table_elems(const Axis1D &ax) { return (ax.K + 1) + 512 + 1024; }
 bool line_tstore_ok(const Axis1D &ax, const RowAddr &ra, int64_t lines, const void *g, const void *f) {
     if (getenv("MCI_2D_TSTORE") && atoi(getenv("MCI_2D_TSTORE")) == 0) return false;
     const bool tiled_in = ra.s0 == 1 && ra.ss != 1 && ra.ss % 4 == 0;  // adjacent lines, strided samples
-    const bool contig_in = ra.ss == 1 && ra.s0 % 4 == 0;               // contiguous lines (prefetched)
+    const bool contig_in = ra.ss == 1 && ra.s0 % 4 == 0 &&              // contiguous lines (prefetched)
+                           !(getenv("MCI_LINE_PF") && atoi(getenv("MCI_LINE_PF")) == 0);
     return line_supported(ax) && (tiled_in || contig_in) && ra.D0 % 16 == 0 && lines % 16 == 0 &&
            (((uintptr_t)g) & 15) == 0 && (((uintptr_t)f) & 15) == 0 && ra.cs % 4 == 0 && ra.s1 % 4 == 0 &&
            ra.s2 % 4 == 0;
