@@ -107,6 +107,11 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
     // w16[t] = wlo[16 t] = e^{2 pi i 16 t / L}: the forward pass-3 twiddle's low factor, whose
     // wlo index is a multiple of 16 (one bank pair: 16-way conflicts) -- here 16 consecutive slots
     float2 *w16 = reinterpret_cast<float2 *>(stage + M * N);
+    // likewise contiguous copies of two strided whi reads: u32[p1] = whi[8 p1] (pass-1 fold
+    // factor; 8 phases per warp at stride 8: 4-way) and t16[16 j + k] = whi[(j k) mod 256]
+    // (forward pass-2 twiddles; stride j across lanes: up to 8-way)
+    float2 *u32 = w16 + 16;
+    float2 *t16 = u32 + 32;
     __shared__ __align__(8) uint64_t mbar;
     __shared__ float smx[8][2];
     __shared__ float ssc[2];
@@ -129,6 +134,8 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
         whi[i] = tb.whi[i];
         wlo[i] = tb.wlo[i];
         if (i < 16) w16[i] = tb.wlo[16 * i];
+        if (i < 32) u32[i] = tb.whi[8 * i];
+        t16[i] = tb.whi[((i >> 4) * (i & 15)) & 255];
     }
     for (int i = threadIdx.x; i < 32 * ITW_LD; i += NT) itw[i] = tb.itw[i];
     if (threadIdx.x == 0) {
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) x[j] = mk(F[pad4(b + 256 * j)]);
 #pragma unroll
-                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(whi[(j * k) & 255])));
+                for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], pkx::conj(mk(t16[16 * j + k])));
                 dft<16, -1>(x);
                 bar();
 #pragma unroll
@@ -297,7 +304,7 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
             pk x[64];
             {  // pass 1 (Ls = 1): k' = bt + 32 j; Zin(k') = w^{k' p1} (Z(k') + u Z(k' + S)),
                // w^{k' p1} = w^{bt p1} e^{2 pi i j p1 / 2048} (itw row p1)
-                const pk u = mk(whi[8 * p1]);  // e^{2 pi i 2048 p1 / L}
+                const pk u = mk(u32[p1]);  // e^{2 pi i 2048 p1 / L}
                 const pk wb = wL(bt * p1);
 #pragma unroll
                 for (int j = 0; j < 64; ++j) {
@@ -386,7 +393,7 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     tb.wlo = base + 256;
     tb.itw = base + 512;
     tb.deriv = ax.bank_deriv01;
-    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4 + 16 * 8;
+    const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4 + (16 + 32 + 256) * 8;
     // MCI_HILBERT_VARIANT=1: the 8-warp layout storing directly (A/B); default: store warpgroup
     const int variant = getenv("MCI_HILBERT_VARIANT") ? atoi(getenv("MCI_HILBERT_VARIANT")) : 0;
     const bool stw = variant != 1;
