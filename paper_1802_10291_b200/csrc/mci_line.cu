@@ -88,18 +88,25 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     using namespace linek;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
+    // CT (tiled, tensor-memory tables, 8 warps): compact shared memory -- no copies of Q~
+    // (read through L1), of the pre-twiddles or of the inverse twiddles (both in TMEM) -- so
+    // two CTAs fit per SM and one's tile write-out overlaps the other's transforms
+    constexpr bool CT = TILED && TM && WARPS == 8;
     float2 *Qs = reinterpret_cast<float2 *>(smem);  // NQ*4
     float2 *wps = Qs + NQ * 4;                      // K+1 (+1 pad)
-    float2 *fwt = wps + K + 2;                      // 512
+    float2 *fwt = CT ? Qs : wps + K + 2;            // 512
     float2 *iw = fwt + 512;                         // 1024
     // (measured: running the untiled TST CTA as two independent 8-warp halves with 8-line
     // tiles and named barriers was slower, 0.33 -> 0.39 ms per 65,536 lines)
     constexpr int TW = WARPS;  // lines per tile
-    constexpr int BUFS = BUF;
-    float2 *bufs = iw + 1024;                       // WARPS x BUFS
+    // CT: buffer stride = 2 (mod 16) float2 for the 8-line write-out mapping
+    constexpr int BUFS = CT ? BUF + 1 : BUF;
+    float2 *bufs = CT ? fwt + 512 : iw + 1024;      // WARPS x BUFS
     float *stage = reinterpret_cast<float *>(bufs + WARPS * BUFS);  // TILED: [2][WARPS][SP]
-    for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
-    for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
+    if (!CT) {
+        for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
+        for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
+    }
     // forward 8 x 8 x 8 twiddles, from the plan's e^{+2 pi i p / L} by quarter turns (exact):
     // fwt[64 (j-1) + b] = W512^{j b} (j = 1..7, b < 64), fwt[448 + 8 (j-1) + k] = W64^{j k} (k < 8)
     for (int i = threadIdx.x; i < 448 + 56; i += WARPS * 32) {
@@ -111,7 +118,7 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     }
     // inverse pass-2 twiddles re-laid as pairs for 128-bit loads:
     // iw[64 p + 2 i + h] = iw_{2p+1+h}(i) (p < 15), iw[960 + i] = iw_31(i)
-    for (int i = threadIdx.x; i < 15 * 64 + 32; i += WARPS * 32)
+    for (int i = threadIdx.x; !CT && i < 15 * 64 + 32; i += WARPS * 32)
         iw[i] = i < 960 ? tb.iw[(2 * (i >> 6) + 1 + (i & 1)) * 32 + ((i & 63) >> 1)] : tb.iw[31 * 32 + (i - 960)];
     __shared__ uint32_t tm_base;
     if (TM) {
@@ -156,8 +163,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     }
     __syncthreads();
     if (TM) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    auto ldQ = [&](int i) { return Qs[i]; };
-    auto ldwp = [&](int i) { return wps[i]; };
+    auto ldQ = [&](int i) { return CT ? __ldg(tb.Qt + i) : Qs[i]; };
+    auto ldwp = [&](int i) { return CT ? __ldg(tb.wp + i) : wps[i]; };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float2 *buf = bufs + warp * BUFS;
     const uint32_t tmA = TM ? tm_base + ((uint32_t)(32 * (warp & 3)) << 16) : 0u;
@@ -178,13 +185,17 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     // rows of 64 B whose 16-byte chunks are XOR-swizzled by (n >> 1) & 3 (8 copies per
     // thread instead of 32); a warp's column reads are then 4-way bank conflicted
     constexpr bool G16 = TILED && PF;
-    auto g16_idx = [](int m, int n, int l) { return ((m * N + n) << 4) + ((((l >> 2) ^ (n >> 1)) & 3) << 2) + (l & 3); };
+    constexpr int CPR = TW / 4;  // 16-byte chunks per stage row (TW lines)
+    auto g16_idx = [](int m, int n, int l) {
+        return (m * N + n) * TW + ((((l >> 2) ^ (TW == 16 ? (n >> 1) : 0)) & (CPR - 1)) << 2) + (l & 3);
+    };
     auto fetch_tile = [&](int64_t t, int64_t tb0) {
         if (G16) {
             if (t < ntiles) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const int q = threadIdx.x + WARPS * 32 * i, c = q & 3, n = (q >> 2) & (N - 1), m = q >> 11;
+                    const int q = threadIdx.x + WARPS * 32 * i, c = q & (CPR - 1), n = (q / CPR) & (N - 1),
+                              m = q / (CPR * N);
                     const uint32_t dst = (uint32_t)__cvta_generic_to_shared(stage + g16_idx(m, n, 4 * c));
                     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst),
                                  "l"(g + tb0 + m * ra.cs + (int64_t)n * ra.ss + 4 * c)
@@ -479,11 +490,13 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
             float *ob = f + (l0 / ra.D0) * (int64_t)L * ra.D0 + (l0 % ra.D0);
             {
                 __syncthreads();  // the tile's 16 lines are in the warp buffers
-                // thread (c, p2): lines 4c..4c+3 of rows 2 p2, 2 p2 + 1 (one 64-bit read per line;
-                // buffer stride = 1 (mod 16) float2, so a half-warp's reads hit 16 bank pairs)
-                const int c = threadIdx.x & 3;
+                // thread (c, p2): lines 4c..4c+3 of rows 2 p2, 2 p2 + 1 (one 64-bit read per line).
+                // 16 lines: c = tid & 3, buffer stride = 1 (mod 16) float2; 8 lines: c = bit 3 of
+                // tid, stride = 2 (mod 16): either way a half-warp's reads hit 16 bank pairs
+                const int c = TW == 16 ? (threadIdx.x & 3) : ((threadIdx.x >> 3) & 1);
+                const int p20 = TW == 16 ? (threadIdx.x >> 2) : ((threadIdx.x & 7) + 8 * (threadIdx.x >> 4));
 #pragma unroll 2
-                for (int p2 = threadIdx.x >> 2; p2 < L / 2; p2 += WARPS * 8) {
+                for (int p2 = p20; p2 < L / 2; p2 += WARPS * 32 / CPR) {
                     const float2 u0 = bufs[(4 * c + 0) * BUFS + p2], u1 = bufs[(4 * c + 1) * BUFS + p2];
                     const float2 u2 = bufs[(4 * c + 2) * BUFS + p2], u3 = bufs[(4 * c + 3) * BUFS + p2];
                     __stcs(reinterpret_cast<float4 *>(ob + (2 * p2) * ra.D0) + c, make_float4(u0.x, u1.x, u2.x, u3.x));
@@ -543,7 +556,6 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // tiled or transposed-store: one 16-warp CTA per SM (a tile = 16 lines); else two 8-warp CTAs
     const bool tstore_c = tstore && !tiled;  // untiled transposed store (prefetched contiguous lines)
     if (tstore_c && !pf) return cudaErrorInvalidValue;
-    const int WARPS = (tiled || tstore) ? 16 : 8;
     // tiled passes: 16-byte gather into a swizzled [m][n][16] stage (config 5: 0.808 -> 0.775
     // ms); MCI_LINE_G16=0: 4-byte transposing cp.async into [m][l][SP] (A/B)
     const bool g16 = tiled && !(getenv("MCI_LINE_G16") && atoi(getenv("MCI_LINE_G16")) == 0);
@@ -551,15 +563,21 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // MCI_LINE_VARIANT=1: all tables in shared memory, 2: tensor memory on the tiled path only (A/B)
     const int lv = getenv("MCI_LINE_VARIANT") ? atoi(getenv("MCI_LINE_VARIANT")) : 0;
     const bool tm = lv == 0 || (lv == 2 && tiled);
-    auto kern = tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
+    // MCI_LINE_CT8=1 (A/B): tiled transposed-store pass as two 8-warp CTAs per SM (8-line tiles,
+    // compact shared memory), so one CTA's write-out overlaps the other's transforms
+    const bool ct8 = tstore && tiled && g16 && tm && getenv("MCI_LINE_CT8") && atoi(getenv("MCI_LINE_CT8")) == 1;
+    const int WARPS = ct8 ? 8 : (tiled || tstore) ? 16 : 8;
+    auto kern = ct8 ? mci_line_kernel<8, true, true, true, true>
+                : tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
                 : (tstore && g16) ? (tm ? mci_line_kernel<16, true, true, true, true> : mci_line_kernel<16, true, false, true, true>)
                 : tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
                 : (tiled && g16) ? (tm ? mci_line_kernel<16, true, true, false, true> : mci_line_kernel<16, true, false, false, true>)
                 : tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
                 : pf    ? (tm ? mci_line_kernel<8, false, true, false, true> : mci_line_kernel<8, false, false, false, true>)
                         : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
-    const size_t smem = (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
-                        (tiled ? (size_t)2 * WARPS * linek::SP * 4 : tstore_c ? (size_t)WARPS * 2 * linek::N * 4 : 0);
+    const size_t smem = ct8 ? (size_t)(512 + WARPS * (linek::BUF + 1)) * 8 + (size_t)2 * WARPS * linek::SP * 4
+                            : (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
+                                  (tiled ? (size_t)2 * WARPS * linek::SP * 4 : tstore_c ? (size_t)WARPS * 2 * linek::N * 4 : 0);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
@@ -580,7 +598,7 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
                 WARPS, (int)tiled, (int)tstore, (int)pf, smem, occ, occ0, fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, avail);
     }
     if (occ < 1) occ = 1;
-    if (tm && WARPS == 8) {
+    if (tm && WARPS == 8) {  // (also the CT8 tiled pass)
         // the occupancy query reports one CTA per SM for a kernel that allocates tensor memory;
         // two 8-warp CTAs fit (2 x 256 of the 512 TMEM columns, 2 x 92 KB shared memory, 2 x 32K
         // registers) and run (measured: 0.217 -> 0.202 ms per 65,536 contiguous lines)
