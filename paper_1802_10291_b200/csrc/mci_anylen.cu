@@ -685,24 +685,21 @@ cudaError_t launch_anylen_residual(const Axis1D &ax, const RowAddr &ra, int64_t 
 }
 
 // eps(f, N) of a batch of spectra: one warp per signal, sums in fp64 (Eq. averageerror)
-template <typename T>
-__global__ void mci_avg_error_kernel(const cv<T> *__restrict__ spec, int64_t k_lo, int nf, int64_t batch, int M,
-                                     int N, int64_t K1, const cv<T> *__restrict__ Q, double omega_sum, AnyErrSys sy,
-                                     T *__restrict__ out) {
+// Per-coefficient weights of eps(f, N) (Theorem error, Eq. errorestimate): for band-external
+// n, wt[i] = (1 + sum_l |sum_m r_m(j + lN) b_m(n)|^2, sum_m |b_m(n)|^2); in-band n: (-1, 0).
+// They depend on n only, so they are computed once per call instead of once per spectrum.
+__global__ void mci_avg_error_weights(int64_t k_lo, int nf, int M, int N, int64_t K1, const void *Qv, bool q64,
+                                      AnyErrSys sy, double2 *__restrict__ wt) {
     using namespace anyk;
-    const int lane = threadIdx.x & 31;
-    const int64_t sig = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    if (sig >= batch) return;
-    const cv<T> *a = spec + sig * (int64_t)nf;
-    double e2 = 0, oob = 0, cs = 0;
-    for (int i = lane; i < nf; i += 32) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
         const int64_t n = k_lo + i;
         const int64_t d = n - K1;
         const int64_t kb = (d >= 0 ? d / N : -((-d + N - 1) / N)) + 1;  // block index of n
-        if (kb >= 1 && kb <= M) continue;
-        const cv<T> an = a[i];
-        const double a2 = (double)an.x * an.x + (double)an.y * an.y;
-        const int64_t j = n - (kb - 1) * N;        // the class element of I_1
+        if (kb >= 1 && kb <= M) {
+            wt[i] = make_double2(-1.0, 0.0);
+            continue;
+        }
+        const int64_t j = n - (kb - 1) * N;  // the class element of I_1
         const int q = (int)(((j % N) + N) % N);
         double2 b[8];
         double bsum = 0;
@@ -714,16 +711,41 @@ __global__ void mci_avg_error_kernel(const cv<T> *__restrict__ spec, int64_t k_l
         for (int l = 0; l < M; ++l) {  // S_l = sum_m r_m(j + lN) b_m(n), r_m(j + lN) = N Q~_q[m][l]
             double sr = 0, si = 0;
             for (int m = 0; m < M; ++m) {
-                const cv<T> r = Q[((int64_t)q * M + m) * M + l];
-                const double rr = (double)r.x * N, ri = (double)r.y * N;
+                const int64_t e = ((int64_t)q * M + m) * M + l;
+                double rr, ri;
+                if (q64) {
+                    const double2 r = static_cast<const double2 *>(Qv)[e];
+                    rr = r.x * N, ri = r.y * N;
+                } else {
+                    const float2 r = static_cast<const float2 *>(Qv)[e];
+                    rr = (double)r.x * N, ri = (double)r.y * N;
+                }
                 sr += rr * b[m].x - ri * b[m].y;
                 si += rr * b[m].y + ri * b[m].x;
             }
             w += sr * sr + si * si;
         }
-        e2 += a2 * (1.0 + w);
+        wt[i] = make_double2(1.0 + w, bsum);
+    }
+}
+
+// One warp per spectrum: fp64 sums of |a(n)|^2 times the precomputed weights.
+template <typename T>
+__global__ void mci_avg_error_kernel(const cv<T> *__restrict__ spec, int nf, int64_t batch, int M, double omega_sum,
+                                     const double2 *__restrict__ wt, T *__restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t sig = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (sig >= batch) return;
+    const cv<T> *a = spec + sig * (int64_t)nf;
+    double e2 = 0, oob = 0, cs = 0;
+    for (int i = lane; i < nf; i += 32) {
+        const double2 w = __ldg(wt + i);
+        if (w.x < 0.0) continue;  // in-band coefficient
+        const cv<T> an = a[i];
+        const double a2 = (double)an.x * an.x + (double)an.y * an.y;
+        e2 += a2 * w.x;
         oob += a2;
-        cs += a2 * bsum;
+        cs += a2 * w.y;
     }
     for (int o = 16; o; o >>= 1) {
         e2 += __shfl_xor_sync(0xffffffffu, e2, o);
@@ -742,16 +764,24 @@ cudaError_t launch_averaged_error(const Axis1D &ax, int64_t batch, const void *s
     if (batch <= 0) return cudaSuccess;
     AnyErrSys sy;
     for (int m = 0; m < 8; ++m) sy.s[m] = ax.sys[m];
+    // weight table: stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on the caller's
+    // stream: no device synchronisation, and concurrent calls on other streams stay independent)
+    double2 *wt = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&wt, (size_t)std::max<int64_t>(n_freq, 1) * sizeof(double2), st);
+    if (e != cudaSuccess) return e;
+    const unsigned wgrid = (unsigned)std::min<int64_t>((n_freq + 255) / 256 + 1, 4096);
+    mci_avg_error_weights<<<wgrid, 256, 0, st>>>(k_lo, (int)n_freq, ax.M, (int)ax.N, ax.K1, ax.Qt,
+                                                 ax.dtype == MCI_F64, sy, wt);
     const unsigned grid = (unsigned)((batch + 7) / 8);
     if (ax.dtype == MCI_F64)
-        mci_avg_error_kernel<double><<<grid, 256, 0, st>>>((const cv<double> *)spec, k_lo, (int)n_freq, batch, ax.M,
-                                                           (int)ax.N, ax.K1, (const cv<double> *)ax.Qt, ax.omega_sum,
-                                                           sy, (double *)out);
+        mci_avg_error_kernel<double><<<grid, 256, 0, st>>>((const cv<double> *)spec, (int)n_freq, batch, ax.M,
+                                                           ax.omega_sum, wt, (double *)out);
     else
-        mci_avg_error_kernel<float><<<grid, 256, 0, st>>>((const cv<float> *)spec, k_lo, (int)n_freq, batch, ax.M,
-                                                          (int)ax.N, ax.K1, (const cv<float> *)ax.Qt, ax.omega_sum, sy,
-                                                          (float *)out);
-    return cudaGetLastError();
+        mci_avg_error_kernel<float><<<grid, 256, 0, st>>>((const cv<float> *)spec, (int)n_freq, batch, ax.M,
+                                                          ax.omega_sum, wt, (float *)out);
+    e = cudaGetLastError();
+    cudaFreeAsync(wt, st);
+    return e;
 }
 
 cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,

@@ -19,7 +19,7 @@ for c in $CONFIGS_BENCH; do
   echo "launches cfg$c rc=$?"
 done
 declare -A KREGEX=([2]="mci_row" [3]="mci_hilbert" [4]="mci_fsf_fb" [5]="mci_line" [6]="mci_anylen"
-                   [7]="mci_anylen" [8]="mci_anylen" [9]="mci_avg_error")
+                   [7]="mci_anylen" [8]="mci_anylen" [9]="mci_avg_error_kernel")
 declare -A SKIP=([2]=4 [3]=4 [4]=2 [5]=9 [6]=4 [7]=4 [8]=8 [9]=4)
 for c in $CONFIGS_FULL; do
   timeout 900 ncu --set full --clock-control none --cache-control none --import-source on \
