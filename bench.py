@@ -204,191 +204,228 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def oracle_sample(cfg, budget_s=12.0, max_steps=None):
-    """Time the fp64 oracle on a bounded sample of the workload on the host cores.
-    Returns (samples_per_s, description, threads, per-step seconds list)."""
-    import oracle
-    c = synth.CONFIGS[cfg]
-    threads = os.cpu_count() or 1
-    if cfg == 4:
-        M, N, L = c["M"], c["N"], c["L"]
-        g, _ = synth.cfg4_signals([0])
-        pts = np.random.default_rng(0).integers(0, L, 64)
-        t0 = time.perf_counter()
-        n = 0
-        while True:
-            oracle.delay_eval_points(M, N, L, g[0], pts, threads=threads)
-            n += len(pts)
-            if time.perf_counter() - t0 > budget_s / 2:
-                break
-        dt = time.perf_counter() - t0
-        return n / dt, f"signal 0, {n} output points (closed-form delay kernel), M*N={M*N} terms each", threads
-    if cfg == 9:
-        P9 = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
-        s9 = make_inputs(9, 0)[:8]
-        t0 = time.perf_counter()
-        n = 0
-        while n < len(s9):
-            oracle.averaged_error(P9, s9[n].astype(np.complex128), -(c["M"] * c["N"]) * 2)
-            n += 1
-            if time.perf_counter() - t0 > budget_s:
-                break
-        dt = time.perf_counter() - t0
-        return n * c["nfreq"] / dt, f"{n} spectra x {c['nfreq']} coefficients (direct loops)", threads
-    if cfg == 8:
-        lr, _ = synth.sisr_images([0])
-        t0 = time.perf_counter()
-        n = 0
-        while True:
-            oracle.sisr(lr[0].astype(np.float64), c["scale"])
-            n += 1
-            if time.perf_counter() - t0 > budget_s / 2:
-                break
-        dt = time.perf_counter() - t0
-        return n * (c["scale"] ** 2) * c["H"] * c["W"] / dt, f"{n} image(s) {c['H']}x{c['W']} -> x{c['scale']}", threads
-    if cfg == 7:
-        P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
-        g = make_inputs(7, 0)[:64].astype(np.float64)
-        t = synth.offgrid_points(c["npts"]).astype(np.float32).astype(np.float64)
-        rows = 0
-        t0 = time.perf_counter()
-        while rows < len(g):
-            P.eval_offgrid(g[rows], t)
-            rows += 1
-            if time.perf_counter() - t0 > budget_s:
-                break
-        dt = time.perf_counter() - t0
-        return rows * c["npts"] / dt, f"{rows} rows x {c['npts']} off-grid points (direct band sums)", threads
-    if cfg == 5:
-        px = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=threads)
-        px.kernel_table()
-        g, _ = synth.cfg5_images([0])
-        cols = np.arange(0, 2048, 2048 // 16)
-        t0 = time.perf_counter()
-        oracle.eval_2d_columns(g[0], px, px, cols)
-        dt = time.perf_counter() - t0
-        return len(cols) * 2048 / dt, f"image 0, {len(cols)} full output columns (2048 px each)", threads
-    M, N, L = c["M"], c["N"], c["L"]
-    P = oracle.OraclePlan(M, N, L, c["bank"], threads=threads)
-    P.kernel_table()
-    if c.get("hilbert"):
-        P.kernel_table(True)
-    rows = 0
-    t0 = time.perf_counter()
-    while True:
-        g = make_row(cfg, rows)
-        P.eval(g)
-        if c.get("hilbert"):
-            P.eval(g, hilbert=True)
-        rows += 1
-        if time.perf_counter() - t0 > budget_s or (max_steps and rows >= max_steps):
-            break
-    dt = time.perf_counter() - t0
-    nout = 2 if c.get("hilbert") else 1
-    return rows * L * nout / dt, f"{rows} rows of the workload (kernel table built before timing)", threads
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
-def make_row(cfg, r):
-    if cfg == 1:
-        return synth.cfg1()["g"]
-    if cfg == 2:
-        return synth.cfg2_rows([r])
-    if cfg == 6:
-        c = synth.CONFIGS[6]
-        return synth.cfg2_batch_fast(256, seed=6, M=c["M"], N=c["N"], bank=c["bank"])[r % 256][None]
-    return synth.cfg3_rows([r])
+class OracleLeg:
+    """The fp64 oracle on units of the benchmarked workload itself (rows / points / columns /
+    images / spectra of the same seeded inputs): its plan is built once (reported separately),
+    then each sampled unit is evaluated, timed, and kept so that the GPU's outputs for the same
+    units can be compared afterwards (the bench line's parity and cpu_baseline come from one
+    run of the oracle)."""
+
+    def __init__(self, cfg, g_host, tpts=None, rank=0, threads=None):
+        import oracle
+        self.oracle = oracle
+        self.cfg, self.g, self.tpts = cfg, g_host, tpts
+        self.c = c = synth.CONFIGS[cfg]
+        self.threads = threads or (os.cpu_count() or 1)
+        self.rank = rank
+        t0 = time.perf_counter()
+        if cfg in (1, 2, 3, 6, 7):
+            self.P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=self.threads)
+            if cfg != 7:
+                self.P.kernel_table()
+                if c.get("hilbert"):
+                    self.P.kernel_table(True)
+        elif cfg == 5:
+            self.P = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=self.threads)
+            self.P.kernel_table()
+        elif cfg == 9:
+            self.P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=self.threads)
+        self.plan_s = time.perf_counter() - t0
+        # unit order: spread over the batch (the first and last units included)
+        self.order = {2: _spread(c.get("batch", 1), 4096), 3: _spread(c.get("batch", 1), 512),
+                      6: _spread(c.get("batch", 1), 4096), 7: _spread(c.get("batch", 1), 512),
+                      8: _spread(c.get("batch", 1), 64), 9: _spread(c.get("batch", 1), 512)}.get(cfg)
+        if cfg == 4:
+            self.pts = np.random.default_rng(0).choice(c["L"], 1 << 16, replace=False)
+        if cfg == 5:
+            self.cols = np.random.default_rng(0).permutation(c["size"])
+        self.results = []  # (unit key, oracle output)
+
+    def set_threads(self, n):
+        self.threads = n
+        if hasattr(self, "P"):
+            self.P.threads = n
+
+    def unit(self, i):
+        """Evaluate sampled unit i; returns (key, oracle values, output samples)."""
+        o, c, cfg = self.oracle, self.c, self.cfg
+        if cfg == 1:
+            return 0, self.P.eval(self.g), c["L"]
+        if cfg in (2, 6):
+            r = int(self.order[i % len(self.order)])
+            return r, self.P.eval(self.g[r:r + 1])[0], c["L"]
+        if cfg == 3:
+            r = int(self.order[i % len(self.order)])
+            return r, (self.P.eval(self.g[r:r + 1])[0], self.P.eval(self.g[r:r + 1], hilbert=True)[0]), 2 * c["L"]
+        if cfg == 4:  # 64 output points of signal 0 per unit (closed-form delay kernel)
+            p = self.pts[64 * (i % 1024): 64 * (i % 1024) + 64]
+            return tuple(p), o.delay_eval_points(c["M"], c["N"], c["L"], self.g[0], p, threads=self.threads), len(p)
+        if cfg == 5:  # two full output columns of image 0 per unit
+            cols = self.cols[2 * (i % 1024): 2 * (i % 1024) + 2]
+            return tuple(cols), o.eval_2d_columns(self.g[0], self.P, self.P, cols), 2 * c["size"]
+        if cfg == 7:
+            r = int(self.order[i % len(self.order)])
+            return r, self.P.eval_offgrid(self.g[r], self.tpts.astype(np.float64)), c["npts"]
+        if cfg == 8:
+            r = int(self.order[i % len(self.order)])
+            return r, o.sisr(self.g[r].astype(np.float64), c["scale"], threads=self.threads), \
+                (c["scale"] ** 2) * c["H"] * c["W"]
+        r = int(self.order[i % len(self.order)])  # cfg 9
+        k_lo = -(c["M"] * c["N"]) * 2
+        return r, np.array(o.averaged_error(self.P, self.g[r].astype(np.complex128), k_lo)), c["nfreq"]
+
+    def run(self, budget_s, max_units=None, keep=True):
+        """Evaluate units until budget_s; returns (samples per second, units done)."""
+        done = n = 0
+        t0 = time.perf_counter()
+        while True:
+            key, val, outs = self.unit(n)
+            if keep:
+                self.results.append((key, val))
+            done += outs
+            n += 1
+            if time.perf_counter() - t0 > budget_s or (max_units and n >= max_units) or self.cfg == 1:
+                break
+        return done / (time.perf_counter() - t0), n
+
+    def sample_text(self, n):
+        c, cfg = self.c, self.cfg
+        return {1: "the whole workload (one fp64 row)",
+                2: f"{n} rows spread over the batch", 3: f"{n} rows spread over the batch (f and Hf)",
+                4: f"{64 * n} output points of signal 0 (closed-form delay kernel, {c.get('M', 0) * c.get('N', 0)} "
+                   f"terms each)",
+                5: f"{2 * n} full output columns of image 0", 6: f"{n} rows spread over the batch",
+                7: f"{n} rows x {c.get('npts')} off-grid points (direct band sums)",
+                8: f"{n} image(s) {c.get('H')}x{c.get('W')} -> x{c.get('scale')}",
+                9: f"{n} spectra x {c.get('nfreq')} coefficients (direct loops)"}[cfg] + \
+            " (oracle plan / kernel tables built before timing)"
+
+    def parity(self, out, hf=None):
+        """Per-unit relative L2 error of the GPU outputs of the sampled units."""
+        import torch
+        rel = []
+        for key, val in self.results:
+            if self.cfg == 1:
+                got = out[0].double().cpu().numpy()
+                rel.append(_rel(got, val[0]))
+            elif self.cfg == 3:
+                rel.append(_rel(out[key].double().cpu().numpy(), val[0]))
+                rel.append(_rel(hf[key].double().cpu().numpy(), val[1]))
+            elif self.cfg == 4:
+                idx = torch.tensor(key, device=out.device)
+                rel.append(_rel(out[0, idx].double().cpu().numpy(), val))
+            elif self.cfg == 5:
+                idx = torch.tensor(key, device=out.device)
+                rel.append(_rel(out[0][:, idx].double().cpu().numpy(), val))
+            elif self.cfg == 9:
+                got = out[key].double().cpu().numpy()
+                rel.append(float(np.max(np.abs(got - val) / np.abs(val))))
+            else:
+                rel.append(_rel(out[key].double().cpu().numpy(), val))
+        return np.asarray(rel)
+
+
+def _spread(batch, n):
+    n = min(n, batch)
+    mid = np.random.default_rng(12345).permutation(np.arange(1, max(batch - 1, 1)))[: max(n - 2, 0)]
+    return np.concatenate([[0], [batch - 1] if batch > 1 else [], mid]).astype(np.int64)
+
+
+def _rel(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
 def run_reference(args, rank, world):
+    """--impl reference: the tier's reference arm is the fp64 oracle (the paper ships no code),
+    timed as it stands on the host cores, one sampled unit of the same workload per step."""
     if rank != 0:
         return
-    import oracle
     cfg = args.config
-    c = synth.CONFIGS[cfg]
     w = workload(cfg)
-    threads = os.cpu_count() or 1
-    # each step = one row (cfg1-3, 6), 64 points (cfg4) or 4 columns (cfg5) of the workload
-    if cfg in (1, 2, 3, 6):
-        P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
-        P.kernel_table()
-        if c.get("hilbert"):
-            P.kernel_table(True)
-        nout = 2 if c.get("hilbert") else 1
-
-        def step(i):
-            g = make_row(cfg, i)
-            P.eval(g)
-            if c.get("hilbert"):
-                P.eval(g, hilbert=True)
-            return c["L"] * nout
-        sample = "one row per step"
-    elif cfg == 4:
-        gg, _ = synth.cfg4_signals([0])
-        pts = np.random.default_rng(0).integers(0, c["L"], 64)
-
-        def step(i):
-            oracle.delay_eval_points(c["M"], c["N"], c["L"], gg[0], pts, threads=threads)
-            return len(pts)
-        sample = "64 output points of signal 0 per step (closed-form delay kernel)"
-    elif cfg == 9:
-        P9 = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
-        s9 = make_inputs(9, 0)[:4]
-
-        def step(i):
-            oracle.averaged_error(P9, s9[i % 4].astype(np.complex128), -(c["M"] * c["N"]) * 2)
-            return c["nfreq"]
-        sample = "one spectrum per step (direct loops of Eq. averageerror)"
-    elif cfg == 8:
-        lr8, _ = synth.sisr_images([0])
-
-        def step(i):
-            oracle.sisr(lr8[0].astype(np.float64), c["scale"])
-            return (c["scale"] ** 2) * c["H"] * c["W"]
-        sample = "one image per step"
-    elif cfg == 7:
-        P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=threads)
-        g7 = make_inputs(7, 0)[:64].astype(np.float64)
-        t7 = synth.offgrid_points(c["npts"]).astype(np.float32).astype(np.float64)
-
-        def step(i):
-            P.eval_offgrid(g7[i % len(g7)], t7)
-            return c["npts"]
-        sample = f"one row's {c['npts']} off-grid points per step (direct band sums)"
-    else:
-        px = oracle.OraclePlan(2, c["N"], c["N"] * c["scale"], c["bank"], threads=threads)
-        px.kernel_table()
-        gi, _ = synth.cfg5_images([0])
-
-        def step(i):
-            oracle.eval_2d_columns(gi[0], px, px, [(i * 131) % 2048, (i * 131 + 1) % 2048])
-            return 2 * 2048
-        sample = "two full output columns of image 0 per step"
+    g_host = make_inputs(cfg, 0)
+    tpts = synth.offgrid_points(synth.CONFIGS[7]["npts"], seed=7).astype(np.float32) if cfg == 7 else None
+    leg = OracleLeg(cfg, g_host, tpts)
     for i in range(args.warmup):
-        step(i)
+        leg.unit(i)
     t0 = time.perf_counter()
     done = 0
     for i in range(args.steps):
-        done += step(i)
+        done += leg.unit(args.warmup + i)[2]
     dt = time.perf_counter() - t0
     v = done / dt
+    sample = leg.sample_text(1).replace(" (oracle plan", " per step (oracle plan")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": w["name"], "sample": sample},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": leg.threads, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model(), "plan_s": leg.plan_s},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def load_traffic(workload_name):
+    """ncu DRAM bytes (read + write) for this workload, from the committed capture summary
+    (profiles/ncu_traffic.json, written by tools/ncu_summarize.py): per step (all launches of
+    one step) when a step-wide metrics capture exists, else per launch of the dominant kernel.
+    Returns (bytes, scope, source) or (None, None, None)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
-            d = json.load(fh)
-        return d.get(workload_name)
+            d = json.load(fh).get(workload_name)
     except Exception:
-        return None
+        return None, None, None
+    if d is None:
+        return None, None, None
+    if isinstance(d, dict):
+        return d.get("bytes"), d.get("scope"), d.get("source")
+    return d, "dominant kernel, one launch", "profiles/ncu_traffic.json"
+
+
+def relaunch_cmd(args_list, n, port):
+    """The torchrun command that runs this script on n ranks of one node (one per GPU)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(args_list)
+
+
+def free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def dry_run_gloo(args, rank, world):
+    """CPU check of the multi-rank host path (tests/test_multirank.py): the torchrun
+    relaunch, the gloo rendezvous, per-rank seeded inputs, the max-over-ranks step time
+    and the single JSON line of rank 0.  No GPU work."""
+    import torch.distributed as dist
+    dist.init_process_group("gloo")
+    g = make_inputs(1, rank)
+    ms = max_over_ranks(1.0 + rank, dist, "cpu")
+    digests = [None] * world
+    dist.all_gather_object(digests, float(np.abs(g).sum()))
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ms_per_step": ms,
+                          "distinct_inputs": len(set(digests)) == world}), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
@@ -400,6 +437,7 @@ def main():
     ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dry-run-gloo", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -410,11 +448,23 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched as plain `python bench.py --gpus N`: one process per GPU under torchrun
+        if not args.dry_run_gloo:
+            import torch
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible")
+        import subprocess
+        sys.exit(subprocess.call(relaunch_cmd(sys.argv[1:], args.gpus, free_port())))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run_gloo:
+        dry_run_gloo(args, rank, world)
+        return
 
     import torch
     import torch.distributed as dist
-
-    import paper_1802_10291_b200 as mci
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -430,7 +480,7 @@ def main():
     units = w["units"]
     c = synth.CONFIGS[cfg]
     hilbert = bool(c.get("hilbert"))
-    tpts = None
+    tpts = t_host = None
     if cfg == 5:
         out = torch.empty((units, c["size"], c["size"]), dtype=tdt, device="cuda")
         hf = None
@@ -449,6 +499,7 @@ def main():
         out = torch.empty((units, c["L"]), dtype=tdt, device="cuda")
         hf = torch.empty_like(out) if hilbert else None
     stream = torch.cuda.current_stream()
+    k_lo9 = -(c.get("M", 0) * c.get("N", 0)) * 2
 
     def step():
         if cfg in (5, 8):
@@ -456,7 +507,7 @@ def main():
         elif cfg == 7:
             plan.execute_offgrid(g, tpts, out)
         elif cfg == 9:
-            plan.averaged_error(g, -(c["M"] * c["N"]) * 2, out)
+            plan.averaged_error(g, k_lo9, out)
         else:
             plan.execute(g, out, hf)
 
@@ -485,22 +536,28 @@ def main():
     value = total_samples / (ms_step / 1e3)
 
     # roofline of the dominant kernel: algorithmic bytes per launch / launch time.
-    # (cfg2: one fused launch per step, so the kernel time is the step time on the stream.)
+    # (configs 1-3, 6, 9: one launch per step, so the kernel time is the step time on the stream;
+    #  configs 4, 5, 8: several kernels per step, so the step's algorithmic bandwidth.)
     peak, peak_src = load_peaks()
     launches = plan.launches(units)
-    if cfg == 9:  # mci_averaged_error: the per-call weight table, then the per-spectrum sums
-        launches = 2
     alg_bytes = units * (w["in_per_unit"] + w["out_floats_per_unit"]) * esz
-    per_launch_ms = ms_step / launches if cfg in (1, 2, 3, 6) else ms_step
-    achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9 if cfg in (1, 2, 3, 6) else alg_bytes / (ms_step / 1e3) / 1e9
+    if cfg == 9:  # the method reads only the out-of-band coefficients (in-band ones carry no error)
+        alg_bytes = units * ((c["nfreq"] - c["M"] * c["N"]) * 2 * esz + w["out_floats_per_unit"] * esz)
+    single = cfg in (1, 2, 3, 6, 9)
+    achieved = alg_bytes / (ms_step / 1e3) / 1e9
+    tr_bytes, tr_scope, tr_src = load_traffic(w["name"])
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": load_traffic(w["name"]), "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": alg_bytes if cfg in (1, 2, 3, 6) else None,
-            "algorithmic_bytes_per_step": alg_bytes}
+            "traffic": tr_bytes, "traffic_scope": tr_scope, "traffic_source": tr_src, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": alg_bytes if single else None,
+            "algorithmic_bytes_per_step": alg_bytes,
+            "scope": "single kernel (one launch per step)" if single else f"step ({launches} launches)"}
+    if cfg == 9:
+        roof["bytes_note"] = "out-of-band coefficients (8 B each) + 3 outputs per spectrum; in-band ones are not read"
     if cfg == 7:  # direct band sums in fp64: bound by the FP64 FMA pipe
         fl = algorithmic_flops(cfg) * units / (ms_step / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": fl, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": fl / FP64_PEAK_TFLOPS, "traffic": load_traffic(w["name"]),
+                "frac": fl / FP64_PEAK_TFLOPS, "traffic": tr_bytes, "traffic_scope": tr_scope,
+                "traffic_source": tr_src,
                 "peak_source": "measured FP64 DFMA throughput (tools/microbench/f64_throughput.cu, "
                                "profiles/r01/microbench_f64.txt)",
                 "hbm_gbs_algorithmic": achieved}
@@ -528,8 +585,7 @@ def main():
             if cfg == 5:
                 plan.execute_host(gh, oh)
             elif cfg == 9:  # public device API with the host copies inside the timed step
-                oh.copy_(plan.averaged_error(gh.to("cuda", non_blocking=True), -(c["M"] * c["N"]) * 2),
-                         non_blocking=True)
+                oh.copy_(plan.averaged_error(gh.to("cuda", non_blocking=True), k_lo9), non_blocking=True)
                 torch.cuda.synchronize()
             elif cfg == 8:  # public device API with the host copies inside the timed step
                 oh.copy_(plan.execute(gh.to("cuda", non_blocking=True)), non_blocking=True)
@@ -554,11 +610,30 @@ def main():
                "h2d_bytes_per_step": int(gh.numel() * esz) + (int(th.numel() * esz) if cfg == 7 else 0),
                "d2h_bytes_per_step": int(oh.numel() * esz * (2 if hilbert else 1)),
                "ms_per_step": et * 1e3, "steps": e_steps}
+        del gh, oh, hh
 
-    cpu = None
+    # quality numbers BASELINE.json names for the configuration (not timed)
+    quality = quality_numbers(cfg, out, hf, rank)
+
+    # cpu_baseline (rank 0, N = 1): the oracle as it stands on units of this same workload,
+    # and the parity of the GPU outputs for those units
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sample, thr = oracle_sample(cfg)
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "oracle", "sample": sample}
+        leg = OracleLeg(cfg, g_host, t_host, rank)
+        v, n = leg.run(12.0)
+        leg.set_threads(1)
+        v1, n1 = leg.run(4.0, max_units=max(1, n // 4), keep=False)
+        cpu = {"value": v, "unit": UNIT, "cores": (os.cpu_count() or 1), "kind": "oracle",
+               "sample": leg.sample_text(n), "cpu_model": cpu_model(),
+               "single_thread_value": v1, "single_thread_sample": f"{n1} unit(s), threads=1",
+               "plan_s": leg.plan_s,
+               "full_config_s_extrapolated": leg.plan_s + units * w["outs_per_unit"] / v}
+        rel = leg.parity(out, hf)
+        tol = 1e-11 if cfg == 1 else 2e-6
+        parity = {"max_rel_l2": float(rel.max()), "median_rel_l2": float(np.median(rel)), "n": int(rel.size),
+                  "tol": tol, "pass": bool(rel.max() <= tol),
+                  "what": "GPU outputs of the oracle's sampled units of this run vs the fp64 oracle "
+                          "(per-unit relative L2; config 9: max relative error of eps, bound, oob)"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -568,14 +643,46 @@ def main():
                 "config": {"workload": w["name"], "units_per_gpu": units,
                            "l2": "inputs+outputs exceed the 126 MB L2 (no flush needed)" if cfg != 1 else
                            "tiny (latency-bound), L2-resident",
-                           "parallelism": f"dp{world} (independent rows per rank)"},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                           "parallelism": f"dp{world} (independent rows per rank, no collective)"},
+                "roofline": roof, "cpu_baseline": cpu, "parity": parity, "quality": quality, "e2e": e2e,
                 "gpu_launches": int(launches * args.steps),
                 "clocks": clk.summary(),
                 "hbm_gbs_algorithmic": achieved}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def quality_numbers(cfg, out, hf, rank):
+    """Config 3: relative L2 error of f against the analytic f and of Hf against the 2^20-point
+    spectral Hf (BASELINE.json configs[2]; PAPER.md:829-840) over 16 rows spread over the batch;
+    configs 5 / 8: PSNR (peak 255, output clamped to [0, 255], no crop) of the
+    distinct benchmarked images against their ground truth."""
+    import torch
+    c = synth.CONFIGS[cfg]
+    if cfg == 3:
+        rows = _spread(c["batch"], 16)
+        ef, eh = [], []
+        for r in rows:
+            fr, hr = synth.cfg3_reference(int(r), seed=3 + 1000 * rank)
+            ef.append(_rel(out[int(r)].double().cpu().numpy(), fr))
+            eh.append(_rel(hf[int(r)].double().cpu().numpy(), hr))
+        return {"rows": len(rows), "f_vs_analytic_rel_l2_max": max(ef), "f_vs_analytic_rel_l2_median":
+                float(np.median(ef)), "hf_vs_2p20_spectral_rel_l2_max": max(eh),
+                "hf_vs_2p20_spectral_rel_l2_median": float(np.median(eh))}
+    if cfg in (5, 8):
+        if cfg == 5:
+            _, truths = synth.cfg5_images(range(4 * rank, 4 * rank + 4))
+        else:
+            _, truths = synth.sisr_images(range(4 * rank, 4 * rank + 4))
+        ps = []
+        for i, tr in enumerate(truths):
+            o = out[i].double().clamp(0, 255)
+            mse = float(((o - torch.from_numpy(np.asarray(tr, dtype=np.float64)).to(o.device)) ** 2).mean())
+            ps.append(10 * math.log10(255.0 ** 2 / mse))
+        return {"psnr_db": ps, "psnr_db_mean": float(np.mean(ps)), "images": len(ps),
+                "what": "PSNR vs the ground-truth image, peak 255, output clamped to [0, 255], no crop"}
+    return None
 
 
 if __name__ == "__main__":

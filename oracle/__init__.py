@@ -254,7 +254,7 @@ def eval_2d_columns(g, plan_x: OraclePlan, plan_y: OraclePlan, px_list):
     return out
 
 
-def sisr(lr, scale=3):
+def sisr(lr, scale=3, threads=None):
     """Single-image super-resolution by MCI as the paper describes it (PAPER.md:869-886;
     SURVEY.md §8(f) NEXT-2), fp64, periodic image model.
 
@@ -267,8 +267,8 @@ def sisr(lr, scale=3):
     lr = np.asarray(lr, dtype=np.float64)
     H, W = lr.shape
     bank = [("identity",), ("derivative", 1), ("derivative", 2)]
-    px = OraclePlan(3, W, scale * W, bank)
-    py = OraclePlan(3, H, scale * H, bank)
+    px = OraclePlan(3, W, scale * W, bank, threads=threads)
+    py = OraclePlan(3, H, scale * H, bank, threads=threads)
 
     def fd(a, axis, n):
         d = 2 * np.pi / n

@@ -122,6 +122,19 @@ def _systems(bank):
     return arr, keep
 
 
+def _host_req(x, name, n_values, dtype, cplx=False):
+    """Host buffers of the *_host entry points: C-contiguous, plan dtype, the expected size."""
+    want = {("f32", False): "float32", ("f64", False): "float64",
+            ("f32", True): "complex64", ("f64", True): "complex128"}[(dtype, bool(cplx))]
+    if hasattr(x, "data_ptr"):  # CPU torch tensor
+        if x.is_cuda or not x.is_contiguous() or str(x.dtype).split(".")[-1] != want or x.numel() != n_values:
+            raise ValueError(f"{name}: contiguous CPU {want} tensor of {n_values} values required")
+    else:
+        if not (isinstance(x, np.ndarray) and x.flags.c_contiguous and x.dtype == np.dtype(want)
+                and x.size == n_values):
+            raise ValueError(f"{name}: C-contiguous {want} array of {n_values} values required")
+
+
 def _dptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
@@ -130,6 +143,22 @@ def _stream(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def _req(t, name, dtype, shape=None, device=None):
+    """Caller-supplied tensor checks (argument marshalling, not arithmetic): the C ABI takes raw
+    pointers, so a wrong dtype, shape, device or a strided view would make the kernels read or
+    write outside the buffer instead of failing."""
+    if not t.is_cuda:
+        raise ValueError(f"{name}: CUDA tensor required (there is no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: contiguous tensor required")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, plan needs {dtype}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
 
 
 def _check(status, what):
@@ -186,13 +215,17 @@ class Plan:
     def execute(self, g, f=None, hf=None, stream=None):
         """g: CUDA tensor [batch][M][N] (contiguous, plan dtype).  Returns f (and hf)."""
         import torch
-        assert g.is_cuda and g.is_contiguous() and g.dtype == self.torch_dtype()
-        assert g.shape[-2:] == (self.M, self.N)
+        _req(g, "g", self.torch_dtype())
+        if g.dim() < 2 or tuple(g.shape[-2:]) != (self.M, self.N):
+            raise ValueError(f"g: shape {tuple(g.shape)}, expected [batch][{self.M}][{self.N}]")
         batch = g.numel() // (self.M * self.N)
         if f is None:
             f = torch.empty((batch, self.L), dtype=g.dtype, device=g.device)
-        if self.hilbert and hf is None:
-            hf = torch.empty((batch, self.L), dtype=g.dtype, device=g.device)
+        _req(f, "f", g.dtype, (batch, self.L), g.device)
+        if self.hilbert:
+            if hf is None:
+                hf = torch.empty((batch, self.L), dtype=g.dtype, device=g.device)
+            _req(hf, "hf", g.dtype, (batch, self.L), g.device)
         st = _lib_handle().mci_execute_1d(self._h, batch, _dptr(g), _dptr(f), _dptr(hf) if self.hilbert else None,
                                           _stream(stream))
         _check(st, "mci_execute_1d")
@@ -202,15 +235,23 @@ class Plan:
         """f(t_j) = Re T_N f(t_j) (and Hf) at arbitrary points t (CUDA tensor [n_pts], radians);
         plan created with offgrid=True.  Returns f [batch][n_pts] (and hf)."""
         import torch
-        assert self.offgrid, "plan was not created with offgrid=True"
-        assert g.is_cuda and g.is_contiguous() and g.dtype == self.torch_dtype()
-        assert t.is_cuda and t.is_contiguous() and t.dtype == g.dtype and t.dim() == 1
+        if not self.offgrid:
+            raise ValueError("plan was not created with offgrid=True")
+        _req(g, "g", self.torch_dtype())
+        if g.dim() < 2 or tuple(g.shape[-2:]) != (self.M, self.N):
+            raise ValueError(f"g: shape {tuple(g.shape)}, expected [batch][{self.M}][{self.N}]")
+        if t.dim() != 1:
+            raise ValueError("t: 1-D tensor of points required")
+        _req(t, "t", g.dtype, device=g.device)
         batch = g.numel() // (self.M * self.N)
         npts = t.numel()
         if f is None:
             f = torch.empty((batch, npts), dtype=g.dtype, device=g.device)
-        if self.hilbert and hf is None:
-            hf = torch.empty((batch, npts), dtype=g.dtype, device=g.device)
+        _req(f, "f", g.dtype, (batch, npts), g.device)
+        if self.hilbert:
+            if hf is None:
+                hf = torch.empty((batch, npts), dtype=g.dtype, device=g.device)
+            _req(hf, "hf", g.dtype, (batch, npts), g.device)
         st = _lib_handle().mci_execute_offgrid(self._h, batch, _dptr(g), npts, _dptr(t), _dptr(f),
                                                _dptr(hf) if self.hilbert else None, _stream(stream))
         _check(st, "mci_execute_offgrid")
@@ -219,10 +260,13 @@ class Plan:
     def consistency_residual(self, g, out=None, stream=None):
         """max_{m,n} |(T_N f * h_m)(t_n) - g_m[n]| per row (plan created with analysis=True)."""
         import torch
-        assert g.is_cuda and g.is_contiguous() and g.dtype == self.torch_dtype()
+        _req(g, "g", self.torch_dtype())
+        if g.dim() < 2 or tuple(g.shape[-2:]) != (self.M, self.N):
+            raise ValueError(f"g: shape {tuple(g.shape)}, expected [batch][{self.M}][{self.N}]")
         batch = g.numel() // (self.M * self.N)
         if out is None:
             out = torch.empty((batch,), dtype=g.dtype, device=g.device)
+        _req(out, "out", g.dtype, (batch,), g.device)
         _check(_lib_handle().mci_consistency_residual(self._h, batch, _dptr(g), _dptr(out), _stream(stream)),
                "mci_consistency_residual")
         return out
@@ -231,12 +275,15 @@ class Plan:
         """eps(f, N), its bound and the out-of-band energy per spectrum: spec complex CUDA tensor
         [batch][n_freq] holding a(k_lo .. k_lo + n_freq - 1).  Returns [batch][3]."""
         import torch
-        assert spec.is_cuda and spec.is_contiguous() and spec.is_complex()
+        cdt = torch.complex128 if self.dtype == "f64" else torch.complex64
+        rdt = torch.float64 if self.dtype == "f64" else torch.float32
+        _req(spec, "spec", cdt)
+        if spec.dim() != 2:
+            raise ValueError("spec: [batch][n_freq] required")
         batch, nf = spec.shape
-        rdt = torch.float64 if spec.dtype == torch.complex128 else torch.float32
-        assert rdt == (torch.float64 if self.dtype == "f64" else torch.float32)
         if out is None:
             out = torch.empty((batch, 3), dtype=rdt, device=spec.device)
+        _req(out, "out", rdt, (batch, 3), spec.device)
         _check(_lib_handle().mci_averaged_error(self._h, batch, _dptr(spec), int(k_lo), nf, _dptr(out),
                                                 _stream(stream)), "mci_averaged_error")
         return out
@@ -246,6 +293,10 @@ class Plan:
         def p(x):
             return ctypes.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data)
         batch = int(np.prod(g.shape)) // (self.M * self.N)
+        _host_req(g, "g", batch * self.M * self.N, self.dtype, self.complex)
+        _host_req(f, "f", batch * self.L, self.dtype, self.complex)
+        if self.hilbert:
+            _host_req(hf, "hf", batch * self.L, self.dtype, self.complex)
         st = _lib_handle().mci_execute_1d_host(self._h, batch, p(g), p(f), p(hf) if self.hilbert else None)
         _check(st, "mci_execute_1d_host")
 
@@ -281,10 +332,13 @@ class Plan2D:
     def execute(self, g, out=None, stream=None):
         import torch
         dt = torch.float64 if self.dtype == "f64" else torch.float32
-        assert g.is_cuda and g.is_contiguous() and g.dtype == dt
+        _req(g, "g", dt)
+        if g.numel() % (self.My * self.Mx * self.Ny * self.Nx):
+            raise ValueError(f"g: {g.numel()} elements is not a whole number of [{self.My}][{self.Mx}][{self.Ny}][{self.Nx}] images")
         n = g.numel() // (self.My * self.Mx * self.Ny * self.Nx)
         if out is None:
             out = torch.empty((n, self.scale * self.Ny, self.scale * self.Nx), dtype=dt, device=g.device)
+        _req(out, "out", dt, (n, self.scale * self.Ny, self.scale * self.Nx), g.device)
         st = _lib_handle().mci_execute_2d(self._h, n, _dptr(g), _dptr(out), _stream(stream))
         _check(st, "mci_execute_2d")
         return out
@@ -293,6 +347,8 @@ class Plan2D:
         def p(x):
             return ctypes.c_void_p(x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data)
         n = int(np.prod(g.shape)) // (self.My * self.Mx * self.Ny * self.Nx)
+        _host_req(g, "g", n * self.My * self.Mx * self.Ny * self.Nx, self.dtype)
+        _host_req(out, "out", n * self.scale * self.Ny * self.scale * self.Nx, self.dtype)
         st = _lib_handle().mci_execute_2d_host(self._h, n, p(g), p(out))
         _check(st, "mci_execute_2d_host")
 
@@ -327,10 +383,14 @@ class SisrPlan:
     def execute(self, lr, hr=None, stream=None):
         """lr: CUDA tensor [n][H][W] (plan dtype).  Returns hr [n][scale H][scale W]."""
         import torch
-        assert lr.is_cuda and lr.is_contiguous() and lr.shape[-2:] == (self.H, self.W)
+        dt = torch.float64 if self.dtype == "f64" else torch.float32
+        _req(lr, "lr", dt)
+        if lr.dim() < 2 or tuple(lr.shape[-2:]) != (self.H, self.W):
+            raise ValueError(f"lr: shape {tuple(lr.shape)}, expected [n][{self.H}][{self.W}]")
         n = lr.numel() // (self.H * self.W)
         if hr is None:
-            hr = torch.empty((n, self.scale * self.H, self.scale * self.W), dtype=lr.dtype, device=lr.device)
+            hr = torch.empty((n, self.scale * self.H, self.scale * self.W), dtype=dt, device=lr.device)
+        _req(hr, "hr", dt, (n, self.scale * self.H, self.scale * self.W), lr.device)
         st = _lib_handle().mci_execute_sisr(self._h, n, _dptr(lr), _dptr(hr), _stream(stream))
         _check(st, "mci_execute_sisr")
         return hr

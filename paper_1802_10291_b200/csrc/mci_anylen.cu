@@ -684,78 +684,104 @@ cudaError_t launch_anylen_residual(const Axis1D &ax, const RowAddr &ra, int64_t 
     return anylen_dispatch(ax, ra, rows, g, out, nullptr, st, &marker, -1);
 }
 
-// eps(f, N) of a batch of spectra: one warp per signal, sums in fp64 (Eq. averageerror)
-// Per-coefficient weights of eps(f, N) (Theorem error, Eq. errorestimate): for band-external
-// n, wt[i] = (1 + sum_l |sum_m r_m(j + lN) b_m(n)|^2, sum_m |b_m(n)|^2); in-band n: (-1, 0).
-// They depend on n only, so they are computed once per call instead of once per spectrum.
-__global__ void mci_avg_error_weights(int64_t k_lo, int nf, int M, int N, int64_t K1, const void *Qv, bool q64,
-                                      AnyErrSys sy, double2 *__restrict__ wt) {
+// eps(f, N) of a batch of spectra (Theorem error, Eq. averageerror / errorestimate).
+// The weight of a band-external coefficient n,
+//   wt(n) = (1 + sum_l |sum_m r_m(j + lN) b_m(n)|^2,  sum_m |b_m(n)|^2),  in-band n: (-1, 0),
+// depends on n only.  Execute never allocates (include/mci.h), so no table is shared across
+// the batch: each CTA owns AE_SPEC spectra and walks the frequency axis in chunks of AE_FC,
+// computing the chunk's weights into shared memory once and streaming its spectra's chunk
+// through them (fp64 partial sums in shared memory, fixed order: deterministic).  The
+// weights are recomputed once per CTA (batch / AE_SPEC times in all), a few per cent of
+// the step for config 9; the spectra stream from HBM exactly once.
+constexpr int AE_FC = 1024;   // frequencies per chunk (16 KB of fp64 weights)
+constexpr int AE_SPEC = 64;   // spectra per CTA
+constexpr int AE_THREADS = 256;
+
+__device__ __forceinline__ double2 avg_error_weight(int64_t n, int M, int N, int64_t K1, const void *Qv, bool q64,
+                                                    const AnyErrSys &sy) {
     using namespace anyk;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
-        const int64_t n = k_lo + i;
-        const int64_t d = n - K1;
-        const int64_t kb = (d >= 0 ? d / N : -((-d + N - 1) / N)) + 1;  // block index of n
-        if (kb >= 1 && kb <= M) {
-            wt[i] = make_double2(-1.0, 0.0);
-            continue;
-        }
-        const int64_t j = n - (kb - 1) * N;  // the class element of I_1
-        const int q = (int)(((j % N) + N) % N);
-        double2 b[8];
-        double bsum = 0;
-        for (int m = 0; m < M; ++m) {
-            b[m] = bmul(sy.s[m], n);
-            bsum += b[m].x * b[m].x + b[m].y * b[m].y;
-        }
-        double w = 0;
-        for (int l = 0; l < M; ++l) {  // S_l = sum_m r_m(j + lN) b_m(n), r_m(j + lN) = N Q~_q[m][l]
-            double sr = 0, si = 0;
-            for (int m = 0; m < M; ++m) {
-                const int64_t e = ((int64_t)q * M + m) * M + l;
-                double rr, ri;
-                if (q64) {
-                    const double2 r = static_cast<const double2 *>(Qv)[e];
-                    rr = r.x * N, ri = r.y * N;
-                } else {
-                    const float2 r = static_cast<const float2 *>(Qv)[e];
-                    rr = (double)r.x * N, ri = (double)r.y * N;
-                }
-                sr += rr * b[m].x - ri * b[m].y;
-                si += rr * b[m].y + ri * b[m].x;
-            }
-            w += sr * sr + si * si;
-        }
-        wt[i] = make_double2(1.0 + w, bsum);
+    const int64_t d = n - K1;
+    const int64_t kb = (d >= 0 ? d / N : -((-d + N - 1) / N)) + 1;  // block index of n
+    if (kb >= 1 && kb <= M) return make_double2(-1.0, 0.0);
+    const int64_t j = n - (kb - 1) * N;  // the class element of I_1
+    const int q = (int)(((j % N) + N) % N);
+    double2 b[8];
+    double bsum = 0;
+    for (int m = 0; m < M; ++m) {
+        b[m] = bmul(sy.s[m], n);
+        bsum += b[m].x * b[m].x + b[m].y * b[m].y;
     }
+    double w = 0;
+    for (int l = 0; l < M; ++l) {  // S_l = sum_m r_m(j + lN) b_m(n), r_m(j + lN) = N Q~_q[m][l]
+        double sr = 0, si = 0;
+        for (int m = 0; m < M; ++m) {
+            const int64_t e = ((int64_t)q * M + m) * M + l;
+            double rr, ri;
+            if (q64) {
+                const double2 r = static_cast<const double2 *>(Qv)[e];
+                rr = r.x * N, ri = r.y * N;
+            } else {
+                const float2 r = static_cast<const float2 *>(Qv)[e];
+                rr = (double)r.x * N, ri = (double)r.y * N;
+            }
+            sr += rr * b[m].x - ri * b[m].y;
+            si += rr * b[m].y + ri * b[m].x;
+        }
+        w += sr * sr + si * si;
+    }
+    return make_double2(1.0 + w, bsum);
 }
 
-// One warp per spectrum: fp64 sums of |a(n)|^2 times the precomputed weights.
 template <typename T>
-__global__ void mci_avg_error_kernel(const cv<T> *__restrict__ spec, int nf, int64_t batch, int M, double omega_sum,
-                                     const double2 *__restrict__ wt, T *__restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int64_t sig = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    if (sig >= batch) return;
-    const cv<T> *a = spec + sig * (int64_t)nf;
-    double e2 = 0, oob = 0, cs = 0;
-    for (int i = lane; i < nf; i += 32) {
-        const double2 w = __ldg(wt + i);
-        if (w.x < 0.0) continue;  // in-band coefficient
-        const cv<T> an = a[i];
-        const double a2 = (double)an.x * an.x + (double)an.y * an.y;
-        e2 += a2 * w.x;
-        oob += a2;
-        cs += a2 * w.y;
+__global__ void __launch_bounds__(AE_THREADS) mci_avg_error_kernel(const cv<T> *__restrict__ spec, int nf,
+                                                                    int64_t batch, int64_t k_lo, int M, int N,
+                                                                    int64_t K1, const void *Qv, bool q64,
+                                                                    AnyErrSys sy, double omega_sum,
+                                                                    T *__restrict__ out) {
+    __shared__ double2 wt[AE_FC];
+    __shared__ double acc[AE_SPEC][3];  // (e2, oob, cs) per spectrum of this CTA
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = AE_THREADS / 32;
+    const int64_t s0 = (int64_t)blockIdx.x * AE_SPEC;
+    const int ns = batch - s0 < AE_SPEC ? (int)(batch - s0) : AE_SPEC;
+    for (int i = threadIdx.x; i < AE_SPEC * 3; i += AE_THREADS) (&acc[0][0])[i] = 0.0;
+    for (int c0 = 0; c0 < nf; c0 += AE_FC) {
+        const int nc = min(AE_FC, nf - c0);
+        __syncthreads();  // previous chunk's weights consumed (and acc zeroed on the first pass)
+        for (int i = threadIdx.x; i < nc; i += AE_THREADS)
+            wt[i] = avg_error_weight(k_lo + c0 + i, M, N, K1, Qv, q64, sy);
+        __syncthreads();
+        for (int s = warp; s < ns; s += NW) {  // warp s % NW owns spectrum s: no races on acc[s]
+            const cv<T> *a = spec + (s0 + s) * (int64_t)nf + c0;
+            double e2 = 0, oob = 0, cs = 0;
+            for (int i = lane; i < nc; i += 32) {
+                const double2 w = wt[i];
+                if (w.x < 0.0) continue;  // in-band coefficient: not read
+                const cv<T> an = a[i];
+                const double a2 = (double)an.x * an.x + (double)an.y * an.y;
+                e2 += a2 * w.x;
+                oob += a2;
+                cs += a2 * w.y;
+            }
+            for (int o = 16; o; o >>= 1) {
+                e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+                oob += __shfl_xor_sync(0xffffffffu, oob, o);
+                cs += __shfl_xor_sync(0xffffffffu, cs, o);
+            }
+            if (lane == 0) {
+                acc[s][0] += e2;
+                acc[s][1] += oob;
+                acc[s][2] += cs;
+            }
+        }
     }
-    for (int o = 16; o; o >>= 1) {
-        e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-        oob += __shfl_xor_sync(0xffffffffu, oob, o);
-        cs += __shfl_xor_sync(0xffffffffu, cs, o);
-    }
-    if (lane == 0) {
-        out[sig * 3 + 0] = (T)sqrt(e2);
-        out[sig * 3 + 1] = (T)sqrt(oob + M * omega_sum * cs);
-        out[sig * 3 + 2] = (T)oob;
+    __syncthreads();
+    for (int s = threadIdx.x; s < ns; s += AE_THREADS) {
+        const double e2 = acc[s][0], oob = acc[s][1], cs = acc[s][2];
+        T *o = out + (s0 + s) * 3;
+        o[0] = (T)sqrt(e2);
+        o[1] = (T)sqrt(oob + M * omega_sum * cs);
+        o[2] = (T)oob;
     }
 }
 
@@ -764,24 +790,17 @@ cudaError_t launch_averaged_error(const Axis1D &ax, int64_t batch, const void *s
     if (batch <= 0) return cudaSuccess;
     AnyErrSys sy;
     for (int m = 0; m < 8; ++m) sy.s[m] = ax.sys[m];
-    // weight table: stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on the caller's
-    // stream: no device synchronisation, and concurrent calls on other streams stay independent)
-    double2 *wt = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&wt, (size_t)std::max<int64_t>(n_freq, 1) * sizeof(double2), st);
-    if (e != cudaSuccess) return e;
-    const unsigned wgrid = (unsigned)std::min<int64_t>((n_freq + 255) / 256 + 1, 4096);
-    mci_avg_error_weights<<<wgrid, 256, 0, st>>>(k_lo, (int)n_freq, ax.M, (int)ax.N, ax.K1, ax.Qt,
-                                                 ax.dtype == MCI_F64, sy, wt);
-    const unsigned grid = (unsigned)((batch + 7) / 8);
+    const int64_t grid = (batch + AE_SPEC - 1) / AE_SPEC;
+    if (grid > 0x7fffffff) return cudaErrorInvalidValue;
     if (ax.dtype == MCI_F64)
-        mci_avg_error_kernel<double><<<grid, 256, 0, st>>>((const cv<double> *)spec, (int)n_freq, batch, ax.M,
-                                                           ax.omega_sum, wt, (double *)out);
+        mci_avg_error_kernel<double><<<(unsigned)grid, AE_THREADS, 0, st>>>(
+            (const cv<double> *)spec, (int)n_freq, batch, k_lo, ax.M, (int)ax.N, ax.K1, ax.Qt, true, sy,
+            ax.omega_sum, (double *)out);
     else
-        mci_avg_error_kernel<float><<<grid, 256, 0, st>>>((const cv<float> *)spec, (int)n_freq, batch, ax.M,
-                                                          ax.omega_sum, wt, (float *)out);
-    e = cudaGetLastError();
-    cudaFreeAsync(wt, st);
-    return e;
+        mci_avg_error_kernel<float><<<(unsigned)grid, AE_THREADS, 0, st>>>(
+            (const cv<float> *)spec, (int)n_freq, batch, k_lo, ax.M, (int)ax.N, ax.K1, ax.Qt, false, sy,
+            ax.omega_sum, (float *)out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_anylen_offgrid(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, int64_t n_pts,

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(IC_NT) mci_fs_ic(const FSArgs<T> a) {
         }
         T *dst = frow + (int64_t)R * (u0 + t + a.S2 * v);
         if constexpr (sizeof(T) == 4) {
-            if (R == 4) {
+            if (R == 4 && aligned16(dst)) {
                 *reinterpret_cast<float4 *>(dst) = make_float4(vals[0], vals[1], vals[2], vals[3]);
                 continue;
             }
@@ -295,7 +295,7 @@ static cudaError_t fs_launch_t(const Axis1D &ax, int64_t batch, const void *g, v
     if ((e = cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fs_fb<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fs_ic<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ic_sm))) return e;
-    const bool fast = fourstep_fast_ok(ax) && !getenv("MCI_FOURSTEP_GENERIC");
+    const bool fast = fourstep_fast_ok(ax) && aligned16(g) && aligned16(f) && !getenv("MCI_FOURSTEP_GENERIC");
     for (int64_t s0 = 0; s0 < batch; s0 += ws_sig) {
         const int64_t ns = (batch - s0 < ws_sig) ? batch - s0 : ws_sig;
         a.sig0 = s0;

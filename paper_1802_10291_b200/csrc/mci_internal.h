@@ -55,6 +55,11 @@ struct Axis1D {
     AnyRadix radN, radL;
 };
 
+// Vector accesses of the specialised kernels (128-bit loads / TMA bulk copies / float2 and
+// float4 stores) need 16-byte aligned row bases; misaligned buffers (an offset view of a
+// tensor, a C caller's odd pointer) are routed to kernels that access elements one by one.
+__host__ __device__ inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
 enum Path { PATH_FUSED = 0, PATH_FOURSTEP = 1, PATH_2D = 2, PATH_SISR = 3 };
 
 // Row addressing of the fused kernel: row r starts at

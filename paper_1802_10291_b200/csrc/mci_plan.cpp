@@ -675,11 +675,11 @@ namespace mci {
 cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const void *g, void *f, void *hf,
                         cudaStream_t st, int *nl) {
     if (ax.special == 4) return launch_anylen(ax, ra, rows, g, f, hf, st, nl);
-    if (ax.special == 1 && ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N)
-        return launch_row(ax, ax.rowtab, rows, g, f, st, nl);
-    if (ax.special == 2) return launch_line(ax, ra, rows, g, f, st, nl);
-    if (ax.special == 3 && ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N)
-        return launch_hilbert(ax, rows, g, f, hf, st, nl);
+    const bool dense = ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N;
+    const bool al = aligned16(g) && aligned16(f) && (!hf || aligned16(hf));
+    if (ax.special == 1 && dense && al) return launch_row(ax, ax.rowtab, rows, g, f, st, nl);
+    if (ax.special == 2) return launch_line(ax, ra, rows, g, f, st, nl);  // checks its own alignment
+    if (ax.special == 3 && dense && al) return launch_hilbert(ax, rows, g, f, hf, st, nl);
     return launch_fused(ax, ra, rows, g, f, hf, st, nl);
 }
 }  // namespace mci
@@ -845,8 +845,12 @@ void mci_plan_destroy(mci_plan p) {
     delete p;
 }
 
+// the 1D entry points serve 1D plans only: a 2D or SISR plan has neither the 1D axis nor the
+// workspace layout exec_1d would launch on
+static bool is_1d(mci_plan p) { return p && (p->path == mci::PATH_FUSED || p->path == mci::PATH_FOURSTEP); }
+
 mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, void *hf, void *stream) {
-    if (!p || p->path == mci::PATH_2D || batch < 0) return MCI_E_ARG;
+    if (!is_1d(p) || batch < 0) return MCI_E_ARG;
     if (batch == 0) return MCI_OK;
     if (!g || !f) return MCI_E_ARG;
     if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
@@ -855,7 +859,7 @@ mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, voi
 
 mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t n_pts, const void *t, void *f,
                                void *hf, void *stream) {
-    if (!p || p->path == mci::PATH_2D || !(p->flags & MCI_OFFGRID) || p->ay.special != 4 || batch < 0 ||
+    if (!is_1d(p) || !(p->flags & MCI_OFFGRID) || p->ay.special != 4 || batch < 0 ||
         n_pts < 0 || n_pts > INT32_MAX)
         return MCI_E_ARG;
     if (batch == 0 || n_pts == 0) return MCI_OK;
@@ -869,7 +873,7 @@ mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t
 }
 
 mci_status mci_consistency_residual(mci_plan p, int64_t batch, const void *g, void *out, void *stream) {
-    if (!p || p->path == mci::PATH_2D || p->path == mci::PATH_SISR || !(p->flags & MCI_ANALYSIS) ||
+    if (!is_1d(p) || !(p->flags & MCI_ANALYSIS) ||
         p->ay.special != 4 || batch < 0)
         return MCI_E_ARG;
     if (batch == 0) return MCI_OK;
@@ -883,7 +887,7 @@ mci_status mci_consistency_residual(mci_plan p, int64_t batch, const void *g, vo
 
 mci_status mci_averaged_error(mci_plan p, int64_t batch, const void *spec, int64_t k_lo, int64_t n_freq, void *out,
                               void *stream) {
-    if (!p || p->path == mci::PATH_2D || p->path == mci::PATH_SISR || !(p->flags & MCI_ANALYSIS) ||
+    if (!is_1d(p) || !(p->flags & MCI_ANALYSIS) ||
         p->ay.special != 4 || batch < 0 || n_freq < 0 || n_freq > INT32_MAX)
         return MCI_E_ARG;
     if (batch == 0) return MCI_OK;
@@ -965,7 +969,7 @@ static mci_status exec_host(mci_plan p, int64_t units, const void *g, void *f, v
 }
 
 mci_status mci_execute_1d_host(mci_plan p, int64_t batch, const void *g, void *f, void *hf) {
-    if (!p || p->path == mci::PATH_2D || batch < 0) return MCI_E_ARG;
+    if (!is_1d(p) || batch < 0) return MCI_E_ARG;
     if (batch == 0) return MCI_OK;
     if (!g || !f) return MCI_E_ARG;
     if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;

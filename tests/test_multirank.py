@@ -47,3 +47,21 @@ def test_two_ranks_gloo():
     for rank, mx, gathered in res:
         assert mx == pytest.approx(2.5)            # max over ranks
         assert gathered[0] != gathered[1]          # each rank owns distinct rows
+
+
+def test_bench_launcher_two_ranks():
+    """`python bench.py --gpus 2` relaunches itself under torch.distributed.run (one process
+    per GPU); the dry run exercises that launcher, the rendezvous on 127.0.0.1, per-rank
+    seeded inputs and the max-over-ranks step time on gloo, and rank 0 alone prints one line."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run-gloo"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["ms_per_step"] == pytest.approx(2.0) and d["distinct_inputs"]

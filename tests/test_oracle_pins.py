@@ -486,3 +486,35 @@ def test_p13_consistency_residual():
     P.r = P.r.copy()
     P.r[1, 5] += 1e-3
     assert oracle.consistency_residual(P, g) > 1e-6
+
+
+def test_p13_bound_closed_forms():
+    """Exact values of eps, bound and oob (Eq. averageerror / errorestimate, PAPER.md:722-747,
+    DESIGN.md reading R12) worked by hand, so that a slip in the bound (Omega = sup|r| instead
+    of sup|r|^2, a dropped factor M, sum_m Omega_m replaced by max) fails:
+    (i) M = 1 identity channel: r = 1, Omega = 1, b = 1, so every out-of-band coefficient
+        aliases onto one in-band bin with weight 1 + 1 and bound^2 = oob + 1 * 1 * oob:
+        eps = bound = sqrt(2 oob).
+    (ii) M = 2, (1, ik), N = 4, band -4..3, a(5) = 1 only.  H_j = [[1, ij], [1, i(j+N)]],
+        det = iN, H_j^{-1} = (1/(iN)) [[i(j+N), -ij], [-1, 1]] (Eq. defH),
+        so r_0(j) = (j+N)/N, r_0(j+N) = -j/N, r_1(j) = i/N, r_1(j+N) = -i/N.  n = 5 lies in
+        block k = 3 of class j = -3: the weights are |r_0(-3) + 5i r_1(-3)|^2 = |1/4 - 5/4|^2 = 1
+        and |r_0(1) + 5i r_1(1)|^2 = |3/4 + 5/4|^2 = 4 (reconstruction -e^{-3it} + 2e^{it}
+        from the aliased samples e^{it_n}, 5i e^{it_n}), so eps^2 = 1 + 1 + 4 = 6.
+        Omega_0 = sup|r_0|^2 = 1 (r_0(0) = 1), Omega_1 = 1/16, sum_m |b_m(5)|^2 = 1 + 25:
+        bound^2 = 1 + 2 (1 + 1/16) 26 = 56.25, bound = 7.5."""
+    P1 = oracle.OraclePlan(1, 8, 32, [("identity",)])
+    rng = np.random.default_rng(131)
+    k_lo = -20
+    spec = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+    eps, bound, oob = oracle.averaged_error(P1, spec, k_lo)
+    n = np.arange(k_lo, k_lo + 40)
+    oob_ref = np.sum(np.abs(spec[(n < -4) | (n >= 4)]) ** 2)
+    assert abs(oob - oob_ref) < 1e-12 * oob_ref
+    assert abs(eps - np.sqrt(2 * oob_ref)) < 1e-12 * eps
+    assert abs(bound - np.sqrt(2 * oob_ref)) < 1e-12 * bound
+    P2 = oracle.OraclePlan(2, 4, 16, [("identity",), ("derivative", 1)])
+    eps, bound, oob = oracle.averaged_error(P2, np.array([1.0 + 0j]), 5)
+    assert abs(oob - 1.0) < 1e-14
+    assert abs(eps - np.sqrt(6.0)) < 1e-13
+    assert abs(bound - 7.5) < 1e-13
