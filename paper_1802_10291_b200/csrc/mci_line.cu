@@ -22,10 +22,14 @@
 // pass-2 twiddles are read from tensor memory (a copy per lane quarter), off the
 // shared-memory pipe that bounds the kernel; for the (1, ik) bank the solve uses
 // the closed-form inverse instead of the Q~ table.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "mci_internal.h"
 #include "mci_pk.cuh"
@@ -82,9 +86,13 @@ struct LineTables {
 // through the warp buffers; the row pass then reads contiguous lines.
 // PF (contiguous lines, untiled; with TILED it selects the G16 gather below): the next line's two channel rows are copied by 16-byte
 // cp.async into the warp's own buffer while the current line's inverse finishes.
-template <int WARPS, bool TILED, bool TM = false, bool TST = false, bool PF = false>
+// TMA (TILED with PF): the [m][n][16 lines] tile arrives by four tensor-map box loads
+// (cp.async.bulk.tensor, 16 lines x 256 samples each, 64-byte swizzle = the G16 chunk XOR)
+// issued by one thread on an mbarrier, instead of 8 cp.async per thread through the LSU.
+template <int WARPS, bool TILED, bool TM = false, bool TST = false, bool PF = false, bool TMA = false>
 __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kernel(const float *__restrict__ g, float *__restrict__ f,
-                                                              int64_t lines, RowAddr ra, LineTables tb) {
+                                                              int64_t lines, RowAddr ra, LineTables tb,
+                                                              const __grid_constant__ CUtensorMap tmap) {
     using namespace linek;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -102,7 +110,12 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     // CT: buffer stride = 2 (mod 16) float2 for the 8-line write-out mapping
     constexpr int BUFS = CT ? BUF + 1 : BUF;
     float2 *bufs = CT ? fwt + 512 : iw + 1024;      // WARPS x BUFS
-    float *stage = reinterpret_cast<float *>(bufs + WARPS * BUFS);  // TILED: [2][WARPS][SP]
+    // TILED: [2][WARPS][SP]; TMA: [2][N][16] at a 1024-byte boundary (the swizzle pattern is
+    // a function of the shared-memory address bits)
+    float *stage = reinterpret_cast<float *>(
+        TMA ? (unsigned char *)(((uintptr_t)(bufs + WARPS * BUFS) + 1023) & ~(uintptr_t)1023)
+            : (unsigned char *)(bufs + WARPS * BUFS));
+    __shared__ __align__(8) uint64_t tbar;  // TMA: tile landed (expect_tx)
     if (!CT) {
         for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
         for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
@@ -190,6 +203,29 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         return (m * N + n) * TW + ((((l >> 2) ^ (TW == 16 ? (n >> 1) : 0)) & (CPR - 1)) << 2) + (l & 3);
     };
     auto fetch_tile = [&](int64_t t, int64_t tb0) {
+        if constexpr (TMA) {
+            if (threadIdx.x == 0 && t < ntiles) {
+                const uint32_t l0 = (uint32_t)(t * WARPS), a = l0 / uD0, x0 = l0 - a * uD0, c4 = a / uD1,
+                               c3 = a - c4 * uD1;
+                const uint32_t bar = s32(&tbar);
+                // the stage was read through the generic proxy (CTA barrier before this call)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                             "r"((uint32_t)(2 * N * TW * 4))
+                             : "memory");
+#pragma unroll
+                for (int m = 0; m < 2; ++m)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+                        asm volatile(
+                            "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(s32(stage + (m * N + hh * 256) * TW)),
+                            "l"(&tmap), "r"(x0), "r"(hh * 256), "r"(m), "r"(c3), "r"(c4), "r"(bar)
+                            : "memory");
+            }
+            (void)tb0;
+            return;
+        }
         if (G16) {
             if (t < ntiles) {
 #pragma unroll
@@ -248,6 +284,14 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if constexpr (PF && !TILED) prefetch_line((int64_t)blockIdx.x * WARPS + warp);
+    uint32_t tph = 0;  // TMA: parity of the tile barrier
+    if constexpr (TMA) {
+        if (threadIdx.x == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&tbar)) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
     // TILED: D0 % WARPS == 0, so a tile's lines share the outer indices: base = tile base + warp s0
     int64_t tbase = 0;
     if constexpr (TILED) {
@@ -265,8 +309,19 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         pk x[16];
         float m0 = 0.f, m1 = 0.f;
         if constexpr (TILED) {
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
-            __syncthreads();  // tile tl has landed
+            if constexpr (TMA) {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile(
+                        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                        : "=r"(done)
+                        : "r"(s32(&tbar)), "r"(tph)
+                        : "memory");
+                tph ^= 1u;
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+                __syncthreads();  // tile tl has landed
+            }
             if (line < lines) {
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -519,6 +574,37 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     }
 }
 
+// Tensor map of the tiled 2D pass input: dims (innermost first) line-in-block x (D0, stride 1),
+// sample n (N, stride ss), channel m (2, stride cs), block a1 (D1, stride s1), block b (stride s2),
+// fp32; box 16 lines x 256 samples x 1 x 1 x 1, 64-byte swizzle (16-byte chunk c of 64-byte
+// row n stored at chunk c ^ ((n >> 1) & 3), the layout of the G16 gather).  The driver entry
+// point comes through the runtime (no libcuda link dependency).
+static bool encode_tile_map(CUtensorMap *tm, const void *g, const RowAddr &ra, int64_t lines, int N) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            cudaGetLastError();
+            return false;
+        }
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    if (ra.s0 != 1 || ra.D0 % 16 != 0 || lines % (ra.D0 * ra.D1) != 0) return false;
+    const int64_t nb = lines / (ra.D0 * ra.D1);
+    if (ra.D0 >= (1ll << 31) || nb >= (1ll << 31) || ra.D1 >= (1ll << 31)) return false;
+    auto okst = [](int64_t s) { return s > 0 && (s * 4) % 16 == 0 && s * 4 < (1ll << 40); };
+    const int64_t s1 = ra.D1 > 1 ? ra.s1 : 4, s2 = nb > 1 ? ra.s2 : 4;
+    if (!okst(ra.ss) || !okst(ra.cs) || !okst(s1) || !okst(s2)) return false;
+    const cuuint64_t dims[5] = {(cuuint64_t)ra.D0, (cuuint64_t)N, 2, (cuuint64_t)ra.D1, (cuuint64_t)nb};
+    const cuuint64_t strides[4] = {(cuuint64_t)ra.ss * 4, (cuuint64_t)ra.cs * 4, (cuuint64_t)s1 * 4, (cuuint64_t)s2 * 4};
+    const cuuint32_t box[5] = {16, 256, 1, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<void *>(g), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool line_supported(const Axis1D &ax) {
     return ax.dtype == MCI_F32 && !ax.analytic && ax.M == 2 && ax.N == 512 && ax.L == 2048 && ax.S == 1024;
 }
@@ -567,7 +653,14 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // compact shared memory), so one CTA's write-out overlaps the other's transforms
     const bool ct8 = tstore && tiled && g16 && tm && getenv("MCI_LINE_CT8") && atoi(getenv("MCI_LINE_CT8")) == 1;
     const int WARPS = ct8 ? 8 : (tiled || tstore) ? 16 : 8;
+    // tiled 16-line transposed-store pass: the tile gather by TMA tensor-map box loads
+    // (MCI_LINE_TMA=0: the 16-byte cp.async gather, A/B)
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof(tmap));
+    const bool tma = tstore && tiled && g16 && tm && !ct8 && !(getenv("MCI_LINE_TMA") && atoi(getenv("MCI_LINE_TMA")) == 0) &&
+                     encode_tile_map(&tmap, g, ra, lines, linek::N);
     auto kern = ct8 ? mci_line_kernel<8, true, true, true, true>
+                : tma ? mci_line_kernel<16, true, true, true, true, true>
                 : tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
                 : (tstore && g16) ? (tm ? mci_line_kernel<16, true, true, true, true> : mci_line_kernel<16, true, false, true, true>)
                 : tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
@@ -577,7 +670,8 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
                         : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
     const size_t smem = ct8 ? (size_t)(512 + WARPS * (linek::BUF + 1)) * 8 + (size_t)2 * WARPS * linek::SP * 4
                             : (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
-                                  (tiled ? (size_t)2 * WARPS * linek::SP * 4 : tstore_c ? (size_t)WARPS * 2 * linek::N * 4 : 0);
+                                  (tiled ? (size_t)2 * WARPS * linek::SP * 4 : tstore_c ? (size_t)WARPS * 2 * linek::N * 4 : 0) +
+                                  (tma ? 1024 : 0);  // TMA: the stage starts at a 1024-byte boundary
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148, occ = 1;
@@ -609,7 +703,7 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     const int64_t need = (lines + WARPS - 1) / WARPS;
     if (grid > need) grid = need;
     if (n_launches) *n_launches += 1;
-    kern<<<(unsigned)grid, WARPS * 32, smem, st>>>((const float *)g, (float *)f, lines, ra, tb);
+    kern<<<(unsigned)grid, WARPS * 32, smem, st>>>((const float *)g, (float *)f, lines, ra, tb, tmap);
     return cudaGetLastError();
 }
 
