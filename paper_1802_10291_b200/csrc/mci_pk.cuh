@@ -100,6 +100,64 @@ template <int R, int E, int DIR> __device__ __forceinline__ pk twc(pk v) {
     }
 }
 
+// Fused twiddle butterfly: (a, b) <- (a + w b, a - w b), w = e^{DIR 2 pi i E / 64}, E compile-time.
+// Quadrant points are swizzled adds (2 instructions); a general w = c + i s costs 3 instead of the
+// 4 of a complex multiply and two adds: u = b + (s/c)(i b), then a +- c u (|c| >= |s|), or
+// u = i b + (c/s) b, then a +- s u.  Each output is rounded twice, as with the unfused form.
+#ifndef MCI_PK_FUSED
+#define MCI_PK_FUSED 1
+#endif
+template <int E, int DIR> __device__ __forceinline__ void twf(pk &a, pk &b) {
+    constexpr int e = ((E % 64) + 64) % 64;
+    const pk t = a;
+    if constexpr (e == 0) {
+        a = add(t, b);
+        b = sub(t, b);
+    } else if constexpr (e == 16) {
+        a = add_rot<DIR>(t, b);
+        b = sub_rot<DIR>(t, b);
+    } else if constexpr (e == 32) {
+        a = sub(t, b);
+        b = add(t, b);
+    } else if constexpr (e == 48) {
+        a = sub_rot<DIR>(t, b);
+        b = add_rot<DIR>(t, b);
+    } else {
+        constexpr double c = cl::cos64(e), sn = DIR * cl::sin64(e);
+        constexpr bool CB = (c < 0 ? -c : c) >= (sn < 0 ? -sn : sn);
+        constexpr float f = (float)(CB ? c : sn), r = (float)(CB ? sn / c : c / sn);
+        const float2 bf = f2(b);
+        const pk ib = mk(-bf.y, bf.x);  // i b
+        const pk u = CB ? fma(ib, bc(r), b) : fma(b, bc(r), ib);
+        a = fma(u, bc(f), t);
+        b = fma(u, bc(-f), t);
+    }
+}
+
+// DFT of size R (power of two, <= 64) of the inputs x[n] w^{n E}, w = e^{DIR 2 pi i / 64}
+// (input twiddles E compile-time, in 64ths of a turn), natural order in and out: radix-2
+// decimation in time whose every twiddle rides in a fused butterfly (twf).
+template <int R, int E, int DIR> __device__ __forceinline__ void dftw(pk *x) {
+    if constexpr (R == 2) {
+        twf<E, DIR>(x[0], x[1]);
+    } else if constexpr (R > 2) {
+        pk ev[R / 2], od[R / 2];
+#pragma unroll
+        for (int m = 0; m < R / 2; ++m) {
+            ev[m] = x[2 * m];
+            od[m] = x[2 * m + 1];
+        }
+        dftw<R / 2, 2 * E, DIR>(ev);
+        dftw<R / 2, 2 * E, DIR>(od);
+        cl::static_for<0, R / 2>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            twf<E + (64 / R) * k, DIR>(ev[k], od[k]);
+            x[k] = ev[k];
+            x[k + R / 2] = od[k];
+        });
+    }
+}
+
 template <int DIR> __device__ __forceinline__ void dft2(pk &a, pk &b) {
     const pk t = a;
     a = add(t, b);
@@ -126,18 +184,19 @@ template <int R1, int R2, int DIR> __device__ __forceinline__ void dft2s(pk *x) 
         dft<R2, DIR>(t);
         cl::static_for<0, R2>([&](auto k2c) {
             constexpr int k2 = decltype(k2c)::value;
-            y[n1 + R1 * k2] = twc<R, n1 * k2, DIR>(t[k2]);
+            y[n1 + R1 * k2] = MCI_PK_FUSED ? t[k2] : twc<R, n1 * k2, DIR>(t[k2]);
         });
     });
-#pragma unroll
-    for (int k2 = 0; k2 < R2; ++k2) {
+    cl::static_for<0, R2>([&](auto k2c) {
+        constexpr int k2 = decltype(k2c)::value;
         pk t[R1];
 #pragma unroll
         for (int n1 = 0; n1 < R1; ++n1) t[n1] = y[n1 + R1 * k2];
-        dft<R1, DIR>(t);
+        if constexpr (MCI_PK_FUSED) dftw<R1, (64 / R) * k2, DIR>(t);  // twiddles w^{n1 k2} fused
+        else dft<R1, DIR>(t);
 #pragma unroll
         for (int k1 = 0; k1 < R1; ++k1) x[k2 + R2 * k1] = t[k1];
-    }
+    });
 }
 
 // In-register DFT of size R (natural order in/out).
@@ -212,18 +271,19 @@ template <int R1, int R2, int DIR, unsigned long long Z> __device__ __forceinlin
         dftz<R2, DIR, zm>(t);
         cl::static_for<0, R2>([&](auto k2c) {
             constexpr int k2 = decltype(k2c)::value;
-            y[n1 + R1 * k2] = twc<R, n1 * k2, DIR>(t[k2]);
+            y[n1 + R1 * k2] = MCI_PK_FUSED ? t[k2] : twc<R, n1 * k2, DIR>(t[k2]);
         });
     });
-#pragma unroll
-    for (int k2 = 0; k2 < R2; ++k2) {
+    cl::static_for<0, R2>([&](auto k2c) {
+        constexpr int k2 = decltype(k2c)::value;
         pk t[R1];
 #pragma unroll
         for (int n1 = 0; n1 < R1; ++n1) t[n1] = y[n1 + R1 * k2];
-        dft<R1, DIR>(t);
+        if constexpr (MCI_PK_FUSED) dftw<R1, (64 / R) * k2, DIR>(t);
+        else dft<R1, DIR>(t);
 #pragma unroll
         for (int k1 = 0; k1 < R1; ++k1) x[k2 + R2 * k1] = t[k1];
-    }
+    });
 }
 
 template <int R, int DIR, unsigned long long Z> __device__ __forceinline__ void dftz(pk *x) {

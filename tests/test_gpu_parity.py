@@ -405,7 +405,9 @@ def test_cfg5_transposed_workspace(ws_mb, streams, monkeypatch):
     MCI_2D_TSTORE=0: column first with a strided workspace; MCI_LINE_G16=0: the tiled
     gather by 4-byte transposing copies instead of 16-byte copies into a swizzled stage;
     MCI_LINE_CT8=1: the column pass as two 8-warp CTAs per SM with 8-line tiles (same
-    per-line arithmetic: bit-identical).  MCI_2D_ORDER=1: row pass first on contiguous input lines, storing
+    per-line arithmetic: bit-identical); MCI_LINE_TMA=0: the default tile gather by
+    tensor-map box loads (cp.async.bulk.tensor, 64-byte swizzle) replaced by the 16-byte
+    cp.async gather into the same swizzled layout (bit-identical).  MCI_2D_ORDER=1: row pass first on contiguous input lines, storing
     ws[img][my][px][ny], then the column pass on contiguous lines storing the image
     transposed: the other pass order (order-independent), equal to fp32
     rounding.  24 MB chunks put 3 images per workspace fill over 5 images (ragged last chunk);
@@ -420,8 +422,8 @@ def test_cfg5_transposed_workspace(ws_mb, streams, monkeypatch):
     gt = torch.from_numpy(g).cuda()
     outs = []
     for env in ({}, {"MCI_2D_ORDER": "1"}, {"MCI_2D_TSTORE": "0"}, {"MCI_LINE_G16": "0"},
-                {"MCI_2D_TSTORE": "0", "MCI_LINE_G16": "0"}, {"MCI_LINE_CT8": "1"}):
-        for k in ("MCI_2D_ORDER", "MCI_2D_TSTORE", "MCI_LINE_G16", "MCI_LINE_CT8"):
+                {"MCI_2D_TSTORE": "0", "MCI_LINE_G16": "0"}, {"MCI_LINE_CT8": "1"}, {"MCI_LINE_TMA": "0"}):
+        for k in ("MCI_2D_ORDER", "MCI_2D_TSTORE", "MCI_LINE_G16", "MCI_LINE_CT8", "MCI_LINE_TMA"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
