@@ -43,6 +43,8 @@ struct Axis1D {
     const void *rowtab = nullptr;  // tables of the specialised row kernel (mci_row.cu), or null
     int bank_deriv012 = 0;         // bank is exactly (1, ik, -k^2): closed-form inverse available
     int bank_deriv01 = 0;          // bank is exactly (1, ik): closed-form inverse available
+    int bank_derivM = 0;           // bank is exactly (ik)^m, m = 0..M-1: Vandermonde closed form (mci_rowg.cu)
+    int rowg = 0;                  // special == 1 served by the row-kernel family (mci_rowg.cu)
     int bank_delay_uniform = 0;    // bank is e^{ik 2 pi m/(MN)}, m < M = 4: H = W diag(e^{ij tau_m}) (closed form)
     int row_variant = 0;  // row kernel: 0 = 3 groups (default), 2 = 2 groups, 1 = 2 groups + 2-warp forward (MCI_ROW_VARIANT)
     int special = 0;  // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu), 3 Hilbert (mci_hilbert.cu),
@@ -76,6 +78,8 @@ size_t fused_smem_bytes(const Axis1D &ax);
 bool fused_supported(const Axis1D &ax);
 
 bool row_supported(const Axis1D &ax);
+bool rowg_supported(const Axis1D &ax);
+cudaError_t launch_rowg(const Axis1D &ax, int64_t rows, const void *g, void *f, cudaStream_t st, int *n_launches);
 bool line_supported(const Axis1D &ax);
 bool hilbert_supported(const Axis1D &ax);
 cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *f, void *hf, cudaStream_t st,

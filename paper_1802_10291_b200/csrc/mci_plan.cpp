@@ -217,20 +217,42 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
     push_roots(blob, L, ax.LO, 1, +1);
     if (!fourstep && !getenv("MCI_DISABLE_ROW") && std::is_same<T, float>::value) {
         ax.dtype = MCI_F32;
-        if (mci::row_supported(ax)) {
+        if (mci::row_supported(ax) || mci::rowg_supported(ax)) {
             // Example 2 bank (f, f', f'') with no null bins: the row kernel evaluates the
             // paper's closed-form H^{-1} instead of reading the table
             ax.bank_deriv012 = (M == 3 && n_null == 0 && sys[0].kind == MCI_SYS_IDENTITY &&
                                 sys[1].kind == MCI_SYS_DERIVATIVE && sys[1].order == 1 &&
                                 sys[2].kind == MCI_SYS_DERIVATIVE && sys[2].order == 2 && !getenv("MCI_ROW_QTAB"))
                                    ? 1 : 0;
-            // specialised row kernel tables: [wp: K+1][fw2: 32x32][itw: 64x64][fw3: 16x64][fw8: 8x8]
+            // derivative bank (ik)^m, m < M (the row-kernel family's Vandermonde closed form)
+            bool dm = n_null == 0 && !getenv("MCI_ROW_QTAB") && sys[0].kind == MCI_SYS_IDENTITY;
+            for (int m = 1; dm && m < M; ++m) dm = sys[m].kind == MCI_SYS_DERIVATIVE && sys[m].order == m;
+            ax.bank_derivM = dm ? 1 : 0;
+            // the config-2 shape runs the tuned kernel (mci_row.cu); the other shapes run the
+            // family kernel (mci_rowg.cu).  A/B: MCI_ROWG=1 runs the family kernel on the config-2
+            // shape too, MCI_ROWG=2 in addition with the generic derivative-bank solve
+            const int fam = getenv("MCI_ROWG") ? atoi(getenv("MCI_ROWG")) : 0;
+            ax.rowg = !mci::row_supported(ax) || fam >= 1;
+            if (fam == 2 && ax.bank_derivM) ax.bank_deriv012 = 0;
+            // row kernel tables: [wp: K+1][fw2: 32x32][itw: 64x64][fw3: 16x64][fw8: 8x8]
+            // + family: [tw256: 16x16][tw2k: 2048][ainv: M x M reals, padded to an even count]
             offs.push_back(blob.size());
             push_roots(blob, L, K + 1, 1, +1);
             for (int j = 0; j < 32; ++j) push_roots(blob, 1024, 32, j, -1);
             for (int j = 0; j < 64; ++j) push_roots(blob, 4096, 64, j, +1);
             for (int j = 0; j < 16; ++j) push_roots(blob, 1024, 64, j, -1);
             for (int j = 0; j < 8; ++j) push_roots(blob, 64, 8, j, -1);
+            for (int j = 0; j < 16; ++j) push_roots(blob, 256, 16, j, -1);
+            push_roots(blob, 2048, 2048, 1, -1);
+            {  // W[r][l] = (l N)^r; v = W^{-1} f, stored as ainv[l M + r] = (W^{-1})[l][r] / N
+                std::vector<cd> W(M * M), Wi;
+                for (int r = 0; r < M; ++r)
+                    for (int l = 0; l < M; ++l) W[r * M + l] = std::pow((double)l * (double)N, (double)r);
+                if (!lu_inverse(M, W, Wi, 0.0)) return MCI_E_ARG;
+                for (int l = 0; l < M; ++l)
+                    for (int r = 0; r < M; ++r) blob.push_back((T)(Wi[l * M + r].real() / (double)N));
+                if ((M * M) & 1) blob.push_back((T)0);
+            }
             ax.row_variant = getenv("MCI_ROW_VARIANT") ? atoi(getenv("MCI_ROW_VARIANT")) : 0;
             ax.special = 1;
         } else if (mci::line_supported(ax)) {
@@ -677,7 +699,8 @@ cudaError_t launch_axis(const Axis1D &ax, const RowAddr &ra, int64_t rows, const
     if (ax.special == 4) return launch_anylen(ax, ra, rows, g, f, hf, st, nl);
     const bool dense = ra.D0 == 1 && ra.D1 == 1 && ra.ss == 1 && ra.cs == ax.N && ra.s2 == ax.M * ax.N;
     const bool al = aligned16(g) && aligned16(f) && (!hf || aligned16(hf));
-    if (ax.special == 1 && dense && al) return launch_row(ax, ax.rowtab, rows, g, f, st, nl);
+    if (ax.special == 1 && dense && al)
+        return ax.rowg ? launch_rowg(ax, rows, g, f, st, nl) : launch_row(ax, ax.rowtab, rows, g, f, st, nl);
     if (ax.special == 2) return launch_line(ax, ra, rows, g, f, st, nl);  // checks its own alignment
     if (ax.special == 3 && dense && al) return launch_hilbert(ax, rows, g, f, hf, st, nl);
     return launch_fused(ax, ra, rows, g, f, hf, st, nl);

@@ -171,6 +171,14 @@ CONFIGS = {
     # SURVEY.md §8(f) NEXT-4 measurement line: eps(f, N) of 16,384 spectra on 4x the config-2 band
     9: dict(M=3, N=1024, L=16384, batch=16384, nfreq=4 * 3 * 1024,
             bank=[("identity",), ("derivative", 1), ("derivative", 2)], dtype="f32"),
+    # off-benchmark shapes (speed beyond the five benchmark shapes), same
+    # generator and about the HBM bytes per step of config 2: two channels (f, f') of N = 2048
+    # samples, and four derivative channels (f and its first three derivatives) of N = 1024
+    # (MN = 4096 -> L = 16384 = 4 x 4096: the row-kernel family, mci_rowg.cu)
+    10: dict(M=2, N=2048, L=16384, batch=65536,
+             bank=[("identity",), ("derivative", 1)], dtype="f32"),
+    11: dict(M=4, N=1024, L=16384, batch=65536,
+             bank=[("identity",), ("derivative", 1), ("derivative", 2), ("derivative", 3)], dtype="f32"),
 }
 
 

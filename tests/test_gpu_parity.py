@@ -894,3 +894,58 @@ def test_boundary_rejects_wrong_plans_and_buffers():
     f3m, h3m = h.execute(raw3[2:].view(g3.shape))
     assert row_rel(f3m.double().cpu().numpy(), f3.double().cpu().numpy()).max() < F32_TOL
     assert row_rel(h3m.double().cpu().numpy(), h3.double().cpu().numpy()).max() < F32_TOL
+
+
+# -------------------------------------------------------------------------- row-kernel family
+# mci_rowg.cu: the config-2 kernel's layout for the other S = 4096, R = 4 shapes (L = 16384,
+# 2048 < MN <= 4096), VERDICT r01 item 10.  Banks: the derivative bank (ik)^m (Vandermonde
+# closed form), a delay bank and an arbitrary table bank (Q~ table path).
+def _family_bank(kind, M, N):
+    if kind == "deriv":
+        return [("identity",)] + [("derivative", m) for m in range(1, M)]
+    if kind == "delay":
+        return [("delay", 0.37 * m * 2 * math.pi / (M * N)) for m in range(M)]
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("M,N,kind,rows", [
+    (4, 1024, "deriv", 301), (4, 1024, "deriv", 1), (4, 1024, "delay", 37),
+    (2, 2048, "deriv", 301), (2, 2048, "deriv", 2), (2, 2048, "delay", 37)])
+def test_row_family_vs_oracle(M, N, kind, rows):
+    """Row-kernel family (mci_rowg.cu) vs the fp64 oracle on bandlimited and non-bandlimited
+    rows (the edge bins +-K = +-S/2 meet at k' = S/2 for MN = 4096), ragged batches; a row
+    computed alone gives the same bits."""
+    m = mci()
+    L = 16384
+    bank = _family_bank(kind, M, N)
+    g = synth.cfg2_batch_fast(rows, seed=M * N + rows, M=M, N=N, bank=bank)
+    if rows > 1:
+        g[::2] = np.random.default_rng(9).standard_normal(g[::2].shape).astype(np.float32) * \
+            g[::2].std(axis=2, keepdims=True)
+    plan = m.Plan(M, N, L, bank)
+    out = run_plan(plan, g)
+    P = oracle.OraclePlan(M, N, L, bank)
+    pick = sorted({0, rows // 2, rows - 1} | ({1} if rows > 1 else set()))
+    assert row_rel(out[pick], P.eval(g[pick])).max() < F32_TOL
+    one = run_plan(plan, g[-1:])
+    assert np.array_equal(one[0], out[-1])
+
+
+@pytest.mark.parametrize("env", [{"MCI_ROWG": "1"}, {"MCI_ROWG": "2"}, {"MCI_ROWG": "1", "MCI_ROW_QTAB": "1"}])
+def test_row_family_config2_shape(env, monkeypatch):
+    """The family kernel on the config-2 shape: Example 2 closed form (MCI_ROWG=1), the
+    generic derivative-bank solve (MCI_ROWG=2) and the Q~ table (MCI_ROW_QTAB=1), each vs
+    the oracle and vs the tuned config-2 kernel (mci_row.cu)."""
+    m = mci()
+    c = synth.CONFIGS[2]
+    g = synth.cfg2_rows(np.arange(299))
+    g[1::3] = np.random.default_rng(3).standard_normal(g[1::3].shape).astype(np.float32) * \
+        g[1::3].std(axis=2, keepdims=True)
+    ref_gpu = run_plan(m.Plan(3, 1024, 16384, c["bank"]), g)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    out = run_plan(m.Plan(3, 1024, 16384, c["bank"]), g)
+    P = oracle.OraclePlan(3, 1024, 16384, c["bank"])
+    pick = [0, 1, 150, 298]
+    assert row_rel(out[pick], P.eval(g[pick])).max() < F32_TOL
+    assert row_rel(out, ref_gpu).max() < F32_TOL
