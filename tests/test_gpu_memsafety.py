@@ -80,7 +80,8 @@ def run_checked(call, inputs, out_specs):
 def with_env(monkeypatch, env):
     for k in ("MCI_ROW_VARIANT", "MCI_ROW_QTAB", "MCI_HILBERT_VARIANT", "MCI_DISABLE_ROW", "MCI_LINE_PF",
               "MCI_LINE_VARIANT", "MCI_LINE_TMA", "MCI_LINE_G16", "MCI_LINE_CT8", "MCI_2D_TSTORE", "MCI_2D_ORDER",
-              "MCI_2D_STREAMS", "MCI_2D_WS_MB", "MCI_FS_WS_MB", "MCI_FOURSTEP_GENERIC", "MCI_FORCE_ANYLEN"):
+              "MCI_2D_STREAMS", "MCI_2D_WS_MB", "MCI_FS_WS_MB", "MCI_FOURSTEP_GENERIC", "MCI_FORCE_ANYLEN",
+              "MCI_ROWG"):
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
@@ -95,6 +96,13 @@ CASES_1D = [
     *[(f"row_v{v}_q{q}", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROW_VARIANT": str(v), "MCI_ROW_QTAB": str(q)})
       for v in range(9) for q in (0, 1)],
     ("row_generic", 3, 1024, 16384, FDD, {}, 5, {"MCI_DISABLE_ROW": "1"}),
+    ("rowg_3_1024_ex2", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROWG": "1"}),
+    ("rowg_3_1024_deriv", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROWG": "2"}),
+    ("rowg_3_1024_table", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROWG": "1", "MCI_ROW_QTAB": "1"}),
+    ("rowg_4_1024_deriv", 4, 1024, 16384, FDD + [("derivative", 3)], {}, 7, {}),
+    ("rowg_4_1024_delay", 4, 1024, 16384, [("delay", 0.001 * m) for m in range(4)], {}, 7, {}),
+    ("rowg_2_2048_deriv", 2, 2048, 16384, FD, {}, 7, {}),
+    ("rowg_2_2048_delay", 2, 2048, 16384, [("delay", 0.0), ("delay", 0.0007)], {}, 7, {}),
     ("hilbert_store_wg", 2, 4096, 65536, FD, {"hilbert": True}, 3, {}),
     ("hilbert_direct", 2, 4096, 65536, FD, {"hilbert": True}, 3, {"MCI_HILBERT_VARIANT": "1"}),
     ("fused_f32", 2, 64, 1024, FD, {}, 9, {}),
