@@ -22,6 +22,7 @@
 // when its working set is small, else a 256-thread CTA does.
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "mci_fft.cuh"
 #include "mci_internal.h"
@@ -686,16 +687,20 @@ cudaError_t launch_anylen_residual(const Axis1D &ax, const RowAddr &ra, int64_t 
 
 // eps(f, N) of a batch of spectra (Theorem error, Eq. averageerror / errorestimate).
 // The weight of a band-external coefficient n,
-//   wt(n) = (1 + sum_l |sum_m r_m(j + lN) b_m(n)|^2,  sum_m |b_m(n)|^2),  in-band n: (-1, 0),
-// depends on n only.  Execute never allocates (include/mci.h), so no table is shared across
-// the batch: each CTA owns AE_SPEC spectra and walks the frequency axis in chunks of AE_FC,
-// computing the chunk's weights into shared memory once and streaming its spectra's chunk
-// through them (fp64 partial sums in shared memory, fixed order: deterministic).  The
-// weights are recomputed once per CTA (batch / AE_SPEC times in all), a few per cent of
-// the step for config 9; the spectra stream from HBM exactly once.
-constexpr int AE_FC = 1024;   // frequencies per chunk (16 KB of fp64 weights)
-constexpr int AE_SPEC = 64;   // spectra per CTA
-constexpr int AE_THREADS = 256;
+// Averaged error eps(f, N) (Eq. averageerror) with its bound (Eq.
+// errorestimate, reading R12) and the out-of-band energy, per spectrum a(k_lo .. k_lo + nf - 1).
+// The weight of an out-of-band coefficient, 1 + sum_l |sum_m r_m(n + (l-k)N) b_m(n)|^2, and
+// sum_m |b_m(n)|^2 depend on n only.  Execute never allocates (include/mci.h), so the weights
+// live in shared memory: persistent CTAs (one per SM) compute the table for the whole
+// frequency range once (weights in the plan's precision: 8 B per frequency in fp32, 16 B in
+// fp64; up to AE_CAP frequencies), then stream their spectra through it, one warp per spectrum,
+// the in-band run [K1, K1 + MN) skipped whole (those coefficients carry no error).  Longer
+// frequency ranges are walked in chunks of AE_CAP, the chunk's weights recomputed per group of
+// a CTA's spectra (partial sums in shared memory).  Sums are fp64 in a fixed order:
+// deterministic.  The spectra stream from HBM exactly once.
+constexpr int AE_THREADS = 1024;
+constexpr int AE_SMEM = 200 * 1024;           // weight table bytes per CTA
+constexpr int AE_GROUP = 256;                 // spectra per partial-sum group (chunked mode)
 
 __device__ __forceinline__ double2 avg_error_weight(int64_t n, int M, int N, int64_t K1, const void *Qv, bool q64,
                                                     const AnyErrSys &sy) {
@@ -732,56 +737,108 @@ __device__ __forceinline__ double2 avg_error_weight(int64_t n, int M, int N, int
     return make_double2(1.0 + w, bsum);
 }
 
+// weight entry in the table's precision
+template <typename T> struct AEW { using type = float2; };
+template <> struct AEW<double> { using type = double2; };
+
 template <typename T>
-__global__ void __launch_bounds__(AE_THREADS) mci_avg_error_kernel(const cv<T> *__restrict__ spec, int nf,
-                                                                    int64_t batch, int64_t k_lo, int M, int N,
-                                                                    int64_t K1, const void *Qv, bool q64,
-                                                                    AnyErrSys sy, double omega_sum,
-                                                                    T *__restrict__ out) {
-    __shared__ double2 wt[AE_FC];
-    __shared__ double acc[AE_SPEC][3];  // (e2, oob, cs) per spectrum of this CTA
+__global__ void __launch_bounds__(AE_THREADS, 1) mci_avg_error_kernel(const cv<T> *__restrict__ spec, int nf,
+                                                                       int64_t batch, int64_t k_lo, int M, int N,
+                                                                       int64_t K1, const void *Qv, bool q64,
+                                                                       AnyErrSys sy, double omega_sum,
+                                                                       T *__restrict__ out) {
+    using W = typename AEW<T>::type;
+    constexpr int CAP = AE_SMEM / sizeof(W);
+    extern __shared__ __align__(16) unsigned char ae_smem[];
+    W *wt = reinterpret_cast<W *>(ae_smem);
+    __shared__ double acc[AE_GROUP][3];  // chunked mode: (e2, oob, cs) per spectrum of the group
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NW = AE_THREADS / 32;
-    const int64_t s0 = (int64_t)blockIdx.x * AE_SPEC;
-    const int ns = batch - s0 < AE_SPEC ? (int)(batch - s0) : AE_SPEC;
-    for (int i = threadIdx.x; i < AE_SPEC * 3; i += AE_THREADS) (&acc[0][0])[i] = 0.0;
-    for (int c0 = 0; c0 < nf; c0 += AE_FC) {
-        const int nc = min(AE_FC, nf - c0);
-        __syncthreads();  // previous chunk's weights consumed (and acc zeroed on the first pass)
-        for (int i = threadIdx.x; i < nc; i += AE_THREADS)
-            wt[i] = avg_error_weight(k_lo + c0 + i, M, N, K1, Qv, q64, sy);
-        __syncthreads();
-        for (int s = warp; s < ns; s += NW) {  // warp s % NW owns spectrum s: no races on acc[s]
-            const cv<T> *a = spec + (s0 + s) * (int64_t)nf + c0;
-            double e2 = 0, oob = 0, cs = 0;
-            for (int i = lane; i < nc; i += 32) {
-                const double2 w = wt[i];
-                if (w.x < 0.0) continue;  // in-band coefficient: not read
-                const cv<T> an = a[i];
-                const double a2 = (double)an.x * an.x + (double)an.y * an.y;
-                e2 += a2 * w.x;
-                oob += a2;
-                cs += a2 * w.y;
+    const int64_t MN = (int64_t)M * N;
+    const bool one = nf <= CAP;  // whole range resident: weights once, then stream
+    // spectra of this CTA: s = blockIdx.x + i gridDim.x; groups of AE_GROUP in chunked mode
+    const int64_t mine = batch > blockIdx.x ? (batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t gsz = one ? mine : AE_GROUP;
+    for (int64_t g0 = 0; g0 < mine; g0 += gsz) {
+        const int64_t ng = mine - g0 < gsz ? mine - g0 : gsz;
+        if (!one) {
+            __syncthreads();  // previous group's sums written out
+            for (int i = threadIdx.x; i < AE_GROUP * 3; i += AE_THREADS) (&acc[0][0])[i] = 0.0;
+        }
+        for (int c0 = 0; c0 < nf; c0 += CAP) {
+            const int nc = min(CAP, nf - c0);
+            if (!one || g0 == 0) {
+                __syncthreads();  // previous chunk's weights consumed
+                for (int i = threadIdx.x; i < nc; i += AE_THREADS) {
+                    const double2 w = avg_error_weight(k_lo + c0 + i, M, N, K1, Qv, q64, sy);
+                    wt[i] = W{(decltype(W::x))w.x, (decltype(W::x))w.y};
+                }
+                __syncthreads();
             }
-            for (int o = 16; o; o >>= 1) {
-                e2 += __shfl_xor_sync(0xffffffffu, e2, o);
-                oob += __shfl_xor_sync(0xffffffffu, oob, o);
-                cs += __shfl_xor_sync(0xffffffffu, cs, o);
-            }
-            if (lane == 0) {
-                acc[s][0] += e2;
-                acc[s][1] += oob;
-                acc[s][2] += cs;
+            // in-band run of this chunk, [ib0, ib1) (chunk-relative), skipped whole
+            const int64_t lo = K1 - (k_lo + c0), hi = lo + MN;
+            auto clampc = [&](int64_t x) { return (int)(x < 0 ? 0 : x > nc ? nc : x); };
+            const int ib0 = clampc(lo), ib1 = clampc(hi);
+            for (int64_t si = warp; si < ng; si += NW) {  // one warp per spectrum
+                const int64_t sp = blockIdx.x + (g0 + si) * gridDim.x;
+                const cv<T> *a = spec + sp * (int64_t)nf + c0;
+                double e2 = 0, oob = 0, cs = 0;
+                auto run = [&](int b0, int b1) {
+                    int i = b0 + lane;
+                    for (; i + 96 < b1; i += 128) {  // four independent loads in flight per lane
+                        cv<T> av[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) av[u] = a[i + 32 * u];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const W w = wt[i + 32 * u];
+                            const double a2 = (double)av[u].x * av[u].x + (double)av[u].y * av[u].y;
+                            e2 += a2 * (double)w.x;
+                            oob += a2;
+                            cs += a2 * (double)w.y;
+                        }
+                    }
+                    for (; i < b1; i += 32) {
+                        const cv<T> an = a[i];
+                        const W w = wt[i];
+                        const double a2 = (double)an.x * an.x + (double)an.y * an.y;
+                        e2 += a2 * (double)w.x;
+                        oob += a2;
+                        cs += a2 * (double)w.y;
+                    }
+                };
+                run(0, ib0);
+                run(ib1, nc);
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    e2 += __shfl_xor_sync(0xffffffffu, e2, o);
+                    oob += __shfl_xor_sync(0xffffffffu, oob, o);
+                    cs += __shfl_xor_sync(0xffffffffu, cs, o);
+                }
+                if (one) {
+                    if (lane == 0) {
+                        T *o = out + sp * 3;
+                        o[0] = (T)sqrt(e2);
+                        o[1] = (T)sqrt(oob + M * omega_sum * cs);
+                        o[2] = (T)oob;
+                    }
+                } else if (lane == 0) {
+                    acc[si][0] += e2;
+                    acc[si][1] += oob;
+                    acc[si][2] += cs;
+                }
             }
         }
-    }
-    __syncthreads();
-    for (int s = threadIdx.x; s < ns; s += AE_THREADS) {
-        const double e2 = acc[s][0], oob = acc[s][1], cs = acc[s][2];
-        T *o = out + (s0 + s) * 3;
-        o[0] = (T)sqrt(e2);
-        o[1] = (T)sqrt(oob + M * omega_sum * cs);
-        o[2] = (T)oob;
+        if (!one) {
+            __syncthreads();
+            for (int si = threadIdx.x; si < ng; si += AE_THREADS) {
+                const double e2 = acc[si][0], oob = acc[si][1], cs = acc[si][2];
+                T *o = out + (blockIdx.x + (g0 + si) * gridDim.x) * 3;
+                o[0] = (T)sqrt(e2);
+                o[1] = (T)sqrt(oob + M * omega_sum * cs);
+                o[2] = (T)oob;
+            }
+        }
     }
 }
 
@@ -790,16 +847,24 @@ cudaError_t launch_averaged_error(const Axis1D &ax, int64_t batch, const void *s
     if (batch <= 0) return cudaSuccess;
     AnyErrSys sy;
     for (int m = 0; m < 8; ++m) sy.s[m] = ax.sys[m];
-    const int64_t grid = (batch + AE_SPEC - 1) / AE_SPEC;
-    if (grid > 0x7fffffff) return cudaErrorInvalidValue;
-    if (ax.dtype == MCI_F64)
-        mci_avg_error_kernel<double><<<(unsigned)grid, AE_THREADS, 0, st>>>(
-            (const cv<double> *)spec, (int)n_freq, batch, k_lo, ax.M, (int)ax.N, ax.K1, ax.Qt, true, sy,
-            ax.omega_sum, (double *)out);
-    else
-        mci_avg_error_kernel<float><<<(unsigned)grid, AE_THREADS, 0, st>>>(
-            (const cv<float> *)spec, (int)n_freq, batch, k_lo, ax.M, (int)ax.N, ax.K1, ax.Qt, false, sy,
-            ax.omega_sum, (float *)out);
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = std::min<int64_t>(nsm, batch);  // persistent: one CTA per SM
+    if (const char *e = getenv("MCI_AE_GRID")) grid = std::max<int64_t>(1, std::min<int64_t>(atoi(e), batch));  // tests
+    if (ax.dtype == MCI_F64) {
+        auto k = mci_avg_error_kernel<double>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, AE_SMEM) != cudaSuccess)
+            return cudaErrorInvalidValue;
+        k<<<(unsigned)grid, AE_THREADS, AE_SMEM, st>>>((const cv<double> *)spec, (int)n_freq, batch, k_lo, ax.M,
+                                                       (int)ax.N, ax.K1, ax.Qt, true, sy, ax.omega_sum, (double *)out);
+    } else {
+        auto k = mci_avg_error_kernel<float>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, AE_SMEM) != cudaSuccess)
+            return cudaErrorInvalidValue;
+        k<<<(unsigned)grid, AE_THREADS, AE_SMEM, st>>>((const cv<float> *)spec, (int)n_freq, batch, k_lo, ax.M,
+                                                       (int)ax.N, ax.K1, ax.Qt, false, sy, ax.omega_sum, (float *)out);
+    }
     return cudaGetLastError();
 }
 

@@ -824,6 +824,29 @@ def test_cfg9_full_batch_sampled():
         assert np.max(np.abs(out[i] - ref) / ref) < F32_TOL
 
 
+@pytest.mark.parametrize("dtype,nf,grid", [("f64", 13000, "2"), ("f32", 26000, "2"), ("f64", 3000, "3")])
+def test_averaged_error_chunked_and_grouped(dtype, nf, grid, monkeypatch):
+    """The averaged-error kernel's chunked mode (frequency range beyond the shared-memory weight
+    table: 12,800 entries in fp64, 25,600 in fp32) and its spectrum groups (a forced 2- or 3-CTA
+    grid gives each CTA several groups of 256 spectra), vs the oracle."""
+    m = mci()
+    monkeypatch.setenv("MCI_AE_GRID", grid)
+    cdt = np.complex128 if dtype == "f64" else np.complex64
+    rng = np.random.default_rng(nf)
+    batch = 600
+    k_lo = -nf // 2
+    kk = np.arange(k_lo, k_lo + nf)
+    spec = ((rng.standard_normal((batch, nf)) + 1j * rng.standard_normal((batch, nf))) /
+            (1 + np.abs(kk) / 64.0)).astype(cdt)
+    plan = m.Plan(3, 64, 256, BANKS["f_df_ddf"], dtype=dtype, analysis=True)
+    out = plan.averaged_error(torch.from_numpy(spec).cuda(), k_lo).double().cpu().numpy()
+    P = oracle.OraclePlan(3, 64, 256, BANKS["f_df_ddf"])
+    tol = 1e-11 if dtype == "f64" else F32_TOL
+    for i in (0, 1, 299, batch - 1):
+        ref = np.array(oracle.averaged_error(P, spec[i].astype(np.complex128), k_lo))
+        assert np.max(np.abs(out[i] - ref) / ref) < tol
+
+
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_averaged_error_hand_values(dtype):
     """The hand-worked values of pin P13 (tests/test_oracle_pins.py::test_p13_bound_closed_forms)
