@@ -20,8 +20,12 @@
 //   * 4 rounds of 8 consecutive phases p1 = 8 r + c: lanes c = lane & 7 run phase c on
 //     butterfly tid >> 3, so every warp store writes 4 whole 32-byte sectors of f (and of Hf);
 //     pass 1 radix 64 with the pre-twiddle fused into its loads, pass 2 radix 32 x 2.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdint>
 #include <cstdlib>
+#include <cstring>
 
 #include "mci_internal.h"
 #include "mci_pk.cuh"
@@ -86,16 +90,23 @@ struct HilbertTables {
     int deriv;          // 1: bank is (1, ik) -> closed-form inverse
 };
 
-// STW: a fourth... (ninth to twelfth) warp set -- a store warpgroup -- takes each round's 64 outputs
-// per thread out of tensor memory (lane = compute thread, 128 columns per compute warpgroup,
-// double-buffered by round) and writes them with the compute threads' sector-aligned pattern,
-// so the output stores never stall the transform.
-template <bool STW>
-__global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
+// MODE 1 (STW): a fourth... (ninth to twelfth) warp set -- a store warpgroup -- takes each round's 64
+// outputs per thread out of tensor memory (lane = compute thread, 128 columns per compute
+// warpgroup, double-buffered by round) and writes them with the compute threads' sector-aligned
+// pattern, so the output stores never stall the transform.
+// MODE 2 (TS): after pass 2 the compute threads write the round's outputs into a staging tile
+// [p2][8 phases] (f and Hf planes, 128 KB) laid over the phase buffers, and one thread stores it
+// with TMA tensor stores (cp.async.bulk.tensor, boxes of 256 p2 x 8 phases = 32-byte runs at a
+// 128-byte pitch): the 4,096 sector-scattered 32-bit global stores per row leave the LSU pipe.
+// MODE 0: the compute threads store directly.
+template <int MODE>
+__global__ void __launch_bounds__(hilk::NT + (MODE == 1 ? 128 : 0), 1)
     mci_hilbert_kernel(const float *__restrict__ g, float *__restrict__ f, float *__restrict__ hf, int64_t rows,
-                       HilbertTables tb) {
+                       HilbertTables tb, const __grid_constant__ CUtensorMap tmf,
+                       const __grid_constant__ CUtensorMap tmh) {
     using namespace hilk;
     using namespace pkx;
+    constexpr bool STW = MODE == 1, TS = MODE == 2;
     extern __shared__ __align__(16) unsigned char smem[];
     float2 *Z = reinterpret_cast<float2 *>(smem);  // [ZLEN]
     float2 *bufs = Z + ZLEN;                        // NBUF x BUF; the forward aliases bufs[0 .. 4352)
@@ -112,6 +123,9 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
     // (forward pass-2 twiddles; stride j across lanes: up to 8-way)
     float2 *u32 = w16 + 16;
     float2 *t16 = u32 + 32;
+    // TS: staging planes [2048 p2][8 phases] of f and Hf, 128-byte aligned, over the phase buffers
+    float *Sf = reinterpret_cast<float *>(((uintptr_t)bufs + 127) & ~(uintptr_t)127);
+    float *Sh = Sf + 2048 * 8;
     __shared__ __align__(8) uint64_t mbar;
     __shared__ float smx[8][2];
     __shared__ float ssc[2];
@@ -211,6 +225,7 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
                 smx[warp][0] = m0;
                 smx[warp][1] = m1;
             }
+            if (TS && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             bar();  // maxima visible; previous row's last reads of the buffers are complete
             if (tid == 0 && row + gridDim.x < rows) {  // stage consumed: fetch the next row
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -317,6 +332,8 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
                 }
             }
             dft<64, 1>(x);
+            // TS: the previous round's staging tile has been read by its TMA stores
+            if (TS && tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             bar();  // previous round's pass-2 loads are complete before the buffers are rewritten
 #pragma unroll
             for (int j = 0; j < 64; ++j) buf[pad6(64 * bt + j)] = f2(x[j]);
@@ -329,6 +346,44 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
             if (STW) {  // the store warpgroup has drained this TMEM buffer (two rounds ago)
                 stage_wait(&tempty[rcc & 1], ((rcc >> 1) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            if constexpr (TS) {
+                pk y[2][32];
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) y[hh][j] = mk(buf[pad6(bt + 32 * hh + 64 * j)]);
+                bar();  // every pass-2 load done: the staging tile may overwrite the buffers
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const int t = bt + 32 * hh;
+#pragma unroll
+                    for (int j = 1; j < 32; ++j) y[hh][j] = pkx::cmul(y[hh][j], mk(itw[j * ITW_LD + t]));
+                    dft<32, 1>(y[hh]);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {  // output p2 = t + 64 j, phase c of the round
+                        const float2 z = f2(y[hh][j]);
+                        Sf[(t + 64 * j) * 8 + c] = z.x;
+                        Sh[(t + 64 * j) * 8 + c] = z.y;
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bar();
+                if (tid == 0) {
+#pragma unroll 1
+                    for (int b = 0; b < 8; ++b) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(&tmf),
+                            "r"(8 * r), "r"(256 * b), "r"((int)row), "r"(su32(Sf + 2048 * b))
+                            : "memory");
+                        asm volatile(
+                            "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(&tmh),
+                            "r"(8 * r), "r"(256 * b), "r"((int)row), "r"(su32(Sh + 2048 * b))
+                            : "memory");
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                continue;
             }
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
@@ -369,6 +424,7 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
             }
         }
     }
+    if (TS && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }  // compute warps
     if (STW) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -376,6 +432,27 @@ __global__ void __launch_bounds__(hilk::NT + (STW ? 128 : 0), 1)
         if (threadIdx.x < 32)
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm_base) : "memory");
     }
+}
+
+// TMA view of an output plane [rows][2048 p2][32 p1] (p = 32 p2 + p1), box 8 phases x 256 p2
+static bool encode_out_map(CUtensorMap *tm, void *base, int64_t rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn) {
+            cudaGetLastError();
+            return false;
+        }
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    }
+    const cuuint64_t dims[3] = {32, 2048, (cuuint64_t)rows};
+    const cuuint64_t strides[2] = {32 * 4, (cuuint64_t)hilk::L * 4};
+    const cuuint32_t box[3] = {8, 256, 1}, es[3] = {1, 1, 1};
+    return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
 }
 
 bool hilbert_supported(const Axis1D &ax) {
@@ -394,10 +471,16 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     tb.itw = base + 512;
     tb.deriv = ax.bank_deriv01;
     const size_t smem = (size_t)(ZLEN + NBUF * BUF + 512 + 32 * ITW_LD) * 8 + M * N * 4 + (16 + 32 + 256) * 8;
-    // MCI_HILBERT_VARIANT=1: the 8-warp layout storing directly (A/B); default: store warpgroup
+    // MCI_HILBERT_VARIANT=1: the 8-warp layout storing directly, 2: TMA tensor stores from a
+    // staging tile (A/B); default: store warpgroup
     const int variant = getenv("MCI_HILBERT_VARIANT") ? atoi(getenv("MCI_HILBERT_VARIANT")) : 0;
-    const bool stw = variant != 1;
-    auto kern = stw ? mci_hilbert_kernel<true> : mci_hilbert_kernel<false>;
+    const bool stw = variant == 0;
+    CUtensorMap tmf, tmh;
+    memset(&tmf, 0, sizeof(tmf));
+    memset(&tmh, 0, sizeof(tmh));
+    const bool ts = variant == 2 && rows < (1ll << 31) && aligned16(f) && aligned16(hf) &&
+                    encode_out_map(&tmf, f, rows) && encode_out_map(&tmh, hf, rows);
+    auto kern = stw ? mci_hilbert_kernel<1> : ts ? mci_hilbert_kernel<2> : mci_hilbert_kernel<0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int dev = 0, nsm = 148;
@@ -406,7 +489,8 @@ cudaError_t launch_hilbert(const Axis1D &ax, int64_t rows, const void *g, void *
     int64_t grid = nsm;
     if (grid > rows) grid = rows;
     if (n_launches) *n_launches += 1;
-    kern<<<(unsigned)grid, NT + (stw ? 128 : 0), smem, st>>>((const float *)g, (float *)f, (float *)hf, rows, tb);
+    kern<<<(unsigned)grid, NT + (stw ? 128 : 0), smem, st>>>((const float *)g, (float *)f, (float *)hf, rows, tb, tmf,
+                                                            tmh);
     return cudaGetLastError();
 }
 

@@ -105,6 +105,7 @@ CASES_1D = [
     ("rowg_2_2048_delay", 2, 2048, 16384, [("delay", 0.0), ("delay", 0.0007)], {}, 7, {}),
     ("hilbert_store_wg", 2, 4096, 65536, FD, {"hilbert": True}, 3, {}),
     ("hilbert_direct", 2, 4096, 65536, FD, {"hilbert": True}, 3, {"MCI_HILBERT_VARIANT": "1"}),
+    ("hilbert_tma_store", 2, 4096, 65536, FD, {"hilbert": True}, 3, {"MCI_HILBERT_VARIANT": "2"}),
     ("fused_f32", 2, 64, 1024, FD, {}, 9, {}),
     ("fused_f32_hilbert", 2, 64, 1024, FD, {"hilbert": True}, 9, {}),
     ("fused_f64", 2, 64, 1024, FD, {"dtype": "f64"}, 9, {}),

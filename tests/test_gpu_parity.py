@@ -233,11 +233,11 @@ def test_cfg3_full_batch_sampled(parity_log):
         assert (neg <= 1e-10 * tot).all().item()
 
 
-@pytest.mark.parametrize("qtab,variant", [(False, 0), (True, 0), (False, 1), (True, 1)])
+@pytest.mark.parametrize("qtab,variant", [(False, 0), (True, 0), (False, 1), (True, 1), (False, 2), (True, 2)])
 def test_hilbert_kernel_vs_oracle_and_generic(qtab, variant, monkeypatch):
     """The specialised config-3 kernel (mci_hilbert.cu; closed-form (1, ik) inverse or
     the Q table; variant 0 = store warpgroup draining the outputs from tensor memory,
-    1 = direct stores) on a batch larger than the persistent grid, with
+    1 = direct stores, 2 = TMA tensor stores of a staging tile) on a batch larger than the persistent grid, with
     non-bandlimited rows: within tolerance of the oracle (sampled rows) and of the
     generic fused kernel (all rows), and bit-for-bit independent of batch size."""
     monkeypatch.setenv("MCI_HILBERT_VARIANT", str(variant))
