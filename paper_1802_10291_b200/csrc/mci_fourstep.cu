@@ -299,19 +299,25 @@ static cudaError_t fs_launch_t(const Axis1D &ax, int64_t batch, const void *g, v
     for (int64_t s0 = 0; s0 < batch; s0 += ws_sig) {
         const int64_t ns = (batch - s0 < ws_sig) ? batch - s0 : ws_sig;
         a.sig0 = s0;
-        if ((e = cudaMemsetAsync(a.cmax, 0, sizeof(*a.cmax) * ns * a.M, st))) return e;
-        mci_fs_max<T><<<(unsigned)(ns * a.M * MX_BLK), MX_NT, 0, st>>>(a);
+        // channel maxima for the exact power-of-two scaling before channel packing (R10); a
+        // unimodular bank (|b_m(k)| = 1) gives channels of equal energy: no pre-pass, the
+        // words stay 0 (zeroed at plan creation), i.e. no scaling (reading R14)
+        const int pre = ax.bank_unimodular ? 0 : 1;
+        if (pre) {
+            if ((e = cudaMemsetAsync(a.cmax, 0, sizeof(*a.cmax) * ns * a.M, st))) return e;
+            mci_fs_max<T><<<(unsigned)(ns * a.M * MX_BLK), MX_NT, 0, st>>>(a);
+        }
         if constexpr (std::is_same<T, float>::value) {
             if (fast) {
                 if ((e = fourstep_fast_chunk(a, ns, st))) return e;
-                if (nl) *nl += 4;
+                if (nl) *nl += 3 + pre;
                 continue;
             }
         }
         fa<<<(unsigned)(ns * a.npair * (a.N2 / tn2)), FA_NT, fa_sm, st>>>(a);
         mci_fs_fb<T><<<(unsigned)(ns * (N1 / 2 + 1)), FB_NT, fb_sm, st>>>(a);
         mci_fs_ic<T><<<(unsigned)(ns * (a.S2 / IC_TU)), IC_NT, ic_sm, st>>>(a);
-        if (nl) *nl += 4;
+        if (nl) *nl += 3 + pre;
         if ((e = cudaGetLastError())) return e;
     }
     return cudaSuccess;

@@ -46,6 +46,8 @@ struct Axis1D {
     int bank_derivM = 0;           // bank is exactly (ik)^m, m = 0..M-1: Vandermonde closed form (mci_rowg.cu)
     int rowg = 0;                  // special == 1 served by the row-kernel family (mci_rowg.cu)
     int bank_delay_uniform = 0;    // bank is e^{ik 2 pi m/(MN)}, m < M = 4: H = W diag(e^{ij tau_m}) (closed form)
+    int bank_unimodular = 0;       // every |b_m(k)| = 1 (identity / delay channels): equal channel energies,
+                                   // the four-step path skips the channel-magnitude pre-pass (reading R14)
     int row_variant = 0;  // row kernel: 0 = 3 groups (default), 2 = 2 groups, 1 = 2 groups + 2-warp forward (MCI_ROW_VARIANT)
     int special = 0;  // 0 generic fused, 1 row kernel (mci_row.cu), 2 line kernel (mci_line.cu), 3 Hilbert (mci_hilbert.cu),
                       // 4 arbitrary lengths (mci_anylen.cu: Qt has all N classes, twF = e^{-2 pi i m/N} [N],

@@ -204,6 +204,9 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             du = sys[m].kind == MCI_SYS_DELAY &&
                  std::abs(sys[m].tau - 2 * PI * m / ((double)M * N)) <= 1e-12 * (1 + 2 * PI * m / ((double)M * N));
         ax.bank_delay_uniform = du ? 1 : 0;
+        bool um = !getenv("MCI_FS_CHANNEL_MAX");
+        for (int m = 0; um && m < M; ++m) um = sys[m].kind == MCI_SYS_IDENTITY || sys[m].kind == MCI_SYS_DELAY;
+        ax.bank_unimodular = um ? 1 : 0;
     }
     // ---- forward-sign root table e^{-2 pi i m/TW}
     if (fourstep) ax.TW = std::max<int64_t>({1024, N / 1024, ax.S / 1024});
@@ -545,6 +548,8 @@ mci_status create_1d(mci_plan p, int M, int64_t N, int64_t L, const mci_system *
         p->ws_units = units;
         p->ws_bytes = per * units;
         if (cudaMalloc(&p->ws, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
+        // unimodular bank: the channel-magnitude words stay 0 (no scaling), written once here
+        if (ax.bank_unimodular && cudaMemset(p->ws, 0, p->ws_bytes) != cudaSuccess) return MCI_E_CUDA;
     }
     return MCI_OK;
 }
@@ -1016,7 +1021,7 @@ int64_t mci_plan_launches(mci_plan p, int64_t batch) {
     if (p->path == mci::PATH_FUSED) return 1;
     const int64_t chunks = (batch + p->ws_units - 1) / p->ws_units;
     if (p->path == mci::PATH_SISR) return 5 * chunks;  // fd rows, MCI x, fd cols, MCI y, transpose
-    return p->path == mci::PATH_FOURSTEP ? 4 * chunks : 2 * chunks;
+    return p->path == mci::PATH_FOURSTEP ? (p->ax.bank_unimodular ? 3 : 4) * chunks : 2 * chunks;
 }
 
 const char *mci_status_str(mci_status s) {

@@ -327,16 +327,19 @@ def test_cfg4_closed_form_vs_table_vs_generic(monkeypatch):
     M, N, L = c["M"], c["N"], c["L"]
     g = np.random.default_rng(21).standard_normal((2, M, N)).astype(np.float32)
     outs = []
-    for env in ({}, {"MCI_ROW_QTAB": "1"}, {"MCI_FOURSTEP_GENERIC": "1"}):
-        for k in ("MCI_ROW_QTAB", "MCI_FOURSTEP_GENERIC"):
+    for env in ({}, {"MCI_ROW_QTAB": "1"}, {"MCI_FOURSTEP_GENERIC": "1"}, {"MCI_FS_CHANNEL_MAX": "1"}):
+        for k in ("MCI_ROW_QTAB", "MCI_FOURSTEP_GENERIC", "MCI_FS_CHANNEL_MAX"):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
         plan = m.Plan(M, N, L, c["bank"])
         assert plan.path == "fourstep"
+        # the unimodular delay bank skips the channel-magnitude pre-pass (reading R14)
+        assert plan.launches(2) == (4 if env.get("MCI_FS_CHANNEL_MAX") else 3)
         outs.append(run_plan(plan, g))
     assert row_rel(outs[0], outs[1]).max() < F32_TOL
     assert row_rel(outs[0], outs[2]).max() < F32_TOL
+    assert row_rel(outs[0], outs[3]).max() < F32_TOL
     pts = np.random.default_rng(22).integers(0, L, 48)
     ref = oracle.delay_eval_points(M, N, L, g[1], pts)
     assert np.linalg.norm(outs[0][1, pts] - ref) / np.linalg.norm(ref) < F32_TOL
