@@ -657,10 +657,10 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // (MCI_LINE_TMA=0: the 16-byte cp.async gather, A/B)
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
-    const bool tma = tstore && tiled && g16 && tm && !ct8 && !(getenv("MCI_LINE_TMA") && atoi(getenv("MCI_LINE_TMA")) == 0) &&
+    const bool tma = tiled && g16 && tm && !ct8 && !(getenv("MCI_LINE_TMA") && atoi(getenv("MCI_LINE_TMA")) == 0) &&
                      encode_tile_map(&tmap, g, ra, lines, linek::N);
     auto kern = ct8 ? mci_line_kernel<8, true, true, true, true>
-                : tma ? mci_line_kernel<16, true, true, true, true, true>
+                : tma ? (tstore ? mci_line_kernel<16, true, true, true, true, true> : mci_line_kernel<16, true, true, false, true, true>)
                 : tstore_c ? (tm ? mci_line_kernel<16, false, true, true, true> : mci_line_kernel<16, false, false, true, true>)
                 : (tstore && g16) ? (tm ? mci_line_kernel<16, true, true, true, true> : mci_line_kernel<16, true, false, true, true>)
                 : tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
