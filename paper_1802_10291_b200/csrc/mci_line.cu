@@ -116,6 +116,10 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         TMA ? (unsigned char *)(((uintptr_t)(bufs + WARPS * BUFS) + 1023) & ~(uintptr_t)1023)
             : (unsigned char *)(bufs + WARPS * BUFS));
     __shared__ __align__(8) uint64_t tbar;  // TMA: tile landed (expect_tx)
+    // TMA on the untiled prefetch path (BULK): each warp's next line arrives by two 1D bulk copies
+    // (cp.async.bulk, one per channel row) on the warp's own mbarrier instead of 8 cp.async per lane
+    constexpr bool BULK = TMA && PF && !TILED && !TST;
+    __shared__ __align__(8) uint64_t lbar[BULK ? WARPS : 1];
     if (!CT) {
         for (int i = threadIdx.x; i < NQ * 4; i += WARPS * 32) Qs[i] = tb.Qt[i];
         for (int i = threadIdx.x; i <= K; i += WARPS * 32) wps[i] = tb.wp[i];
@@ -271,6 +275,23 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     // the buffer carries the outputs, so the stage is a separate [WARPS][2N] region
     float *pstage = (TST && !TILED) ? stage + warp * 2 * N : reinterpret_cast<float *>(buf + (warp & 1));
     auto prefetch_line = [&](int64_t ln) {
+        if constexpr (BULK) {
+            if (ln < lines && lane == 0) {
+                const float *src = g + line_base((uint32_t)ln);
+                const uint32_t bar = s32(&lbar[warp]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer was read generically
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * N * 4)
+                             : "memory");
+#pragma unroll
+                for (int m = 0; m < 2; ++m)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            s32(pstage + m * N)),
+                        "l"(src + m * ra.cs), "r"(N * 4), "r"(bar)
+                        : "memory");
+            }
+            return;
+        }
         if (ln < lines) {
             const float *src = g + line_base((uint32_t)ln);
             const uint32_t d = (uint32_t)__cvta_generic_to_shared(pstage);
@@ -283,9 +304,17 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
+    uint32_t lph = 0;  // BULK: parity of the warp's line barrier
+    if constexpr (BULK) {
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&lbar[warp])) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     if constexpr (PF && !TILED) prefetch_line((int64_t)blockIdx.x * WARPS + warp);
     uint32_t tph = 0;  // TMA: parity of the tile barrier
-    if constexpr (TMA) {
+    if constexpr (TMA && TILED) {
         if (threadIdx.x == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&tbar)) : "memory");
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -340,7 +369,18 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
             __syncwarp();  // previous line's reads of buf are complete
         } else if constexpr (PF) {
             if (line >= lines) continue;
-            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            if constexpr (BULK) {
+                uint32_t done = 0;
+                while (!done)
+                    asm volatile(
+                        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                        : "=r"(done)
+                        : "r"(s32(&lbar[warp])), "r"(lph)
+                        : "memory");
+                lph ^= 1u;
+            } else {
+                asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
             __syncwarp();  // this line's rows have landed in the warp buffer
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -657,6 +697,8 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
     // (MCI_LINE_TMA=0: the 16-byte cp.async gather, A/B)
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof(tmap));
+    // untiled prefetched lines: the next line by TMA bulk copies (MCI_LINE_TMA=0: 16-byte cp.async)
+    const bool bulk = pf && !(getenv("MCI_LINE_TMA") && atoi(getenv("MCI_LINE_TMA")) == 0) && ra.cs % 4 == 0;
     const bool tma = tiled && g16 && tm && !ct8 && !(getenv("MCI_LINE_TMA") && atoi(getenv("MCI_LINE_TMA")) == 0) &&
                      encode_tile_map(&tmap, g, ra, lines, linek::N);
     auto kern = ct8 ? mci_line_kernel<8, true, true, true, true>
@@ -666,7 +708,8 @@ cudaError_t launch_line(const Axis1D &ax, const RowAddr &ra, int64_t lines, cons
                 : tstore  ? (tm ? mci_line_kernel<16, true, true, true> : mci_line_kernel<16, true, false, true>)
                 : (tiled && g16) ? (tm ? mci_line_kernel<16, true, true, false, true> : mci_line_kernel<16, true, false, false, true>)
                 : tiled ? (tm ? mci_line_kernel<16, true, true> : mci_line_kernel<16, true, false>)
-                : pf    ? (tm ? mci_line_kernel<8, false, true, false, true> : mci_line_kernel<8, false, false, false, true>)
+                : pf    ? (tm ? (bulk ? mci_line_kernel<8, false, true, false, true, true> : mci_line_kernel<8, false, true, false, true>)
+                              : mci_line_kernel<8, false, false, false, true>)
                         : (tm ? mci_line_kernel<8, false, true> : mci_line_kernel<8, false, false>);
     const size_t smem = ct8 ? (size_t)(512 + WARPS * (linek::BUF + 1)) * 8 + (size_t)2 * WARPS * linek::SP * 4
                             : (size_t)(linek::NQ * 4 + linek::K + 2 + 512 + 1024 + WARPS * linek::BUF) * 8 +
