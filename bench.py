@@ -400,6 +400,19 @@ def load_traffic(workload_name):
     return d, "dominant kernel, one launch", "profiles/ncu_traffic.json"
 
 
+def load_inst(workload_name):
+    """ncu-counted warp instructions of one step (smsp__inst_executed.sum over the step's MCI
+    launches) from profiles/ncu_traffic.json, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh).get(workload_name)
+    except Exception:
+        return None
+    if isinstance(d, dict) and d.get("inst"):
+        return {"inst": d["inst"], "source": d.get("source")}
+    return None
+
+
 def relaunch_cmd(args_list, n, port):
     """The torchrun command that runs this script on n ranks of one node (one per GPU)."""
     return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
@@ -572,6 +585,16 @@ def main():
     roof["fp32"] = {"achieved_tflops": flops / (ms_step / 1e3) / 1e12, "peak_tflops": fp32_peak,
                     "frac": flops / (ms_step / 1e3) / 1e12 / fp32_peak,
                     "peak_source": "148 SM x 128 FP32 lanes x 2 flop x sampled SM clock"}
+    # instruction-issue ceiling (the kernels of configs 6-8 are issue-bound by construction, so
+    # their HBM fraction says little): ncu-counted warp instructions of one step (committed
+    # launch list) over this run's step time, vs 148 SM x 4 schedulers x 1 warp-instr/clk
+    inst = load_inst(w["name"])
+    if inst:
+        ach = inst["inst"] / (ms_step / 1e3) / 1e9
+        peak_i = 148 * 4 * sm_clock / 1e9
+        roof["issue"] = {"achieved_ginst_s": ach, "peak_ginst_s": peak_i, "frac": ach / peak_i,
+                         "inst_per_step": inst["inst"], "source": inst["source"],
+                         "peak_source": "148 SM x 4 schedulers x 1 warp instruction / clk x sampled SM clock"}
 
     # end-to-end through the host-buffer C-ABI call (H2D + compute + D2H inside)
     e2e = None

@@ -17,7 +17,7 @@ done
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 for c in $CONFIGS; do
   [ "$c" = 1 ] && continue
-  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none --csv \
       --log-file $OUT/launches_c$c.csv $CMD --config $c > $OUT/ncu_launch_c$c.log 2>&1
   echo "launches cfg$c rc=$?"
 done

@@ -23,12 +23,15 @@ def step_bytes(path, steps):
     hdr = rows[hi]
     iK, iM, iV, iU = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     tot = collections.defaultdict(float)
+    inst = 0.0
     for r in rows[hi + 1:]:
         if len(r) <= iV or r[iK].startswith("void at::"):
             continue  # torch's own kernels (input casts, reductions) are not part of the step
         if r[iM] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             tot[r[iK]] += float(r[iV].replace(",", "")) * SCALE.get(r[iU], 1)
-    return sum(tot.values()) / steps
+        if r[iM] == "smsp__inst_executed.sum":
+            inst += float(r[iV].replace(",", ""))
+    return sum(tot.values()) / steps, inst / steps
 
 
 def main():
@@ -39,9 +42,11 @@ def main():
         if not os.path.exists(p):
             continue
         # the launch lists run bench.py --steps 3 --warmup 3: six steps under ncu
-        b = step_bytes(p, 6)
+        b, inst = step_bytes(p, 6)
         out[bench.workload(c)["name"]] = {"bytes": b, "scope": "step (all MCI launches of one step, cold cache)",
                                          "source": f"{rnd}/launches_c{c}.csv (ncu dram__bytes_read+write.sum)"}
+        if inst:
+            out[bench.workload(c)["name"]]["inst"] = inst
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as fh:
         json.dump(out, fh, indent=1)
     for k, v in out.items():
