@@ -127,6 +127,41 @@ def test_batch_zero_and_one():
     assert row_rel(out, oracle.OraclePlan(2, 32, 256, BANKS["f_df"]).eval(g1)).max() < F32_TOL
 
 
+@pytest.mark.parametrize("M,N,L,bank,rows,hilbert", [
+    (3, 1024, 16384, "f_df_ddf", 140_000, False),   # row kernel: 2.29e9 output elements
+    (4, 1024, 16384, "f_df_ddf_d3", 140_000, False),  # row-kernel family
+    (2, 4096, 65536, "f_df", 33_000, True),          # Hilbert kernel: 2 x 2.16e9 outputs
+    (2, 512, 2048, "f_df", 1_100_000, False),        # line kernel: 2.25e9 outputs
+])
+def test_element_offsets_beyond_2_31(M, N, L, bank, rows, hilbert):
+    """Maximum-size indexing: batches whose output has more than 2^31 elements (byte offsets
+    beyond 2^33), so every 32-bit index product would wrap.  The last rows (and one in the
+    middle) are checked against the oracle; the batch is the same row repeated, so the
+    check also covers that far rows equal the first."""
+    m = mci()
+    bk = BANKS[bank] if bank in BANKS else BANKS["f_df_ddf"] + [("derivative", 3)]
+    free = torch.cuda.mem_get_info()[0]
+    need = rows * (M * N + L * (2 if hilbert else 1)) * 4
+    if need > 0.8 * free:
+        pytest.skip(f"needs {need / 1e9:.1f} GB")
+    base = synth.cfg2_batch_fast(4, seed=M * N, M=M, N=N, bank=bk)
+    gt = torch.from_numpy(base).cuda().repeat((rows + 3) // 4, 1, 1)[:rows].contiguous()
+    plan = m.Plan(M, N, L, bk, hilbert=hilbert)
+    out = plan.execute(gt)
+    torch.cuda.synchronize()
+    f = out[0] if hilbert else out
+    assert f.numel() > 2 ** 31
+    P = oracle.OraclePlan(M, N, L, bk)
+    for r in (rows - 1, rows - 2, rows // 2):
+        ref = P.eval(base[r % 4:r % 4 + 1])[0]
+        assert row_rel(f[r].double().cpu().numpy()[None], ref[None]).max() < F32_TOL
+        if hilbert:
+            refh = P.eval(base[r % 4:r % 4 + 1], hilbert=True)[0]
+            assert row_rel(out[1][r].double().cpu().numpy()[None], refh[None]).max() < F32_TOL
+    assert torch.equal(f[rows - 1], f[(rows - 1) % 4])
+    del out, f, gt
+
+
 # -------------------------------------------------------------------------- config 2
 def test_cfg2_shape_subset():
     """configs[1] shape (M=3, N=1024, L=16384) on a seeded subset with ragged count."""
