@@ -71,7 +71,8 @@ def workload(cfg):
     M, N, L, B = c["M"], c["N"], c["L"], c["batch"]
     nout = 2 if c.get("hilbert") else 1
     bank = {1: "1, ik", 2: "1, ik, -k^2", 3: "1, ik (+Hf)", 4: "delays 2 pi m/(4N)", 6: "1, ik, -k^2 (NEXT-1, odd band)",
-            10: "1, ik (off-benchmark shape)", 11: "1, ik, -k^2, -ik^3 (off-benchmark shape)"}[cfg]
+            10: "1, ik (off-benchmark shape)", 11: "1, ik, -k^2, -ik^3 (off-benchmark shape)",
+            12: "8 interleaved delays 2 pi m/(MN) (off-benchmark shape)"}[cfg]
     return dict(name=f"cfg{cfg}: {B} x (M={M}, N={N}) -> L={L} x {nout} out, bank {bank}",
                 units=B, outs_per_unit=L * nout, in_per_unit=M * N, out_floats_per_unit=L * nout)
 
@@ -87,7 +88,7 @@ def make_inputs(cfg, rank):
         return synth.cfg3_rows(np.arange(c["batch"]), seed=3 + 1000 * rank)
     if cfg == 4:
         return synth.cfg4_signals(np.arange(c["batch"]), seed=4 + 1000 * rank)[0]
-    if cfg in (6, 10, 11):
+    if cfg in (6, 10, 11, 12):
         return synth.cfg2_batch_fast(c["batch"], seed=cfg + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
     if cfg == 7:
         return synth.cfg2_batch_fast(c["batch"], seed=7 + 1000 * rank, M=c["M"], N=c["N"], bank=c["bank"])
@@ -232,7 +233,7 @@ class OracleLeg:
         self.threads = threads or (os.cpu_count() or 1)
         self.rank = rank
         t0 = time.perf_counter()
-        if cfg in (1, 2, 3, 6, 7, 10, 11):
+        if cfg in (1, 2, 3, 6, 7, 10, 11, 12):
             self.P = oracle.OraclePlan(c["M"], c["N"], c["L"], c["bank"], threads=self.threads)
             if cfg != 7:
                 self.P.kernel_table()
@@ -247,6 +248,7 @@ class OracleLeg:
         # unit order: spread over the batch (the first and last units included)
         self.order = {2: _spread(c.get("batch", 1), 4096), 3: _spread(c.get("batch", 1), 512),
                       10: _spread(c.get("batch", 1), 2048), 11: _spread(c.get("batch", 1), 4096),
+                      12: _spread(c.get("batch", 1), 4096),
                       6: _spread(c.get("batch", 1), 4096), 7: _spread(c.get("batch", 1), 512),
                       8: _spread(c.get("batch", 1), 64), 9: _spread(c.get("batch", 1), 512)}.get(cfg)
         if cfg == 4:
@@ -265,7 +267,7 @@ class OracleLeg:
         o, c, cfg = self.oracle, self.c, self.cfg
         if cfg == 1:
             return 0, self.P.eval(self.g), c["L"]
-        if cfg in (2, 6, 10, 11):
+        if cfg in (2, 6, 10, 11, 12):
             r = int(self.order[i % len(self.order)])
             return r, self.P.eval(self.g[r:r + 1])[0], c["L"]
         if cfg == 3:
@@ -310,6 +312,7 @@ class OracleLeg:
                    f"terms each)",
                 5: f"{2 * n} full output columns of image 0", 6: f"{n} rows spread over the batch",
                 10: f"{n} rows spread over the batch", 11: f"{n} rows spread over the batch",
+                12: f"{n} rows spread over the batch",
                 7: f"{n} rows x {c.get('npts')} off-grid points (direct band sums)",
                 8: f"{n} image(s) {c.get('H')}x{c.get('W')} -> x{c.get('scale')}",
                 9: f"{n} spectra x {c.get('nfreq')} coefficients (direct loops)"}[cfg] + \
@@ -449,7 +452,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=list(range(1, 12)))
+    ap.add_argument("--config", type=int, default=2, choices=list(range(1, 13)))
     ap.add_argument("--impl", default="mci", choices=["mci", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -559,7 +562,7 @@ def main():
     alg_bytes = units * (w["in_per_unit"] + w["out_floats_per_unit"]) * esz
     if cfg == 9:  # the method reads only the out-of-band coefficients (in-band ones carry no error)
         alg_bytes = units * ((c["nfreq"] - c["M"] * c["N"]) * 2 * esz + w["out_floats_per_unit"] * esz)
-    single = cfg in (1, 2, 3, 6, 9, 10, 11)
+    single = cfg in (1, 2, 3, 6, 9, 10, 11, 12)
     achieved = alg_bytes / (ms_step / 1e3) / 1e9
     tr_bytes, tr_scope, tr_src = load_traffic(w["name"])
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

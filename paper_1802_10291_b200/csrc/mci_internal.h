@@ -45,6 +45,8 @@ struct Axis1D {
     int bank_deriv01 = 0;          // bank is exactly (1, ik): closed-form inverse available
     int bank_derivM = 0;           // bank is exactly (ik)^m, m = 0..M-1: Vandermonde closed form (mci_rowg.cu)
     int rowg = 0;                  // special == 1 served by the row-kernel family (mci_rowg.cu)
+    int bank_delay_ti = 0;         // bank is e^{ik 2 pi m/(MN)}, m < M in {2, 4, 8}: time-interleaved sampling
+                                   // (closed-form solve in mci_rowg.cu)
     int bank_delay_uniform = 0;    // bank is e^{ik 2 pi m/(MN)}, m < M = 4: H = W diag(e^{ij tau_m}) (closed form)
     int bank_unimodular = 0;       // every |b_m(k)| = 1 (identity / delay channels): equal channel energies,
                                    // the four-step path skips the channel-magnitude pre-pass (reading R14)

@@ -231,6 +231,14 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
             bool dm = n_null == 0 && !getenv("MCI_ROW_QTAB") && sys[0].kind == MCI_SYS_IDENTITY;
             for (int m = 1; dm && m < M; ++m) dm = sys[m].kind == MCI_SYS_DERIVATIVE && sys[m].order == m;
             ax.bank_derivM = dm ? 1 : 0;
+            // time-interleaved sampling: tau_m = 2 pi m / (M N), M in {2, 4, 8}
+            bool ti = n_null == 0 && !getenv("MCI_ROW_QTAB") && (M == 2 || M == 4 || M == 8);
+            for (int m = 0; ti && m < M; ++m) {
+                const double tau = 2 * PI * m / ((double)M * N);
+                ti = (sys[m].kind == MCI_SYS_DELAY && std::abs(sys[m].tau - tau) <= 1e-12 * (1 + tau)) ||
+                     (m == 0 && sys[m].kind == MCI_SYS_IDENTITY);
+            }
+            ax.bank_delay_ti = ti ? 1 : 0;
             // the config-2 shape runs the tuned kernel (mci_row.cu); the other shapes run the
             // family kernel (mci_rowg.cu).  A/B: MCI_ROWG=1 runs the family kernel on the config-2
             // shape too, MCI_ROWG=2 in addition with the generic derivative-bank solve
@@ -256,6 +264,7 @@ mci_status build_axis(mci::Axis1D &ax, int M, int64_t N, int64_t L, const mci_sy
                     for (int r = 0; r < M; ++r) blob.push_back((T)(Wi[l * M + r].real() / (double)N));
                 if ((M * M) & 1) blob.push_back((T)0);
             }
+            push_roots(blob, 512, 512, 1, -1);  // family, N = 512: e^{-2 pi i m / 512}
             ax.row_variant = getenv("MCI_ROW_VARIANT") ? atoi(getenv("MCI_ROW_VARIANT")) : 0;
             ax.special = 1;
         } else if (mci::line_supported(ax)) {

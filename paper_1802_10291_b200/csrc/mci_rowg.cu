@@ -1,17 +1,20 @@
 // Row-kernel family for real-output shapes with an S = 4096, R = 4 inverse (L = 16384,
 // 2048 < MN <= 4096): (M, N) = (3, 1024) [the config-2 shape, also served by mci_row.cu],
-// (4, 1024) and (2, 2048).  Same mathematics as mci_fused.cu (Lemma 1 forward DFT
+// (4, 1024), (2, 2048) and (5..8, 512).  Same mathematics as mci_fused.cu (Lemma 1 forward DFT
 // PAPER.md:180-233, per-class solve a = D H^{-1} Eq. matrixeqn1, Hermitian-part
 // assembly, zero-padded inverse of Eq. DFTexpression) and the layout of the
 // tuned config-2 kernel (mci_row.cu, its default variant):
 //   * persistent CTA = 3 row groups of 128 threads + a store warpgroup that drains each
 //     finished row from tensor memory and prefetches input rows into L2 two rows ahead;
 //   * forward: the ceil(M/2) channel-pair complex FFTs of length N over all 128 threads of a
-//     group (N = 1024: radix 8 x 8 x 16 for two FFTs; N = 2048: radix 16 x 16 x 8 for one),
-//     channels scaled to unit range by exact powers of two before packing;
-//   * per-class solve, three forms: the paper's Example 2 closed form (M = 3, (1, ik, -k^2)),
+//     group (N = 1024: radix 8 x 8 x 16 for two FFTs; N = 2048: radix 16 x 16 x 8 for one;
+//     N = 512: radix 8 x 8 x 8 for four, two butterflies per thread), channels scaled to unit
+//     range by exact powers of two before packing;
+//   * per-class solve, four forms: the paper's Example 2 closed form (M = 3, (1, ik, -k^2)),
 //     the derivative bank (ik)^m, m < M, as a Vandermonde system in the shifted nodes lN
-//     (binomial shift by j_q, then a constant M x M inverse), or the plan's Q~ table;
+//     (binomial shift by j_q, then a constant M x M inverse), the uniformly interleaved delay
+//     bank tau_m = 2 pi m / (MN) (time-interleaved sampling: H = W diag(e^{i j tau_m}), so
+//     v = DFT_M(G_m e^{-i j tau_m}) / (M N)), or the plan's Q~ table;
 //   * Hermitian assembly + pre-twiddle written straight into the two 4096-point inverse
 //     inputs (A: phases 0, 1; B: phases 2, 3 = a^2 x A's inputs); with MN = 4096 the edge
 //     bins +-K = +-S/2 meet at k' = S/2 and are summed there;
@@ -34,12 +37,13 @@ struct RowGTables {
     const float2 *tw256;  // [16][16]   e^{-2 pi i j i / 256}      (N = 2048 forward pass 2)
     const float2 *tw2k;   // [2048]     e^{-2 pi i m / 2048}       (N = 2048 forward pass 3)
     const float *ainv;    // [M][M]     (Vandermonde in lN)^{-1} / N (derivative bank)
+    const float2 *tw512;  // [512]      e^{-2 pi i m / 512}        (N = 512 forward pass 3)
 };
 
 namespace rowg {
 using namespace sm100;
 constexpr int NT = 128, S = 4096, L = 16384;
-constexpr int BK_TABLE = 0, BK_EX2 = 1, BK_DERIV = 2;
+constexpr int BK_TABLE = 0, BK_EX2 = 1, BK_DERIV = 2, BK_DELAY = 3;
 __device__ __forceinline__ int swz64(int a) { return a + (a >> 6); }  // inverse buffers, 4096 -> 4160
 __device__ __forceinline__ int sw3(int a) { return a ^ ((a >> 3) & 15); }  // N = 1024 forward
 __device__ __forceinline__ int sw4(int a) { return a ^ ((a >> 4) & 15); }  // N = 2048 pass-1 output
@@ -47,8 +51,10 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // TMEM columns (lane = thread of the group): outputs 0..383, tables from 384.  Pre-twiddles of
 // class u of the thread, element l: column base + 8 u + 2 l (one 8-column load per class)
 constexpr int TMC_FW8 = 384, TMC_FW3 = 400;  // N = 1024 forward: 16 + 32 columns
+// columns per class: 8 (M <= 4) or 16 (M <= 8)
+template <int M> constexpr int tmc_cpc() { return M <= 4 ? 8 : 16; }
 template <int N> constexpr int tmc_wp() { return N == 1024 ? 432 : 384; }
-template <int N> constexpr int tmc_wp2() { return N == 1024 ? 464 : 448; }
+template <int N> constexpr int tmc_wp2() { return N == 1024 ? 464 : N == 2048 ? 448 : 416; }
 
 // inverse pass-1 input k' = t + 64 j is structurally zero when K < k' < S - K
 constexpr bool nz(int K, int kp) { return kp <= K || kp >= S - K; }
@@ -79,6 +85,7 @@ constexpr bool allnz(int K, int j) {
 template <int M_, int N_> struct RowGCfg {
     static constexpr int M = M_, N = N_, S = 4096, L = 16384, K = M * N / 2;
     static constexpr int P = (M + 1) / 2;          // channel-pair FFTs in the forward
+    static constexpr int PF = N == 512 ? 4 : N == 1024 ? 2 : 1;  // forward FFTs computed (P of them carry data)
     static constexpr int QPT = N / 256;            // classes q = tid + 128 u (u < QPT) per thread
     static constexpr int EPT = QPT * M;            // emitted spectrum positions per thread
     static constexpr int BUF_ELEMS = S + S / 64;   // 4160
@@ -88,7 +95,8 @@ template <int M_, int N_> struct RowGCfg {
     static constexpr int THREADS = 4 * 128;
     static_assert(P * N <= 2048, "forward spectra fit in half a buffer");
     static_assert(K > 1024 && K <= 2048, "S = next_pow2(2K) = 4096");
-    static_assert(M <= 4 && 8 * QPT <= (N == 1024 ? 32 : 64), "pre-twiddle tables: 8 TMEM columns per class");
+    static_assert(P <= PF, "channel pairs per forward");
+    static_assert(rowg::tmc_cpc<M>() * QPT <= (N == 2048 ? 64 : 32), "pre-twiddle tables: TMEM columns");
 };
 
 template <int M, int N, int BK>
@@ -99,7 +107,7 @@ __global__ void __launch_bounds__(512, 1)
     using C = RowGCfg<M, N>;
     constexpr int K = C::K, P = C::P, QPT = C::QPT, EPT = C::EPT, G = 3;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ float smx[G][4][4];
+    __shared__ float smx[G][4][4];  // per-warp channel maxima (at most four channels per warp)
     __shared__ uint32_t tm_base;
     auto tm_full = [&](int gg) { return reinterpret_cast<uint64_t *>(smem + gg * C::GROUP_BYTES + C::BUF_ELEMS * 8); };
     auto tm_empty = [&](int gg) { return tm_full(gg) + 1; };
@@ -149,25 +157,29 @@ __global__ void __launch_bounds__(512, 1)
         }
 #pragma unroll 1
         for (int u = 0; u < QPT; ++u) {  // pre-twiddles a = e^{2 pi i p/L} of class u, element l, and a^2
-            float v2[8];
+#pragma unroll 1
+            for (int l0 = 0; l0 < tmc_cpc<M>() / 2; l0 += 4) {
+                float v2[8];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                const int q = tt + 128 * u;
-                const int jq = -K + ((q + K) % N);
-                int p = jq + l * N;
-                p = p < 0 ? -p : p;
-                double sn = 0, cs = 0, sn2 = 0, cs2 = 0;
-                if (l < M) {
-                    sincospi(2.0 * p / L, &sn, &cs);
-                    sincospi(4.0 * p / L, &sn2, &cs2);
+                for (int i = 0; i < 4; ++i) {
+                    const int l = l0 + i;
+                    const int q = tt + 128 * u;
+                    const int jq = -K + ((q + K) % N);
+                    int p = jq + l * N;
+                    p = p < 0 ? -p : p;
+                    double sn = 0, cs = 0, sn2 = 0, cs2 = 0;
+                    if (l < M) {
+                        sincospi(2.0 * p / L, &sn, &cs);
+                        sincospi(4.0 * p / L, &sn2, &cs2);
+                    }
+                    v[2 * i] = (float)cs;
+                    v[2 * i + 1] = (float)sn;
+                    v2[2 * i] = (float)cs2;
+                    v2[2 * i + 1] = (float)sn2;
                 }
-                v[2 * l] = (float)cs;
-                v[2 * l + 1] = (float)sn;
-                v2[2 * l] = (float)cs2;
-                v2[2 * l + 1] = (float)sn2;
+                tm_st8(ta + tmc_wp<N>() + tmc_cpc<M>() * u + 2 * l0, v);
+                tm_st8(ta + tmc_wp2<N>() + tmc_cpc<M>() * u + 2 * l0, v2);
             }
-            tm_st8(ta + tmc_wp<N>() + 8 * u, v);
-            tm_st8(ta + tmc_wp2<N>() + 8 * u, v2);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -226,11 +238,12 @@ __global__ void __launch_bounds__(512, 1)
         // forward spectrum of channel pair c at bin q (natural order, per-N layout)
         auto spec = [&](int c, int q) -> float2 {
             if constexpr (N == 1024) return bufB[c * 1024 + sw3(q)];
+            else if constexpr (N == 512) return bufB[sw3(c * 512 + q)];
             else return bufB[q];
         };
         for (int64_t row = (int64_t)blockIdx.x * G + grp; row < rows; row += gstride) {
             const float *src = g + row * (int64_t)(M * N);
-            int e[4] = {0, 0, 0, 0};
+            int e[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             // ---- forward
             if constexpr (N == 1024) {
                 // two 1024-point FFTs, channel pairs (g0, g1), (g2, g3 or 0): radix 8 x 8 x 16
@@ -307,6 +320,92 @@ __global__ void __launch_bounds__(512, 1)
                     dft<16, -1>(x);
 #pragma unroll
                     for (int j = 0; j < 16; ++j) bufB[c * 1024 + sw3(bb + 64 * j)] = f2(x[j]);
+                }
+                group_bar<NT>(barid);
+            } else if constexpr (N == 512) {
+                // four 512-point FFTs, channel pairs (g0, g1) .. (g6, g7) (missing channels 0):
+                // radix 8 x 8 x 8 (Stockham), thread b runs butterfly bf = b % 64 of FFTs
+                // c = b / 64 and c + 2; buffer slot sw3(512 c + a) (brute-force checked conflict-free)
+                const int bf = tid & 63, c0 = tid >> 6;
+                {  // pass 1: Ls = 1, inputs bf + 64 j
+                    pk x[2][8];
+                    float mx[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int c = c0 + 2 * i;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const float a0 = 2 * c < M ? __ldcs(src + (2 * c) * N + bf + 64 * j) : 0.f;
+                            const float a1 = 2 * c + 1 < M ? __ldcs(src + (2 * c + 1) * N + bf + 64 * j) : 0.f;
+                            x[i][j] = mk(a0, a1);
+                            mx[2 * i] = fmaxf(mx[2 * i], fabsf(a0));
+                            mx[2 * i + 1] = fmaxf(mx[2 * i + 1], fabsf(a1));
+                        }
+                    }
+                    // lanes of a warp share c0 (warps 0-1: c0 = 0, warps 2-3: c0 = 1): per-warp maxima
+                    // of channels 2 c0, 2 c0 + 1, 2 c0 + 4, 2 c0 + 5
+#pragma unroll
+                    for (int o = 16; o; o >>= 1)
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) mx[m] = fmaxf(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+                    if (lane == 0)
+#pragma unroll
+                        for (int m = 0; m < 4; ++m) smx[grp][warp][m] = mx[m];
+                    group_bar<NT>(barid);
+#pragma unroll
+                    for (int m = 0; m < M; ++m) {  // channel m: pair c = m / 2, held by warps with c0 = c % 2
+                        const int c = m >> 1, w0 = 2 * (c & 1), slot = 2 * (c >> 1) + (m & 1);
+                        const float mm = fmaxf(smx[grp][w0][slot], smx[grp][w0 + 1][slot]);
+                        const int E = (__float_as_int(mm) >> 23) & 0xff;
+                        e[m] = E == 0 ? 0 : max(-100, min(100, E - 126));
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int c = c0 + 2 * i;
+                        int ea = 0, eb = 0;
+#pragma unroll
+                        for (int m = 0; m < M; ++m) {
+                            if (m == 2 * c) ea = e[m];
+                            if (m == 2 * c + 1) eb = e[m];
+                        }
+                        const pk sc = mk(pow2f(-ea), pow2f(-eb));
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) x[i][j] = pkx::mul(x[i][j], sc);
+                        dft<8, -1>(x[i]);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) bufB[sw3(512 * c + 8 * bf + k)] = f2(x[i][k]);
+                    }
+                }
+                group_bar<NT>(barid);
+                {  // pass 2: Ls = 8, twiddle w64^{(bf % 8) j}, B -> A
+                    const int k8 = bf & 7;
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int c = c0 + 2 * i;
+                        pk x[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) x[j] = mk(bufB[sw3(512 * c + bf + 64 * j)]);
+#pragma unroll
+                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(__ldg(tb.fw8 + j * 8 + k8)));
+                        dft<8, -1>(x);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) bufA[sw3(512 * c + 64 * (bf >> 3) + k8 + 8 * k)] = f2(x[k]);
+                    }
+                }
+                group_bar<NT>(barid);
+                {  // pass 3: Ls = 64, twiddle w512^{bf j}, natural-order outputs bf + 64 k -> B
+#pragma unroll
+                    for (int i = 0; i < 2; ++i) {
+                        const int c = c0 + 2 * i;
+                        pk x[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) x[j] = mk(bufA[sw3(512 * c + bf + 64 * j)]);
+#pragma unroll
+                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(__ldg(tb.tw512 + bf * j)));
+                        dft<8, -1>(x);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) bufB[sw3(512 * c + bf + 64 * k)] = f2(x[k]);
+                    }
                 }
                 group_bar<NT>(barid);
             } else {
@@ -390,7 +489,7 @@ __global__ void __launch_bounds__(512, 1)
                     }
                 }
             }
-            float hs[4];  // 2^e_m / 2 (the 1/2 of the channel-pair unpacking folded in)
+            float hs[8];  // 2^e_m / 2 (the 1/2 of the channel-pair unpacking folded in)
 #pragma unroll
             for (int m = 0; m < M; ++m) hs[m] = 0.5f * pow2f(e[m]);
             group_bar<NT>(barid);  // forward spectra read: buffer B may now be overwritten
@@ -467,6 +566,27 @@ __global__ void __launch_bounds__(512, 1)
                         for (int r = 1; r < M; ++r) acc = pkx::fma(fr[r], bc(__ldg(tb.ainv + l * M + r)), acc);
                         v[l] = acc;
                     }
+                } else if constexpr (BK == BK_DELAY) {
+                    // H_j = W diag(e^{i j tau_m}), W[l][m] = e^{2 pi i l m / M}, tau_m = 2 pi m / (M N):
+                    // v_l = sum_m (G_m / N) e^{-i j tau_m} e^{-2 pi i l m / M} / M
+                    const int r = ((jq % (M * N)) + M * N) % (M * N);  // j mod MN: exact phase
+                    float sn, cs;
+                    sincospif(-2.f * (float)r / (float)(M * N), &sn, &cs);
+                    const pk w1 = mk(cs, sn);
+                    pk u[M];
+                    pk wm = w1;
+                    const float sc = 1.f / (float)(M * N);
+                    u[0] = pkx::mul(G[0], bc(sc));
+#pragma unroll
+                    for (int m = 1; m < M; ++m) {
+                        u[m] = pkx::mul(pkx::cmul(G[m], wm), bc(sc));
+                        if (m + 1 < M) wm = pkx::cmul(wm, w1);
+                    }
+                    if constexpr (M == 8 || M == 4 || M == 2) {
+                        dft<M, -1>(u);
+#pragma unroll
+                        for (int l = 0; l < M; ++l) v[l] = u[l];
+                    }
                 } else {
                     const float2 *Qq = tb.Qt + (int64_t)q * M * M;
 #pragma unroll
@@ -506,9 +626,14 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int u = 0; u < QPT; ++u) {
                 const int q = tid + 128 * u;
-                float2 wq[4], wq2[4];  // (tcgen05.ld is warp-collective: before the q = 0 branch)
-                tm_ld8(tmA + tmc_wp<N>() + 8 * u, wq);
-                tm_ld8(tmA + tmc_wp2<N>() + 8 * u, wq2);
+                float2 wq[8], wq2[8];  // (tcgen05.ld is warp-collective: before the q = 0 branch)
+                if constexpr (M <= 4) {
+                    tm_ld8(tmA + tmc_wp<N>() + 8 * u, wq);
+                    tm_ld8(tmA + tmc_wp2<N>() + 8 * u, wq2);
+                } else {
+                    tm_ld16(tmA + tmc_wp<N>() + 16 * u, wq);
+                    tm_ld16(tmA + tmc_wp2<N>() + 16 * u, wq2);
+                }
                 if (q == 0) {
                     self_mirror(zq[0], zm[0], 0);
                     continue;
@@ -600,13 +725,16 @@ template <int M, int N>
 static cudaError_t rowg_dispatch(int bk, const RowGTables &tb, int64_t rows, const float *g, float *f, cudaStream_t st) {
     if constexpr (M == 3)
         if (bk == rowg::BK_EX2) return rowg_launch_t<M, N, rowg::BK_EX2>(tb, rows, g, f, st);
+    if constexpr (M == 2 || M == 4 || M == 8)
+        if (bk == rowg::BK_DELAY) return rowg_launch_t<M, N, rowg::BK_DELAY>(tb, rows, g, f, st);
     if (bk == rowg::BK_DERIV) return rowg_launch_t<M, N, rowg::BK_DERIV>(tb, rows, g, f, st);
     return rowg_launch_t<M, N, rowg::BK_TABLE>(tb, rows, g, f, st);
 }
 
 bool rowg_supported(const Axis1D &ax) {
     return ax.dtype == MCI_F32 && !ax.analytic && ax.S == 4096 && ax.R == 4 &&
-           ((ax.M == 3 && ax.N == 1024) || (ax.M == 4 && ax.N == 1024) || (ax.M == 2 && ax.N == 2048));
+           ((ax.M == 3 && ax.N == 1024) || (ax.M == 4 && ax.N == 1024) || (ax.M == 2 && ax.N == 2048) ||
+            (ax.N == 512 && ax.M >= 5 && ax.M <= 8));
 }
 
 cudaError_t launch_rowg(const Axis1D &ax, int64_t rows, const void *g, void *f, cudaStream_t st, int *n_launches) {
@@ -623,13 +751,21 @@ cudaError_t launch_rowg(const Axis1D &ax, int64_t rows, const void *g, void *f, 
     tb.tw256 = tb.fw8 + 8 * 8;
     tb.tw2k = tb.tw256 + 256;
     tb.ainv = (const float *)(tb.tw2k + 2048);
+    tb.tw512 = tb.tw2k + 2048 + (ax.M * ax.M + 1) / 2;  // after ainv (M^2 reals, padded to even)
     if (n_launches) *n_launches += 1;
     const float *gg = (const float *)g;
     float *ff = (float *)f;
-    const int bk = ax.bank_deriv012 && ax.M == 3 ? rowg::BK_EX2 : ax.bank_derivM ? rowg::BK_DERIV : rowg::BK_TABLE;
+    const int bk = ax.bank_deriv012 && ax.M == 3 ? rowg::BK_EX2
+                 : ax.bank_derivM             ? rowg::BK_DERIV
+                 : ax.bank_delay_ti           ? rowg::BK_DELAY
+                                              : rowg::BK_TABLE;
     if (ax.M == 3 && ax.N == 1024) return rowg_dispatch<3, 1024>(bk, tb, rows, gg, ff, st);
     if (ax.M == 4 && ax.N == 1024) return rowg_dispatch<4, 1024>(bk, tb, rows, gg, ff, st);
     if (ax.M == 2 && ax.N == 2048) return rowg_dispatch<2, 2048>(bk, tb, rows, gg, ff, st);
+    if (ax.M == 5 && ax.N == 512) return rowg_dispatch<5, 512>(bk, tb, rows, gg, ff, st);
+    if (ax.M == 6 && ax.N == 512) return rowg_dispatch<6, 512>(bk, tb, rows, gg, ff, st);
+    if (ax.M == 7 && ax.N == 512) return rowg_dispatch<7, 512>(bk, tb, rows, gg, ff, st);
+    if (ax.M == 8 && ax.N == 512) return rowg_dispatch<8, 512>(bk, tb, rows, gg, ff, st);
     return cudaErrorInvalidValue;
 }
 

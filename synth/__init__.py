@@ -179,6 +179,10 @@ CONFIGS = {
              bank=[("identity",), ("derivative", 1)], dtype="f32"),
     11: dict(M=4, N=1024, L=16384, batch=65536,
              bank=[("identity",), ("derivative", 1), ("derivative", 2), ("derivative", 3)], dtype="f32"),
+    # eight time-interleaved channels (tau_m = 2 pi m / (M N): an 8-way interleaved sampler,
+    # PAPER.md:139-147 with delay systems) of N = 512 samples -> L = 16384
+    12: dict(M=8, N=512, L=16384, batch=65536,
+             bank=[("delay", 2 * math.pi * m / (8 * 512)) for m in range(8)], dtype="f32"),
 }
 
 

@@ -103,6 +103,8 @@ CASES_1D = [
     ("rowg_4_1024_delay", 4, 1024, 16384, [("delay", 0.001 * m) for m in range(4)], {}, 7, {}),
     ("rowg_2_2048_deriv", 2, 2048, 16384, FD, {}, 7, {}),
     ("rowg_2_2048_delay", 2, 2048, 16384, [("delay", 0.0), ("delay", 0.0007)], {}, 7, {}),
+    ("rowg_8_512_ti", 8, 512, 16384, [("delay", 2 * math.pi * m / 4096) for m in range(8)], {}, 7, {}),
+    ("rowg_6_512_table", 6, 512, 16384, [("delay", 0.0003 * m) for m in range(6)], {}, 7, {}),
     ("hilbert_store_wg", 2, 4096, 65536, FD, {"hilbert": True}, 3, {}),
     ("hilbert_direct", 2, 4096, 65536, FD, {"hilbert": True}, 3, {"MCI_HILBERT_VARIANT": "1"}),
     ("hilbert_tma_store", 2, 4096, 65536, FD, {"hilbert": True}, 3, {"MCI_HILBERT_VARIANT": "2"}),

@@ -964,14 +964,19 @@ def test_boundary_rejects_wrong_plans_and_buffers():
 def _family_bank(kind, M, N):
     if kind == "deriv":
         return [("identity",)] + [("derivative", m) for m in range(1, M)]
-    if kind == "delay":
-        return [("delay", 0.37 * m * 2 * math.pi / (M * N)) for m in range(M)]
+    if kind == "delay":  # non-uniform delays (Q~ table path); 0.9 of the interleaved spacing keeps
+        # cond(H_j) <= 2.7 for M <= 8 (0.37 would give 1.3e4 at M = 8: beyond fp32 parity)
+        return [("delay", 0.9 * m * 2 * math.pi / (M * N)) for m in range(M)]
+    if kind == "ti":  # time-interleaved sampling, tau_m = 2 pi m / (M N): closed-form solve
+        return [("delay", 2 * math.pi * m / (M * N)) for m in range(M)]
     raise ValueError(kind)
 
 
 @pytest.mark.parametrize("M,N,kind,rows", [
     (4, 1024, "deriv", 301), (4, 1024, "deriv", 1), (4, 1024, "delay", 37),
-    (2, 2048, "deriv", 301), (2, 2048, "deriv", 2), (2, 2048, "delay", 37)])
+    (2, 2048, "deriv", 301), (2, 2048, "deriv", 2), (2, 2048, "delay", 37),
+    (8, 512, "ti", 301), (8, 512, "ti", 1), (8, 512, "delay", 37), (7, 512, "delay", 37),
+    (6, 512, "delay", 37), (5, 512, "delay", 37), (4, 1024, "ti", 37), (2, 2048, "ti", 37)])
 def test_row_family_vs_oracle(M, N, kind, rows):
     """Row-kernel family (mci_rowg.cu) vs the fp64 oracle on bandlimited and non-bandlimited
     rows (the edge bins +-K = +-S/2 meet at k' = S/2 for MN = 4096), ragged batches; a row
