@@ -436,17 +436,8 @@ __global__ void __launch_bounds__(hilk::NT + (MODE == 1 ? 128 : 0), 1)
 
 // TMA view of an output plane [rows][2048 p2][32 p1] (p = 32 p2 + p1), box 8 phases x 256 p2
 static bool encode_out_map(CUtensorMap *tm, void *base, int64_t rows) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        void *fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn) {
-            cudaGetLastError();
-            return false;
-        }
-        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    }
+    const auto enc = (PFN_cuTensorMapEncodeTiled_v12000)tensor_map_encoder();
+    if (!enc) return false;
     const cuuint64_t dims[3] = {32, 2048, (cuuint64_t)rows};
     const cuuint64_t strides[2] = {32 * 4, (cuuint64_t)hilk::L * 4};
     const cuuint32_t box[3] = {8, 256, 1}, es[3] = {1, 1, 1};

@@ -82,6 +82,7 @@ size_t fused_smem_bytes(const Axis1D &ax);
 bool fused_supported(const Axis1D &ax);
 
 bool row_supported(const Axis1D &ax);
+void *tensor_map_encoder();  // PFN_cuTensorMapEncodeTiled_v12000, or nullptr (mci_line.cu)
 bool rowg_supported(const Axis1D &ax);
 cudaError_t launch_rowg(const Axis1D &ax, int64_t rows, const void *g, void *f, cudaStream_t st, int *n_launches);
 bool line_supported(const Axis1D &ax);

@@ -614,23 +614,30 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     }
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link dependency);
+// resolved once, thread-safely (function-local static), nullptr when unavailable
+void *tensor_map_encoder() {
+    static void *const fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return p;
+    }();
+    return fn;
+}
+
 // Tensor map of the tiled 2D pass input: dims (innermost first) line-in-block x (D0, stride 1),
 // sample n (N, stride ss), channel m (2, stride cs), block a1 (D1, stride s1), block b (stride s2),
 // fp32; box 16 lines x 256 samples x 1 x 1 x 1, 64-byte swizzle (16-byte chunk c of 64-byte
 // row n stored at chunk c ^ ((n >> 1) & 3), the layout of the G16 gather).  The driver entry
 // point comes through the runtime (no libcuda link dependency).
 static bool encode_tile_map(CUtensorMap *tm, const void *g, const RowAddr &ra, int64_t lines, int N) {
-    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
-    if (!enc) {
-        void *fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess || !fn) {
-            cudaGetLastError();
-            return false;
-        }
-        enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-    }
+    const auto enc = (PFN_cuTensorMapEncodeTiled_v12000)tensor_map_encoder();
+    if (!enc) return false;
     if (ra.s0 != 1 || ra.D0 % 16 != 0 || lines % (ra.D0 * ra.D1) != 0) return false;
     const int64_t nb = lines / (ra.D0 * ra.D1);
     if (ra.D0 >= (1ll << 31) || nb >= (1ll << 31) || ra.D1 >= (1ll << 31)) return false;
