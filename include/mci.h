@@ -27,8 +27,12 @@
  *    (a cudaStream_t; NULL = legacy default stream).
  *  - The plan owns its device tables (inverse matrices, twiddles) and any
  *    workspace; it is immutable after create and may be used concurrently
- *    from several streams except that plans with workspace (four-step and
- *    2D paths) serialise on their workspace: use one plan per stream there.
+ *    from several streams and host threads.  Plans with a workspace (four-step,
+ *    2D and SISR paths) order their executions on the GPU: each waits (a
+ *    cudaStreamWaitEvent on the caller's stream) for the previous execution's
+ *    workspace use, whatever stream it ran on, so concurrent calls on one such
+ *    plan run one after the other (use one plan per stream for overlap).  The
+ *    host-buffer entry points serialise per plan (internal staging buffers).
  *  - Results are deterministic for a given plan and batch (no atomics).
  *  - Arithmetic type is the plan dtype (MCI_F32: float, MCI_F64: double);
  *    host-side plan construction is always fp64.

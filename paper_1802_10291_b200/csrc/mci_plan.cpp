@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <cstdlib>
+#include <mutex>
 #include <new>
 #include <type_traits>
 #include <vector>
@@ -127,7 +128,27 @@ struct mci_plan_s {
     int ws_halves = 1;
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
+    // plans with a workspace (four-step, 2D, SISR) or host staging are shared state: executions
+    // are ordered on the GPU by an event (each waits for the previous one's workspace use, on
+    // whatever stream it ran) and on the host by a mutex around the enqueue
+    std::mutex mu;
+    cudaEvent_t ws_ev = nullptr;
+    bool ws_ev_recorded = false;
 };
+
+// Enqueue f(stream) for a plan with a workspace: after every earlier execution of the plan (their
+// workspace use, on any stream), and before every later one.  Plans without one run directly.
+template <typename F> mci_status with_workspace(mci_plan p, cudaStream_t st, F &&f) {
+    if (!p->ws) return f(st);
+    std::lock_guard<std::mutex> lock(p->mu);
+    if (!p->ws_ev && cudaEventCreateWithFlags(&p->ws_ev, cudaEventDisableTiming) != cudaSuccess) return MCI_E_CUDA;
+    if (p->ws_ev_recorded && cudaStreamWaitEvent(st, p->ws_ev, 0) != cudaSuccess) return MCI_E_CUDA;
+    const mci_status s = f(st);
+    if (cudaEventRecord(p->ws_ev, st) != cudaSuccess) return MCI_E_CUDA;
+    p->ws_ev_recorded = true;
+    return s;
+}
+
 
 namespace {
 
@@ -840,14 +861,16 @@ mci_status mci_execute_sisr(mci_plan p, int64_t n_images, const void *lr, void *
     if (!lr || !hr) return MCI_E_ARG;
     const size_t es = esize(p->dtype);
     const int H = (int)p->Ny, W = (int)p->Nx, s = (int)(p->Lx / p->Nx);
-    for (int64_t i0 = 0; i0 < n_images; i0 += p->ws_units) {
-        const int64_t ni = std::min<int64_t>(p->ws_units, n_images - i0);
-        cudaError_t e = mci::launch_sisr_chunk(p->ax, p->ay, ni, H, W, s, (const char *)lr + i0 * (int64_t)H * W * es,
-                                               (char *)hr + i0 * (int64_t)s * H * s * W * es, p->ws,
-                                               (cudaStream_t)stream, nullptr);
-        if (e != cudaSuccess) return MCI_E_CUDA;
-    }
-    return MCI_OK;
+    return with_workspace(p, (cudaStream_t)stream, [&](cudaStream_t st) {
+        for (int64_t i0 = 0; i0 < n_images; i0 += p->ws_units) {
+            const int64_t ni = std::min<int64_t>(p->ws_units, n_images - i0);
+            cudaError_t e = mci::launch_sisr_chunk(p->ax, p->ay, ni, H, W, s,
+                                                   (const char *)lr + i0 * (int64_t)H * W * es,
+                                                   (char *)hr + i0 * (int64_t)s * H * s * W * es, p->ws, st, nullptr);
+            if (e != cudaSuccess) return MCI_E_CUDA;
+        }
+        return MCI_OK;
+    });
 }
 
 mci_status mci_plan_create_2d(mci_plan *out, int Mx, int64_t Nx, const mci_system *sx, int My, int64_t Ny,
@@ -870,6 +893,7 @@ mci_status mci_plan_create_2d(mci_plan *out, int Mx, int64_t Nx, const mci_syste
 
 void mci_plan_destroy(mci_plan p) {
     if (!p) return;
+    if (p->ws_ev) cudaEventDestroy(p->ws_ev);
     for (int i = 0; i < 2; ++i)
         if (p->hs[i]) cudaStreamDestroy(p->hs[i]);
     if (p->s2) cudaStreamDestroy(p->s2);
@@ -891,7 +915,8 @@ mci_status mci_execute_1d(mci_plan p, int64_t batch, const void *g, void *f, voi
     if (batch == 0) return MCI_OK;
     if (!g || !f) return MCI_E_ARG;
     if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
-    return exec_1d(p, batch, g, f, hf, (cudaStream_t)stream, nullptr);
+    return with_workspace(p, (cudaStream_t)stream,
+                          [&](cudaStream_t st) { return exec_1d(p, batch, g, f, hf, st, nullptr); });
 }
 
 mci_status mci_execute_offgrid(mci_plan p, int64_t batch, const void *g, int64_t n_pts, const void *t, void *f,
@@ -936,7 +961,8 @@ mci_status mci_execute_2d(mci_plan p, int64_t n_images, const void *g, void *out
     if (!p || p->path != mci::PATH_2D || n_images < 0) return MCI_E_ARG;
     if (n_images == 0) return MCI_OK;
     if (!g || !out) return MCI_E_ARG;
-    return exec_2d(p, n_images, g, out, (cudaStream_t)stream, nullptr);
+    return with_workspace(p, (cudaStream_t)stream,
+                          [&](cudaStream_t st) { return exec_2d(p, n_images, g, out, st, nullptr); });
 }
 
 // Host-buffer execution: two streams ping-pong over chunks (H2D, compute, D2H).
@@ -989,6 +1015,8 @@ static mci_status exec_host(mci_plan p, int64_t units, const void *g, void *f, v
             break;
         }
         if (p->ws && it > 0) cudaStreamWaitEvent(st, done[b ^ 1], 0);
+        // the first chunk also waits for the workspace use of earlier device-buffer executions
+        if (p->ws && it == 0 && p->ws_ev_recorded) cudaStreamWaitEvent(st, p->ws_ev, 0);
         if (p->path == mci::PATH_2D) s = exec_2d(p, n, din, dout, st, nullptr);
         else s = exec_1d(p, n, din, dout, nout == 2 ? dout + n * out_u : nullptr, st, nullptr);
         if (s != MCI_OK) break;
@@ -1010,6 +1038,7 @@ mci_status mci_execute_1d_host(mci_plan p, int64_t batch, const void *g, void *f
     if (batch == 0) return MCI_OK;
     if (!g || !f) return MCI_E_ARG;
     if ((p->flags & MCI_OUT_HILBERT) ? !hf : (hf != nullptr)) return MCI_E_ARG;
+    std::lock_guard<std::mutex> lock(p->mu);  // staging buffers and streams of the plan
     return exec_host(p, batch, g, f, hf);
 }
 
@@ -1017,6 +1046,7 @@ mci_status mci_execute_2d_host(mci_plan p, int64_t n_images, const void *g, void
     if (!p || p->path != mci::PATH_2D || n_images < 0) return MCI_E_ARG;
     if (n_images == 0) return MCI_OK;
     if (!g || !out) return MCI_E_ARG;
+    std::lock_guard<std::mutex> lock(p->mu);  // staging buffers and streams of the plan
     return exec_host(p, n_images, g, out, nullptr);
 }
 

@@ -1015,3 +1015,25 @@ def test_row_family_config2_shape(env, monkeypatch):
     pick = [0, 1, 150, 298]
     assert row_rel(out[pick], P.eval(g[pick])).max() < F32_TOL
     assert row_rel(out, ref_gpu).max() < F32_TOL
+
+
+def test_workspace_plan_shared_across_streams():
+    """A plan with a workspace (2D) executed on two streams back to back, without any
+    synchronisation between them: the second call waits on the GPU for the first one's
+    workspace use (include/mci.h), so both results equal the single-stream result."""
+    m = mci()
+    plan = m.Plan2D(2, 512, BANKS["f_df"], 2, 512, BANKS["f_df"], 4)
+    rng = np.random.default_rng(31)
+    ga = torch.from_numpy(rng.standard_normal((3, 2, 2, 512, 512)).astype(np.float32)).cuda()
+    gb = torch.from_numpy(rng.standard_normal((3, 2, 2, 512, 512)).astype(np.float32)).cuda()
+    ref_a = plan.execute(ga).clone()
+    ref_b = plan.execute(gb).clone()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    oa = torch.empty_like(ref_a)
+    ob = torch.empty_like(ref_b)
+    for _ in range(3):
+        plan.execute(ga, oa, stream=s1)
+        plan.execute(gb, ob, stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(oa, ref_a) and torch.equal(ob, ref_b)
