@@ -51,6 +51,7 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 // TMEM columns (lane = thread of the group): outputs 0..383, tables from 384.  Pre-twiddles of
 // class u of the thread, element l: column base + 8 u + 2 l (one 8-column load per class)
 constexpr int TMC_FW8 = 384, TMC_FW3 = 400;  // N = 1024 forward: 16 + 32 columns
+constexpr int TMC_F5A = 448, TMC_F5B = 464;  // N = 512 forward pass-2 / pass-3 twiddles: 16 + 16 columns
 // columns per class: 8 (M <= 4) or 16 (M <= 8)
 template <int M> constexpr int tmc_cpc() { return M <= 4 ? 8 : 16; }
 template <int N> constexpr int tmc_wp() { return N == 1024 ? 432 : 384; }
@@ -179,6 +180,24 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 tm_st8(ta + tmc_wp<N>() + tmc_cpc<M>() * u + 2 * l0, v);
                 tm_st8(ta + tmc_wp2<N>() + tmc_cpc<M>() * u + 2 * l0, v2);
+            }
+        }
+        if constexpr (N == 512) {  // forward twiddles of butterfly bf = tt % 64, j = 1..7
+            float va[8], vb[8];
+#pragma unroll 1
+            for (int c = 0; c < 16; c += 8) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;
+                    const float2 wa = j <= 7 ? tb.fw8[j * 8 + (tt & 7)] : make_float2(0.f, 0.f);
+                    const float2 wb = j <= 7 ? tb.tw512[(tt & 63) * j] : make_float2(0.f, 0.f);
+                    va[2 * i] = wa.x;
+                    va[2 * i + 1] = wa.y;
+                    vb[2 * i] = wb.x;
+                    vb[2 * i + 1] = wb.y;
+                }
+                tm_st8(ta + TMC_F5A + c, va);
+                tm_st8(ta + TMC_F5B + c, vb);
             }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -379,6 +398,8 @@ __global__ void __launch_bounds__(512, 1)
                 group_bar<NT>(barid);
                 {  // pass 2: Ls = 8, twiddle w64^{(bf % 8) j}, B -> A
                     const int k8 = bf & 7;
+                    float2 w8[8];
+                    tm_ld16(tmA + TMC_F5A, w8);
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
                         const int c = c0 + 2 * i;
@@ -386,7 +407,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) x[j] = mk(bufB[sw3(512 * c + bf + 64 * j)]);
 #pragma unroll
-                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(__ldg(tb.fw8 + j * 8 + k8)));
+                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(w8[j - 1]));
                         dft<8, -1>(x);
 #pragma unroll
                         for (int k = 0; k < 8; ++k) bufA[sw3(512 * c + 64 * (bf >> 3) + k8 + 8 * k)] = f2(x[k]);
@@ -394,6 +415,8 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 group_bar<NT>(barid);
                 {  // pass 3: Ls = 64, twiddle w512^{bf j}, natural-order outputs bf + 64 k -> B
+                    float2 w9[8];
+                    tm_ld16(tmA + TMC_F5B, w9);
 #pragma unroll
                     for (int i = 0; i < 2; ++i) {
                         const int c = c0 + 2 * i;
@@ -401,7 +424,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) x[j] = mk(bufA[sw3(512 * c + bf + 64 * j)]);
 #pragma unroll
-                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(__ldg(tb.tw512 + bf * j)));
+                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(w9[j - 1]));
                         dft<8, -1>(x);
 #pragma unroll
                         for (int k = 0; k < 8; ++k) bufB[sw3(512 * c + bf + 64 * k)] = f2(x[k]);
