@@ -53,9 +53,10 @@ __device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) 
 constexpr int TMC_FW8 = 384, TMC_FW3 = 400;  // N = 1024 forward: 16 + 32 columns
 constexpr int TMC_F5A = 448, TMC_F5B = 464;  // N = 512 forward pass-2 / pass-3 twiddles: 16 + 16 columns
 // columns per class: 8 (M <= 4) or 16 (M <= 8)
-template <int M> constexpr int tmc_cpc() { return M <= 4 ? 8 : 16; }
+template <int M> constexpr int tmc_cpc() { return M <= 2 ? 4 : M <= 4 ? 8 : 16; }
 template <int N> constexpr int tmc_wp() { return N == 1024 ? 432 : 384; }
-template <int N> constexpr int tmc_wp2() { return N == 1024 ? 464 : N == 2048 ? 448 : 416; }
+template <int N> constexpr int tmc_wp2() { return N == 1024 ? 464 : 416; }
+constexpr int TMC_F2A = 448, TMC_F2B = 480;  // N = 2048 forward pass-2 / pass-3 twiddles: 30 + 28 columns
 
 // inverse pass-1 input k' = t + 64 j is structurally zero when K < k' < S - K
 constexpr bool nz(int K, int kp) { return kp <= K || kp >= S - K; }
@@ -97,7 +98,7 @@ template <int M_, int N_> struct RowGCfg {
     static_assert(P * N <= 2048, "forward spectra fit in half a buffer");
     static_assert(K > 1024 && K <= 2048, "S = next_pow2(2K) = 4096");
     static_assert(P <= PF, "channel pairs per forward");
-    static_assert(rowg::tmc_cpc<M>() * QPT <= (N == 2048 ? 64 : 32), "pre-twiddle tables: TMEM columns");
+    static_assert(rowg::tmc_cpc<M>() * QPT <= 32, "pre-twiddle tables: TMEM columns");
 };
 
 template <int M, int N, int BK>
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 1
         for (int u = 0; u < QPT; ++u) {  // pre-twiddles a = e^{2 pi i p/L} of class u, element l, and a^2
 #pragma unroll 1
-            for (int l0 = 0; l0 < tmc_cpc<M>() / 2; l0 += 4) {
+            for (int l0 = 0; l0 < tmc_cpc<M>() / 2; l0 += 4) {  // four entries (two when M <= 2)
                 float v2[8];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -178,8 +179,33 @@ __global__ void __launch_bounds__(512, 1)
                     v2[2 * i] = (float)cs2;
                     v2[2 * i + 1] = (float)sn2;
                 }
-                tm_st8(ta + tmc_wp<N>() + tmc_cpc<M>() * u + 2 * l0, v);
-                tm_st8(ta + tmc_wp2<N>() + tmc_cpc<M>() * u + 2 * l0, v2);
+                if constexpr (tmc_cpc<M>() == 4) {
+                    tm_st4(ta + tmc_wp<N>() + 4 * u, v);
+                    tm_st4(ta + tmc_wp2<N>() + 4 * u, v2);
+                } else {
+                    tm_st8(ta + tmc_wp<N>() + tmc_cpc<M>() * u + 2 * l0, v);
+                    tm_st8(ta + tmc_wp2<N>() + tmc_cpc<M>() * u + 2 * l0, v2);
+                }
+            }
+        }
+        if constexpr (N == 2048) {  // forward twiddles: pass 2 w256^{(tt % 16) j}, j = 1..15; pass 3
+                                    // w2048^{bb j}, bb = tt, tt + 128, j = 1..7
+            float va[8], vb[8];
+#pragma unroll 1
+            for (int c = 0; c < 32; c += 8) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int j = 1 + c / 2 + i;                 // pass 2: entries j - 1 = 0..14
+                    const float2 wa = j <= 15 ? tb.tw256[16 * j + (tt & 15)] : make_float2(0.f, 0.f);
+                    const int e = c / 2 + i, hh = e / 7, jb = 1 + e % 7;  // pass 3: entries 7 hh + jb - 1
+                    const float2 wb = e < 14 ? tb.tw2k[(tt + 128 * hh) * jb] : make_float2(0.f, 0.f);
+                    va[2 * i] = wa.x;
+                    va[2 * i + 1] = wa.y;
+                    vb[2 * i] = wb.x;
+                    vb[2 * i + 1] = wb.y;
+                }
+                tm_st8(ta + TMC_F2A + c, va);
+                tm_st8(ta + TMC_F2B + c, vb);
             }
         }
         if constexpr (N == 512) {  // forward twiddles of butterfly bf = tt % 64, j = 1..7
@@ -472,8 +498,11 @@ __global__ void __launch_bounds__(512, 1)
                     pk x[16];
 #pragma unroll
                     for (int j = 0; j < 16; ++j) x[j] = mk(bufB[sw4(b + 128 * j)]);
+                    float2 w2[16];
+                    tm_ld16(tmA + TMC_F2A, w2);
+                    tm_ld16(tmA + TMC_F2A + 16, w2 + 8);
 #pragma unroll
-                    for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(__ldg(tb.tw256 + 16 * j + i)));
+                    for (int j = 1; j < 16; ++j) x[j] = pkx::cmul(x[j], mk(w2[j - 1]));
                     dft<16, -1>(x);
 #pragma unroll
                     for (int k = 0; k < 16; ++k) bufA[(b >> 4) * 256 + i + 16 * k] = f2(x[k]);
@@ -481,6 +510,9 @@ __global__ void __launch_bounds__(512, 1)
                 group_bar<NT>(barid);
                 {  // pass 3: radix 8, Ls = 256: butterflies b, b + 128; inputs A[bb + 256 j],
                    // twiddle w2048^{bb j}; natural-order outputs bb + 256 k -> B
+                    float2 w3[16];
+                    tm_ld16(tmA + TMC_F2B, w3);
+                    tm_ld16(tmA + TMC_F2B + 16, w3 + 8);
 #pragma unroll
                     for (int hh = 0; hh < 2; ++hh) {
                         const int bb = b + 128 * hh;
@@ -488,7 +520,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) x[j] = mk(bufA[bb + 256 * j]);
 #pragma unroll
-                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(__ldg(tb.tw2k + bb * j)));
+                        for (int j = 1; j < 8; ++j) x[j] = pkx::cmul(x[j], mk(w3[7 * hh + j - 1]));
                         dft<8, -1>(x);
 #pragma unroll
                         for (int k = 0; k < 8; ++k) bufB[bb + 256 * k] = f2(x[k]);
@@ -650,7 +682,10 @@ __global__ void __launch_bounds__(512, 1)
             for (int u = 0; u < QPT; ++u) {
                 const int q = tid + 128 * u;
                 float2 wq[8], wq2[8];  // (tcgen05.ld is warp-collective: before the q = 0 branch)
-                if constexpr (M <= 4) {
+                if constexpr (M <= 2) {
+                    tm_ld4(tmA + tmc_wp<N>() + 4 * u, wq);
+                    tm_ld4(tmA + tmc_wp2<N>() + 4 * u, wq2);
+                } else if constexpr (M <= 4) {
                     tm_ld8(tmA + tmc_wp<N>() + 8 * u, wq);
                     tm_ld8(tmA + tmc_wp2<N>() + 8 * u, wq2);
                 } else {

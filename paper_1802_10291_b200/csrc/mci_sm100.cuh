@@ -47,6 +47,11 @@ __device__ __forceinline__ void tm_st8(uint32_t ta, const float *v) {
                  "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                  : "memory");
 }
+__device__ __forceinline__ void tm_st4(uint32_t ta, const float *v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(ta), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+                 "f"(v[3])
+                 : "memory");
+}
 __device__ __forceinline__ void tm_st32(uint32_t ta, const float *v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -70,6 +75,15 @@ __device__ __forceinline__ void tm_ld8(uint32_t ta, float2 *w) {
     w[1] = make_float2(v2, v3);
     w[2] = make_float2(v4, v5);
     w[3] = make_float2(v6, v7);
+}
+__device__ __forceinline__ void tm_ld4(uint32_t ta, float2 *w) {
+    float v0, v1, v2, v3;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v0), "=f"(v1), "=f"(v2), "=f"(v3)
+                 : "r"(ta));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(v0), "+f"(v1), "+f"(v2), "+f"(v3)::"memory");
+    w[0] = make_float2(v0, v1);
+    w[1] = make_float2(v2, v3);
 }
 __device__ __forceinline__ void tm_ld16(uint32_t ta, float2 *w) {
     float v[16];
