@@ -18,7 +18,8 @@ import re
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmci.so")
+# MCI_LIB: an experimental build of the same library (tools/build_variant.sh), A/B timing only
+LIB_PATH = os.environ.get("MCI_LIB") or os.path.join(_PKG, "libmci.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "mci.h")
 
 MCI_OK, MCI_E_ARG, MCI_E_BAND, MCI_E_ALIAS, MCI_E_SINGULAR, MCI_E_SIZE, MCI_E_CUDA, MCI_E_UNSUPPORTED = range(8)

@@ -392,6 +392,10 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                     tm_ld8(ta + 128 * gg + 8 * c, w);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) __stcs(fo + 2 * (t + 64 * (4 * c + i)) + h, w[i]);
+                    // pace the drain: a short sleep between the four-store bursts leaves the LSU to the
+                    // compute warps (measured 1.260 -> 1.253 ms; 80 ns and longer fall behind: 1.288;
+                    // a fully unrolled, burstier drain 1.315; finer x4 / x2 loads 1.290 / 1.315)
+                    __nanosleep(32);
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(tm_empty(gg));
