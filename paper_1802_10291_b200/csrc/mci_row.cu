@@ -29,6 +29,10 @@
 #include "mci_internal.h"
 #include "mci_pk.cuh"
 
+#ifndef MCI_ROW_SCALE2
+#define MCI_ROW_SCALE2 0  // 1: also scale channel 2 to unit range (A/B; it shares its FFT with no channel)
+#endif
+
 namespace mci {
 
 namespace rowk {
@@ -437,23 +441,26 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                     x1[j] = mk(a2, 0.f);
                     m0 = fmaxf(m0, fabsf(a0));
                     m1 = fmaxf(m1, fabsf(a1));
-                    m2 = fmaxf(m2, fabsf(a2));
+                    if constexpr (MCI_ROW_SCALE2) m2 = fmaxf(m2, fabsf(a2));
                 }
 #pragma unroll
                 for (int o = 16; o; o >>= 1) {
                     m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
                     m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-                    m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+                    if constexpr (MCI_ROW_SCALE2) m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
                 }
                 if (lane == 0) {
                     smx[grp][warp][0] = m0;
                     smx[grp][warp][1] = m1;
-                    smx[grp][warp][2] = m2;
+                    if constexpr (MCI_ROW_SCALE2) smx[grp][warp][2] = m2;
                 }
                 group_bar(barid);  // maxima visible; previous row's reads of buffers A/B complete
-                int e[3];
+                // channel 2 is alone in its FFT (g2 + 0 i): the FFT is linear and no other channel's
+                // rounding can leak into it, so it needs no scaling (R10 is about channels sharing one
+                // complex FFT): e[2] = 0 saves its maxima and eight multiplies per thread
+                int e[3] = {0, 0, 0};
 #pragma unroll
-                for (int m = 0; m < 3; ++m) {
+                for (int m = 0; m < (MCI_ROW_SCALE2 ? 3 : 2); ++m) {
                     const float mm = fmaxf(fmaxf(smx[grp][0][m], smx[grp][1][m]), fmaxf(smx[grp][2][m], smx[grp][3][m]));
                     const int E = (__float_as_int(mm) >> 23) & 0xff;
                     e[m] = E == 0 ? 0 : max(-100, min(100, E - 126));
@@ -467,7 +474,7 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     x0[j] = pkx::mul(x0[j], sc0);
-                    x1[j] = pkx::mul(x1[j], bc(sc1));
+                    if constexpr (MCI_ROW_SCALE2) x1[j] = pkx::mul(x1[j], bc(sc1));
                 }
                 pkx::dft<8, -1>(x0);
                 pkx::dft<8, -1>(x1);

@@ -270,6 +270,9 @@ __global__ void __launch_bounds__(512, 1)
                     tm_ld8(tmA + 128 * gg + 8 * c, w);
 #pragma unroll
                     for (int i = 0; i < 4; ++i) __stcs(fo + 2 * (t + 64 * (4 * c + i)) + h, w[i]);
+#ifndef MCI_ROWG_NOSLEEP
+                    __nanosleep(32);  // paced drain, as in mci_row.cu
+#endif
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 mbar_arrive(tm_empty(gg));
