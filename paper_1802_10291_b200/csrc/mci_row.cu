@@ -29,6 +29,9 @@
 #include "mci_internal.h"
 #include "mci_pk.cuh"
 
+#ifndef MCI_ROW_BALANCED
+#define MCI_ROW_BALANCED 1  // 0: the divergent q = 0 branch and table loads for q* (A/B)
+#endif
 #ifndef MCI_ROW_SCALE2
 #define MCI_ROW_SCALE2 0  // 1: also scale channel 2 to unit range (A/B; it shares its FFT with no channel)
 #endif
@@ -624,6 +627,18 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             tm_ld8(tmA + TB + TM_WP2 + 8, wq2 + 4);
             tm_ld8(tmA + TB + TM_WP2 + 16, wq2 + 8);
         }
+        // emitm: emit with an explicit mirror slot pm (no p > 0 branch): the caller passes S - p, or
+        // the never-read slot 2048 (inside the zero-padding band) for p = 0
+        auto emitm = [&](int p, int pm, pk X, float2 wa, float2 wa2) {
+            const pk a = mk(wa), a2 = mk(wa2);
+            const pk P1 = pkx::cmul(X, a);
+            const pk A = add_rot<1>(X, P1);
+            bufA[swz64(p)] = f2(A);
+            bufB[swz64(p)] = f2(pkx::cmul(A, a2));
+            const pk Am = add_rot<1>(pkx::conj(X), pkx::conj(P1));
+            bufA[swz64(pm)] = f2(Am);
+            bufB[swz64(pm)] = f2(pkx::cmul(Am, pkx::conj(a2)));
+        };
         auto emit = [&](int p, pk X, float2 wa, float2 wa2) {
             const pk a = mk(TMS ? wa : ld_wp(p));
             const pk P1 = pkx::cmul(X, a);
@@ -683,7 +698,26 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             const int q = tid + 128 * u;
             pk v[3];
             solve(zq[u], zm[u], q, v);
-            if (q != 0) {
+            if constexpr (MCI_ROW_BALANCED && TMS && (TM & TM_A2) != 0) {
+                // no divergent branch for q = 0 (thread 0, u = 0): its three outputs are selected into the
+                // regular pattern -- p = N - q and q + N both become N and carry (a(N) + conj a(-N))/2
+                // (the same value written twice), p = q = 0 carries Re a(0) and its mirror goes to the
+                // never-read slot 2048 -- so warp 0 does the same work as the other warps of its group
+                // (they waited for it at the next barrier: 4 % of the compute warps' samples)
+                pk Xa = pkx::conj(v[0]), Xb = v[1], Xc = v[2];
+                int pm = S - q;
+                if (u == 0) {
+                    const bool is0 = q == 0;
+                    const pk avg = pkx::mul(add(v[2], Xa), bc(0.5f));
+                    Xa.v = is0 ? avg.v : Xa.v;
+                    Xc.v = is0 ? avg.v : Xc.v;
+                    Xb.v = is0 ? mk(f2(v[1]).x, 0.f).v : Xb.v;
+                    pm = is0 ? 2048 : pm;
+                }
+                emitm(N - q, S - N + q, Xa, wq[3 * u], wq2[3 * u]);
+                emitm(q, pm, Xb, wq[3 * u + 1], wq2[3 * u + 1]);
+                emitm(q + N, S - N - q, Xc, wq[3 * u + 2], wq2[3 * u + 2]);
+            } else if (q != 0) {
                 emit(N - q, pkx::conj(v[0]), wq[3 * u], wq2[3 * u]);
                 emit(q, v[1], wq[3 * u + 1], wq2[3 * u + 1]);
                 emit(q + N, v[2], wq[3 * u + 2], wq2[3 * u + 2]);
@@ -695,9 +729,20 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
         if (tid == 0) {  // q* = N/2: elements -3N/2 = -K, -N/2, N/2
             pk v[3];
             solve(zq[4], zm[4], N / 2, v);
+            if constexpr (MCI_ROW_BALANCED && L == 16 * N && K == 3 * N / 2) {
+                // a(K) = e^{2 pi i 6/64}, a(N/2) = e^{2 pi i 2/64} and their squares: compile-time constants
+                // (the table loads were two L1/L2 round trips on warp 0's critical path every row)
+                const float2 aK = make_float2((float)cl::cos64(6), (float)cl::sin64(6));
+                const float2 aK2 = make_float2((float)cl::cos64(12), (float)cl::sin64(12));
+                const float2 aH = make_float2((float)cl::cos64(2), (float)cl::sin64(2));
+                const float2 aH2 = make_float2((float)cl::cos64(4), (float)cl::sin64(4));
+                emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)), aK, aK2);
+                emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)), aH, aH2);
+            } else {
             const float2 aK = __ldg(tb.wp + K), aH = __ldg(tb.wp + N / 2);
             emit(K, pkx::mul(pkx::conj(v[0]), bc(0.5f)), aK, f2(pkx::cmul(mk(aK), mk(aK))));
             emit(N / 2, pkx::mul(add(v[2], pkx::conj(v[1])), bc(0.5f)), aH, f2(pkx::cmul(mk(aH), mk(aH))));
+            }
         }
         group_bar(barid);
 
