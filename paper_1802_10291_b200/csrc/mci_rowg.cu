@@ -26,6 +26,10 @@
 #include "mci_pk.cuh"
 #include "mci_sm100.cuh"
 
+#ifndef MCI_ROWG_BALANCED
+#define MCI_ROWG_BALANCED 1  // 0: the q = 0 class in a divergent branch of thread 0 (A/B)
+#endif
+
 namespace mci {
 
 struct RowGTables {
@@ -534,12 +538,13 @@ __global__ void __launch_bounds__(512, 1)
 
             // ---- solve: classes q = tid + 128 u (0 < q < N/2) and the self-mirror classes
             //      q = 0 (u = 0 of thread 0) and q = N/2 (thread 0)
+            constexpr int QS_TID = 64;  // the thread (warp 2) that solves the q* = N/2 class
             pk zq[QPT + 1][P], zm[QPT + 1][P];
 #pragma unroll
             for (int u = 0; u <= QPT; ++u) {
                 const int q = u < QPT ? tid + 128 * u : N / 2;
                 const int qm = (N - q) & (N - 1);
-                if (u < QPT || tid == 0) {
+                if (u < QPT || tid == QS_TID) {
 #pragma unroll
                     for (int c = 0; c < P; ++c) {
                         zq[u][c] = mk(spec(c, q));
@@ -658,29 +663,107 @@ __global__ void __launch_bounds__(512, 1)
             };
             // self-mirror class (q = 0 or N/2, thread 0): X[p] = (a(p) + conj a(-p))/2 within the
             // class (a = 0 out of band; p = 0 gives Re a(0); the edge -K gives X[K] = conj a(-K)/2)
-            auto self_mirror = [&](const pk *zqu, const pk *zmu, int q) {
+            // (q is a compile-time constant: every p below is a multiple of N/2, so the pre-twiddle
+            // e^{2 pi i p / L} and its square are compile-time 64th roots instead of table loads on the
+            // critical path of the one warp that runs this branch)
+            auto self_mirror = [&](const pk *zqu, const pk *zmu, auto qc) {
+                constexpr int q = decltype(qc)::value;
                 pk v[M];
                 solve(zqu, zmu, q, v);
+                constexpr int jq = -K + ((q + K) % N);
+                cl::static_for<0, M>([&](auto lc) {
+                    constexpr int l = decltype(lc)::value;
+                    constexpr int k = jq + l * N;
+                    constexpr int lm = (-k - jq) % N == 0 && (-k - jq) / N >= 0 && (-k - jq) / N < M ? (-k - jq) / N : -1;
+                    if constexpr (!(k < 0 && lm >= 0)) {  // a negative k with a partner is emitted with it
+                        constexpr int p = k < 0 ? -k : k;
+                        static_assert((p * 64) % L == 0, "self-mirror pre-twiddles are 64th roots");
+                        constexpr int e1 = p * 64 / L, e2 = (2 * e1) % 64;
+                        pk X;
+                        if constexpr (k < 0) X = pkx::mul(pkx::conj(v[l]), bc(0.5f));
+                        else if constexpr (lm >= 0) X = pkx::mul(add(v[l], pkx::conj(v[lm])), bc(0.5f));
+                        else X = pkx::mul(v[l], bc(0.5f));
+                        emit(p, X, make_float2((float)cl::cos64(e1), (float)cl::sin64(e1)),
+                             make_float2((float)cl::cos64(e2), (float)cl::sin64(e2)));
+                    }
+                });
+            };
+#if MCI_ROWG_BALANCED
+            // One pattern for every class, q = 0 included (no divergent branch on warp 0, whose three
+            // partner warps waited for it at the next barrier).  The regular class q emits element l at
+            // p = |j_q + l N| with the value a(k) or conj a(k); for q = 0 (thread 0, u = 0) the same slots
+            // are written, partners k and -k twice with the same Hermitian average, k = 0 with Re a(0) and
+            // its mirror sent to a padding slot (raw index 64: swz64 never maps there), and the MN = 4096
+            // edge -K with both terms summed at k' = S/2.
+            auto emitb = [&](int p, int pmraw, bool half, pk X, float2 wa, float2 wa2) {
+                const pk P1 = pkx::cmul(X, mk(wa));
+                const pk a2 = mk(wa2);
+                pk A = add_rot<1>(X, P1);
+                const pk Am = add_rot<1>(pkx::conj(X), pkx::conj(P1));
+                pk B = pkx::cmul(A, a2);
+                const pk Bm = pkx::cmul(Am, pkx::conj(a2));
+                if (half) {  // (only instantiated where p = S/2 can occur)
+                    A = add(A, Am);
+                    B = add(B, Bm);
+                }
+                bufA[swz64(p)] = f2(A);
+                bufB[swz64(p)] = f2(B);
+                bufA[pmraw] = f2(Am);
+                bufB[pmraw] = f2(Bm);
+            };
+            cl::static_for<0, QPT>([&](auto uc) {
+                constexpr int u = decltype(uc)::value;
+                const int q = tid + 128 * u;
+                float2 wq[8], wq2[8];
+                if constexpr (M <= 2) {
+                    tm_ld4(tmA + tmc_wp<N>() + 4 * u, wq);
+                    tm_ld4(tmA + tmc_wp2<N>() + 4 * u, wq2);
+                } else if constexpr (M <= 4) {
+                    tm_ld8(tmA + tmc_wp<N>() + 8 * u, wq);
+                    tm_ld8(tmA + tmc_wp2<N>() + 8 * u, wq2);
+                } else {
+                    tm_ld16(tmA + tmc_wp<N>() + 16 * u, wq);
+                    tm_ld16(tmA + tmc_wp2<N>() + 16 * u, wq2);
+                }
+                pk v[M], w[M];
+                solve(zq[u], zm[u], q, v);
                 const int jq = -K + ((q + K) % N);
 #pragma unroll
-                for (int l = 0; l < M; ++l) {
-                    const int k = jq + l * N;
-                    int lm = -1;
-#pragma unroll
-                    for (int l2 = 0; l2 < M; ++l2)
-                        if (jq + l2 * N == -k) lm = l2;
-                    pk vm = mk(0.f, 0.f);
-#pragma unroll
-                    for (int l2 = 0; l2 < M; ++l2)
-                        if (l2 == lm) vm = v[l2];
-                    if (k < 0 && lm >= 0) continue;  // emitted with its positive partner
-                    const int p = k < 0 ? -k : k;
-                    const pk X = k < 0 ? pkx::mul(pkx::conj(v[l]), bc(0.5f))
-                                       : pkx::mul(add(v[l], pkx::conj(vm)), bc(0.5f));
-                    const float2 a = __ldg(tb.wp + p);
-                    emit(p, X, a, f2(pkx::cmul(mk(a), mk(a))));
+                for (int l = 0; l < M; ++l) w[l] = jq + l * N >= 0 ? v[l] : pkx::conj(v[l]);
+                const bool is0 = u == 0 && q == 0;
+                constexpr int jq0 = -K + (K % N);  // j_q of the class q = 0
+                pk x0[M];
+                if constexpr (u == 0) {
+                    cl::static_for<0, M>([&](auto lc) {
+                        constexpr int l = decltype(lc)::value;
+                        constexpr int k0 = jq0 + l * N;
+                        constexpr int lm = (-k0 - jq0) % N == 0 && (-k0 - jq0) / N >= 0 && (-k0 - jq0) / N < M
+                                               ? (-k0 - jq0) / N : -1;
+                        if constexpr (k0 == 0) x0[l] = mk(f2(v[l]).x, 0.f);
+                        else if constexpr (lm >= 0) x0[l] = pkx::mul(add(w[l], w[lm]), bc(0.5f));
+                        else x0[l] = pkx::mul(w[l], bc(0.5f));
+                    });
                 }
-            };
+                cl::static_for<0, M>([&](auto lc) {
+                    constexpr int l = decltype(lc)::value;
+                    constexpr int k0 = jq0 + l * N;
+                    const int k = jq + l * N;
+                    const int p = k >= 0 ? k : -k;
+                    pk X = w[l];
+                    int pm = swz64(S - p);
+                    bool half = false;
+                    if constexpr (u == 0) {
+                        X.v = is0 ? x0[l].v : X.v;
+                        if constexpr (k0 == 0) pm = is0 ? 64 : pm;
+                        if constexpr (K == S / 2 && k0 == -K) {
+                            half = is0;
+                            pm = is0 ? 64 : pm;
+                        }
+                    }
+                    emitb(p, pm, half, X, wq[l], wq2[l]);
+                });
+            });
+#else
 #pragma unroll
             for (int u = 0; u < QPT; ++u) {
                 const int q = tid + 128 * u;
@@ -696,7 +779,7 @@ __global__ void __launch_bounds__(512, 1)
                     tm_ld16(tmA + tmc_wp2<N>() + 16 * u, wq2);
                 }
                 if (q == 0) {
-                    self_mirror(zq[0], zm[0], 0);
+                    self_mirror(zq[0], zm[0], std::integral_constant<int, 0>{});
                     continue;
                 }
                 pk v[M];
@@ -709,7 +792,10 @@ __global__ void __launch_bounds__(512, 1)
                     else emit(-k, pkx::conj(v[l]), wq[l], wq2[l]);
                 }
             }
-            if (tid == 0) self_mirror(zq[QPT], zm[QPT], N / 2);
+#endif
+            // the q* class runs on warp 2 so that it overlaps warp 0's q = 0 branch (both make the other
+            // warps of the group wait at the next barrier)
+            if (tid == QS_TID) self_mirror(zq[QPT], zm[QPT], std::integral_constant<int, N / 2>{});
             group_bar<NT>(barid);
 
             // ---- inverse pass 1: radix 64, Ls = 1.  Lane pair (2s, 2s+1) runs FFTs A and B on
