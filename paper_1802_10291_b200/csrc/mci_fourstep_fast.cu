@@ -8,6 +8,10 @@
 #include "mci_fourstep.cuh"
 #include "mci_pk.cuh"
 
+#ifndef MCI_FSF_B32
+#define MCI_FSF_B32 1  // 0: phase B of FB with 64-bit indices and three table lookups per class (A/B)
+#endif
+
 namespace mci {
 
 namespace fsf {
@@ -34,6 +38,23 @@ __device__ __forceinline__ void tab_wait(uint64_t *mb) {
                      : "=r"(done)
                      : "r"(su32(mb))
                      : "memory");
+}
+// e^{2 pi i E / 128} as a compile-time constant (half-angle from the 64th-root table)
+constexpr double csqrt(double x) {
+    double r = x > 1 ? x : 1;
+    for (int it = 0; it < 80; ++it) r = 0.5 * (r + x / r);
+    return r;
+}
+constexpr double cos128(int e) {
+    e = ((e % 128) + 128) % 128;
+    if (e % 2 == 0) return cl::cos64(e / 2);
+    const double m = csqrt(0.5 * (1.0 + cl::cos64(e)));  // |cos(a)|, cos(2a) = cos64(e)
+    return (e <= 32 || e >= 96) ? m : -m;
+}
+constexpr double sin128(int e) { return cos128(e - 32); }
+template <int E> __device__ __forceinline__ pkx::pk c128() {
+    constexpr float c = (float)cos128(E), s = (float)sin128(E);
+    return pkx::mk(c, s);
 }
 }  // namespace fsf
 
@@ -119,16 +140,33 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
             tw128[q] = make_float2(v.x, -v.y);
         }
     }
+#if MCI_FSF_B32
+    // warps 2-3, idle during phase A, fill the phase-C table; warps 0-1 go straight to their loads
+    // (the tables are first read after the barrier that ends phase A)
+    if (threadIdx.x >= 64) {
+        const int q = threadIdx.x - 64;
+        const int rq = (q >> 5) == 0 ? q1 : N1 - q1;
+        twE[q] = a.twS((int64_t)32 * rq * (q & 31));
+    }
+#else
     for (int q = threadIdx.x; q < 64; q += 128) {
         const int rq = (q >> 5) == 0 ? q1 : N1 - q1;
         twE[q] = a.twS((int64_t)32 * rq * (q & 31));
     }
+#endif
     const int64_t sl = blockIdx.x / (N1 / 2 + 1);
     const int nres = (q1 == 0 || q1 == N1 / 2) ? 1 : 2;
     const int res[2] = {q1, N1 - q1};
     const int64_t N = a.N, K = a.K;
     const int M = a.M, npair = a.npair, tid = threadIdx.x;
+#if MCI_FSF_B32
+    float sup[4];  // channel scales: their loads overlap phase A
+#pragma unroll
+    for (int m = 0; m < 4; ++m) sup[m] = 0.5f * pow2f(chan_exp(a, sl, m));
+    if (!a.fbt) __syncthreads();  // (generic table fill above used every thread)
+#else
     __syncthreads();
+#endif
     // -- A: 4 forward FFTs of length 256 (residue r, pair c): radix 16 x 16 on 64 threads
     if (tid < 64) {
         const int fi = tid >> 4, b = tid & 15, r = fi >> 1, c = fi & 1;
@@ -157,9 +195,100 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
     }
     __syncthreads();
     // -- B: solve classes q = res_r + N1 q2 <= N/2 and assemble X at p = +-res mod N1
+#if !MCI_FSF_B32
     float sup[4];
 #pragma unroll
     for (int m = 0; m < 4; ++m) sup[m] = 0.5f * pow2f(chan_exp(a, sl, m));
+#endif
+#if MCI_FSF_B32
+    // 32-bit index arithmetic (every index of this shape is below 2^23: N = 2^18, K = 2^19, L = 2^22) and
+    // the delay phases e^{-i j tau_m}, m = 1..3, as powers of one table value instead of three lookups
+    // (phase B took 32 % of the kernel's samples for 48 packed FP instructions out of ~600: 64-bit
+    // index arithmetic and the table round trips)
+    {
+        const int Ni = (int)N, Ki = (int)K, Kmodi = (int)a.Kmod, lmni = (int)a.lmn, xli = (int)xl;
+        const unsigned lmask = (unsigned)a.twL.mask, lolen = (1u << a.twL.lob) - 1u;
+        const int lob = a.twL.lob;
+        auto twL32 = [&](int m) {
+            const unsigned mm = (unsigned)m & lmask;
+            return pkx::cmul(mk(__ldg(a.twL.hi + (mm >> lob))), mk(__ldg(a.twL.lo + (mm & lolen))));
+        };
+        for (int idx = tid; idx < nres * N2; idx += 128) {
+            const int r = idx >> 8, q2 = idx & (N2 - 1);
+            const int q = res[r] + N1 * q2;
+            if (q > Ni / 2) continue;
+            const int rm = (nres == 1) ? 0 : 1 - r;
+            const int q2m = (res[r] == 0) ? ((N2 - q2) & (N2 - 1)) : (N2 - 1 - q2);
+            int jt = q + Kmodi;
+            if (jt >= Ni) jt -= Ni;
+            const int jq = -Ki + jt;
+            pk gm[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                if (m < M) {
+                    const int c = m >> 1;
+                    const pk zc = mk(G[(r * 2 + c) * 256 + q2]), zm = pkx::conj(mk(G[(rm * 2 + c) * 256 + q2m]));
+                    gm[m] = (m & 1) ? mul(rot<-1>(sub(zc, zm)), bc(sup[m])) : mul(add(zc, zm), bc(sup[m]));
+                } else {
+                    gm[m] = mk(0.f, 0.f);
+                }
+            }
+            pk v[4];
+            if (a.delay_uniform) {
+                const float s = 1.f / (float)(M * Ni);
+                const pk w1 = pkx::conj(twL32(jq * lmni));  // e^{-i j tau_1}
+                const pk w2 = pkx::cmul(w1, w1), w3 = pkx::cmul(w2, w1);
+                pk u[4];
+                u[0] = mul(gm[0], bc(s));
+                u[1] = mul(pkx::cmul(gm[1], w1), bc(s));
+                u[2] = mul(pkx::cmul(gm[2], w2), bc(s));
+                u[3] = mul(pkx::cmul(gm[3], w3), bc(s));
+                const pk t0 = add(u[0], u[2]), t1 = sub(u[0], u[2]), t2 = add(u[1], u[3]), t3 = sub(u[1], u[3]);
+                v[0] = add(t0, t2);
+                v[2] = sub(t0, t2);
+                v[1] = add_rot<-1>(t1, t3);
+                v[3] = sub_rot<-1>(t1, t3);
+            } else {
+                const float2 *Qq = reinterpret_cast<const float2 *>(a.Qt) + (int64_t)q * M * M;
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    pk acc = mk(0.f, 0.f);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m < M && l < M) acc = add(acc, pkx::cmul(gm[m], mk(__ldg(Qq + m * M + l))));
+                    v[l] = acc;
+                }
+            }
+            const bool selfm = (q == 0) || (2 * q == Ni);
+#pragma unroll
+            for (int l = 0; l < 4; ++l) {
+                if (l >= M) break;
+                const int k = jq + l * Ni;
+                int p = -1;
+                float2 val;
+                if (!selfm) {
+                    p = k > 0 ? k : -k;
+                    val = k > 0 ? f2(v[l]) : f2(pkx::conj(v[l]));
+                } else {
+                    const int lm = -k - jq;
+                    const bool neg_in = (lm >= 0) && (lm % Ni == 0) && (lm / Ni < M);
+                    if (k >= 0 || !neg_in) {
+                        p = k >= 0 ? k : -k;
+                        pk ap = mk(0.f, 0.f), an = mk(0.f, 0.f);
+                        const int lp = p - jq, ln = -p - jq;
+#pragma unroll
+                        for (int l2 = 0; l2 < 4; ++l2) {
+                            if (l2 < M && lp == l2 * Ni) ap = v[l2];
+                            if (l2 < M && ln == l2 * Ni) an = v[l2];
+                        }
+                        val = f2(mul(add(ap, pkx::conj(an)), bc(0.5f)));
+                    }
+                }
+                if (p >= 0) Xl[((p & (N1 - 1)) == res[0] ? 0 : 1) * xli + (p >> 10)] = val;
+            }
+        }
+    }
+#else
     for (int idx = tid; idx < nres * N2; idx += 128) {
         const int r = idx / N2, q2 = idx % N2;
         const int64_t q = res[r] + (int64_t)N1 * q2;
@@ -235,6 +364,7 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
             if (p >= 0) Xl[((int)(p % N1) == res[0] ? 0 : 1) * xl + p / N1] = val;
         }
     }
+#endif
     __syncthreads();
     // -- C: inverse step 1, 4 FFTs (residue r, pair ip) of length S2 over k1: radix 32 x 32 on 128 threads.
     //    k' = res + N1 k1, k1 = i + 32 j.  With S = 2K: k' < K (j < 16) is k = k' (positive);
@@ -253,6 +383,44 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
             const float2 *Xp = Xl + r * xl, *Xn = Xl + ro * xl;
             const pk P1 = mk(a.twL((int64_t)rr + (int64_t)N1 * i));   // w^{res + N1 i}
             const pk P2 = pkx::cmul(P1, P1), P3 = pkx::cmul(P2, P1);
+#if MCI_FSF_B32
+            // (the factors e^{2 pi i e j / 128} are compile-time constants: immediates of the packed
+            // multiplies instead of shared-memory table reads)
+            cl::static_for<0, 32>([&](auto jc) {
+                constexpr int j = decltype(jc)::value;
+                const int k1 = i + 32 * j;
+                const pk w1 = pkx::cmul(fsf::c128<j>(), P1);           // w^{k'} = w^{res + N1 i} e^{2 pi i j / 128}
+                pk acc;
+                if (j < 16) {  // positive frequencies: Y = X[k1] (slot r)
+                    const pk X = mk(Xp[k1]);
+                    if (ip == 0) {
+                        acc = add_rot<1>(X, pkx::cmul(X, w1));  // X + i X w
+                    } else {
+                        const pk w2 = pkx::cmul(fsf::c128<2 * j>(), P2), w3 = pkx::cmul(fsf::c128<3 * j>(), P3);
+                        acc = add_rot<1>(pkx::cmul(X, w2), pkx::cmul(X, w3));
+                    }
+                } else {  // negative frequencies: Y = conj X[S - k'] (slot ro)
+                    const int idx = (rr == 0) ? (N1 - k1) : (N1 - 1 - k1);
+                    const pk Xc = pkx::conj(mk(Xn[idx]));
+                    if (ip == 0) {
+                        acc = add(Xc, pkx::cmul(Xc, w1));  // conj X + i conj X (-i w)
+                    } else {
+                        const pk w2 = pkx::cmul(fsf::c128<2 * j>(), P2), w3 = pkx::cmul(fsf::c128<3 * j>(), P3);
+                        acc = mul(add(pkx::cmul(Xc, w2), pkx::cmul(Xc, w3)), bc(-1.f));
+                    }
+                    if (rr == 0 && k1 == 512) {  // k' = K: add the k = +K term, Y = X[K]
+                        const pk X = mk(Xp[512]);
+                        if (ip == 0) {
+                            acc = add(acc, add_rot<1>(X, pkx::cmul(X, w1)));
+                        } else {
+                            const pk w2 = pkx::cmul(fsf::c128<2 * j>(), P2), w3 = pkx::cmul(fsf::c128<3 * j>(), P3);
+                            acc = add(acc, add_rot<1>(pkx::cmul(X, w2), pkx::cmul(X, w3)));
+                        }
+                    }
+                }
+                x[j] = acc;
+            });
+#else
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
                 const int k1 = i + 32 * j;
@@ -288,6 +456,7 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
                 }
                 x[j] = acc;
             }
+#endif
             dft<32, 1>(x);
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[pad5(32 * i + j)] = f2(x[j]);
