@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
     const int64_t N = a.N, K = a.K;
     const int M = a.M, npair = a.npair, tid = threadIdx.x;
 #if MCI_FSF_B32
+    // phase C's per-thread factor w^{res + N1 i}: its two table loads overlap phases A-B
+    const pk P1early = mk(a.twL((int64_t)res[(tid >> 6) < nres ? (tid >> 6) : 0] + (int64_t)N1 * (tid & 31)));
     float sup[4];  // channel scales: their loads overlap phase A
 #pragma unroll
     for (int m = 0; m < 4; ++m) sup[m] = 0.5f * pow2f(chan_exp(a, sl, m));
@@ -381,7 +383,11 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
             const int rr = res[r];
             const int ro = (rr == 0) ? 0 : ((nres == 1) ? 0 : 1 - r);  // slot of residue N1 - rr
             const float2 *Xp = Xl + r * xl, *Xn = Xl + ro * xl;
+#if MCI_FSF_B32
+            const pk P1 = P1early;  // w^{res + N1 i}, looked up before phase A
+#else
             const pk P1 = mk(a.twL((int64_t)rr + (int64_t)N1 * i));   // w^{res + N1 i}
+#endif
             const pk P2 = pkx::cmul(P1, P1), P3 = pkx::cmul(P2, P1);
 #if MCI_FSF_B32
             // (the factors e^{2 pi i e j / 128} are compile-time constants: immediates of the packed
