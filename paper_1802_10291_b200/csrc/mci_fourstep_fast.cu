@@ -5,6 +5,8 @@
 // FFTs (packed complex arithmetic, mci_pk.cuh), padded shared buffers and
 // coalesced 32-64 byte global runs.  Selected by launch_fourstep when the
 // shape matches; the generic kernels remain the fallback.
+#include <cstdlib>
+
 #include "mci_fourstep.cuh"
 #include "mci_pk.cuh"
 
@@ -487,27 +489,34 @@ __global__ void __launch_bounds__(128, 5) mci_fsf_fb(const FSArgs<float> a) {
 
 // ---- IC: 16 FFTs (pair ip, 8 consecutive u) of length N1 over k2; output runs of 128 B ----------
 // lane = 16 il + 8 ip + t: butterfly i = 2 warp + il
-__global__ void __launch_bounds__(512) mci_fsf_ic(const FSArgs<float> a) {
+// COLS = 8 (default): 512 threads, 16 FFTs (8 columns x 2 residue pairs), 143 KB of shared memory: one
+// CTA per SM (measured 3.85 TB/s, lg_throttle 46 % of the stall samples at 25 % occupancy).  COLS = 4
+// (MCI_FS_IC_COLS=4, A/B): 256 threads, 8 FFTs, 76 KB, three CTAs per SM in different phases, but loads
+// in 32-byte runs and stores in 64-byte runs instead of 64 / 128: measured slower (0.362 vs 0.325 ms).
+template <int COLS>
+__global__ void __launch_bounds__(64 * COLS, COLS == 4 ? 3 : 1) mci_fsf_ic(const FSArgs<float> a) {
     using namespace fsf;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int BS = 1056 + 1;  // == 1 mod 16: conflict-free for the 16 FFTs of a half-warp
+    // per-FFT stride: == 1 (mod 16) for 16 FFTs per half-warp, == 2 (mod 16) for 8 FFTs x 2 butterflies
+    constexpr int BS = COLS == 8 ? 1056 + 1 : 1056 + 2;
+    constexpr int NT = 64 * COLS, LB = COLS == 8 ? 3 : 2;  // lane bits of the column index
     float2 *bufs = reinterpret_cast<float2 *>(smem);
-    float2 *tw = bufs + 16 * BS;  // [32][32] e^{-2 pi i j i/1024}
+    float2 *tw = bufs + 2 * COLS * BS;  // [32][32] e^{-2 pi i j i/1024}
     __shared__ __align__(8) uint64_t tmb;
     if (a.fbt) {
         if (threadIdx.x == 0) tab_copy(tw, a.fbt + 256, 1024 * 8, &tmb);
     } else {
-        for (int q = threadIdx.x; q < 1024; q += 512) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+        for (int q = threadIdx.x; q < 1024; q += NT) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
     }
     __syncthreads();
-    const int ntiles = S2 / 8;
+    const int ntiles = S2 / COLS;
     const int tile = blockIdx.x % ntiles;
     const int64_t sl = blockIdx.x / ntiles;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = lane & 7, ip = (lane >> 3) & 1, i = 2 * warp + (lane >> 4);
-    const int u = tile * 8 + t;
-    float2 *buf = bufs + (ip * 8 + t) * BS;
+    const int t = lane & (COLS - 1), ip = (lane >> LB) & 1, i = (32 / (2 * COLS)) * warp + (lane >> (LB + 1));
+    const int u = tile * COLS + t;
+    float2 *buf = bufs + (ip * COLS + t) * BS;
     const float2 *ucol = reinterpret_cast<const float2 *>(a.Uw) + (sl * a.npi + ip) * (int64_t)N1 * S2 + u;
     pk x[32];
 #pragma unroll
@@ -541,14 +550,19 @@ cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t
     const size_t fa_sm = (size_t)(8 * (1056 + 2) + 1024) * 8;
     const int64_t xl = a.K / N1 + 2;
     const size_t fb_sm = (size_t)(4 * 1060 + 2 * xl + 96 + 64) * 8;  // ib aliases fb + G
-    const size_t ic_sm = (size_t)(16 * 1057 + 1024) * 8;
+    // MCI_FS_IC_COLS (launch time): 4 = the 256-thread IC kernel (three CTAs per SM; measured slower,
+    // config 4 0.362 vs 0.325 ms: its 32-byte read runs cost more than the occupancy returns), default 8
+    static const int ic_cols = getenv("MCI_FS_IC_COLS") ? atoi(getenv("MCI_FS_IC_COLS")) : 8;
+    const size_t ic_sm = ic_cols == 8 ? (size_t)(16 * 1057 + 1024) * 8 : (size_t)(8 * 1058 + 1024) * 8;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
-    if ((e = cudaFuncSetAttribute(mci_fsf_ic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ic_sm))) return e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_ic<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 * 1057 + 1024) * 8))) return e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_ic<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 1058 + 1024) * 8))) return e;
     mci_fsf_fa<<<(unsigned)(ns * a.npair * (N2 / 8)), 256, fa_sm, st>>>(a);
     mci_fsf_fb<<<(unsigned)(ns * (N1 / 2 + 1)), 128, fb_sm, st>>>(a);
-    mci_fsf_ic<<<(unsigned)(ns * (S2 / 8)), 512, ic_sm, st>>>(a);
+    if (ic_cols == 8) mci_fsf_ic<8><<<(unsigned)(ns * (S2 / 8)), 512, ic_sm, st>>>(a);
+    else mci_fsf_ic<4><<<(unsigned)(ns * (S2 / 4)), 256, ic_sm, st>>>(a);
     return cudaGetLastError();
 }
 
