@@ -62,29 +62,32 @@ template <int E> __device__ __forceinline__ pkx::pk c128() {
 
 using pkx::pk;
 
-// ---- FA: 8 FFTs of length N1 over n1 for 8 consecutive residues n2 -------------------------
-// lane = 8 il + t2: FFT t2 (n2 = tile*8 + t2), butterfly i = 4 warp + il
-__global__ void __launch_bounds__(256) mci_fsf_fa(const FSArgs<float> a) {
+// ---- FA: COLS FFTs of length N1 over n1 for COLS consecutive residues n2 ----------------------
+// COLS = 8 (256 threads, 32-byte input runs, 64-byte T runs, 76 KB) or 16 (512 threads, 64 / 128-byte
+// runs, 143 KB, one CTA per SM); lane = COLS il + t2: FFT t2 (n2 = tile * COLS + t2), butterfly i
+template <int COLS>
+__global__ void __launch_bounds__(32 * COLS) mci_fsf_fa(const FSArgs<float> a) {
     using namespace fsf;
     using namespace pkx;
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int BS = 1056 + 2;  // per-FFT stride (== 2 mod 16: conflict-free)
+    constexpr int BS = COLS == 8 ? 1056 + 2 : 1056 + 1;  // per-FFT stride: conflict-free per half-warp
+    constexpr int NT = 32 * COLS, LB = COLS == 8 ? 3 : 4;
     float2 *bufs = reinterpret_cast<float2 *>(smem);
-    float2 *tw = bufs + 8 * BS;  // [32][32] e^{-2 pi i j i / 1024}
+    float2 *tw = bufs + COLS * BS;  // [32][32] e^{-2 pi i j i / 1024}
     __shared__ __align__(8) uint64_t tmb;
     if (a.fbt) {
         if (threadIdx.x == 0) tab_copy(tw, a.fbt + 256, 1024 * 8, &tmb);
     } else {
-        for (int q = threadIdx.x; q < 1024; q += 256) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
+        for (int q = threadIdx.x; q < 1024; q += NT) tw[q] = __ldg(a.twF + (((q >> 5) * (q & 31)) & 1023));
     }
     __syncthreads();
-    const int ntiles = N2 / 8;
+    const int ntiles = N2 / COLS;
     const int tile = blockIdx.x % ntiles;
     const int c = (blockIdx.x / ntiles) % a.npair;
     const int64_t sl = blockIdx.x / ((int64_t)ntiles * a.npair);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t2 = lane & 7, i = 4 * warp + (lane >> 3);
-    const int n2 = tile * 8 + t2;
+    const int t2 = lane & (COLS - 1), i = (32 / COLS) * warp + (lane >> LB);
+    const int n2 = tile * COLS + t2;
     const float *g0 = a.g + (a.sig0 + sl) * (int64_t)a.M * a.N + (int64_t)(2 * c) * a.N;
     const float *g1 = g0 + a.N;
     const bool has1 = 2 * c + 1 < a.M;
@@ -547,7 +550,9 @@ bool fourstep_fast_ok(const Axis1D &ax) {
 
 cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t st) {
     using namespace fsf;
-    const size_t fa_sm = (size_t)(8 * (1056 + 2) + 1024) * 8;
+    // MCI_FS_FA_COLS (launch time): 16 = the 512-thread FA kernel (64-byte input runs), default 8
+    static const int fa_cols = getenv("MCI_FS_FA_COLS") ? atoi(getenv("MCI_FS_FA_COLS")) : 8;
+    const size_t fa_sm = fa_cols == 16 ? (size_t)(16 * 1057 + 1024) * 8 : (size_t)(8 * (1056 + 2) + 1024) * 8;
     const int64_t xl = a.K / N1 + 2;
     const size_t fb_sm = (size_t)(4 * 1060 + 2 * xl + 96 + 64) * 8;  // ib aliases fb + G
     // MCI_FS_IC_COLS (launch time): 4 = the 256-thread IC kernel (three CTAs per SM; measured slower,
@@ -555,11 +560,13 @@ cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t
     static const int ic_cols = getenv("MCI_FS_IC_COLS") ? atoi(getenv("MCI_FS_IC_COLS")) : 8;
     const size_t ic_sm = ic_cols == 8 ? (size_t)(16 * 1057 + 1024) * 8 : (size_t)(8 * 1058 + 1024) * 8;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(mci_fsf_fa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fa_sm))) return e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_fa<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 1058 + 1024) * 8))) return e;
+    if ((e = cudaFuncSetAttribute(mci_fsf_fa<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 * 1057 + 1024) * 8))) return e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_sm))) return e;
     if ((e = cudaFuncSetAttribute(mci_fsf_ic<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(16 * 1057 + 1024) * 8))) return e;
     if ((e = cudaFuncSetAttribute(mci_fsf_ic<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 1058 + 1024) * 8))) return e;
-    mci_fsf_fa<<<(unsigned)(ns * a.npair * (N2 / 8)), 256, fa_sm, st>>>(a);
+    if (fa_cols == 16) mci_fsf_fa<16><<<(unsigned)(ns * a.npair * (N2 / 16)), 512, fa_sm, st>>>(a);
+    else mci_fsf_fa<8><<<(unsigned)(ns * a.npair * (N2 / 8)), 256, fa_sm, st>>>(a);
     mci_fsf_fb<<<(unsigned)(ns * (N1 / 2 + 1)), 128, fb_sm, st>>>(a);
     if (ic_cols == 8) mci_fsf_ic<8><<<(unsigned)(ns * (S2 / 8)), 512, ic_sm, st>>>(a);
     else mci_fsf_ic<4><<<(unsigned)(ns * (S2 / 4)), 256, ic_sm, st>>>(a);
