@@ -37,7 +37,7 @@ def step_bytes(path, steps):
 def main():
     rnd = sys.argv[1] if len(sys.argv) > 1 else "profiles/r02"
     out = {}
-    for c in range(2, 12):
+    for c in range(2, 13):
         p = os.path.join(ROOT, rnd, f"launches_c{c}.csv")
         if not os.path.exists(p):
             continue
