@@ -112,9 +112,11 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
     float2 *bufs = CT ? fwt + 512 : iw + 1024;      // WARPS x BUFS
     // TILED: [2][WARPS][SP]; TMA: [2][N][16] at a 1024-byte boundary (the swizzle pattern is
     // a function of the shared-memory address bits)
+    // (the boundary is reached by adding an offset to the shared-memory pointer: rounding the pointer
+    // through uintptr_t loses its address space and turns every stage read into a generic LD)
+    unsigned char *stage0 = (unsigned char *)(bufs + WARPS * BUFS);
     float *stage = reinterpret_cast<float *>(
-        TMA ? (unsigned char *)(((uintptr_t)(bufs + WARPS * BUFS) + 1023) & ~(uintptr_t)1023)
-            : (unsigned char *)(bufs + WARPS * BUFS));
+        TMA ? stage0 + ((1024u - ((uint32_t)__cvta_generic_to_shared(stage0) & 1023u)) & 1023u) : stage0);
     __shared__ __align__(8) uint64_t tbar;  // TMA: tile landed (expect_tx)
     // TMA on the untiled prefetch path (BULK): each warp's next line arrives by two 1D bulk copies
     // (cp.async.bulk, one per channel row) on the warp's own mbarrier instead of 8 cp.async per lane
@@ -581,8 +583,10 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
             __syncwarp();  // pass-2 reads of buf are complete
 #pragma unroll
             for (int j = 0; j < 32; ++j) buf[lane + 32 * j] = f2(y[j]);  // f[2 p2 + e] at float 2 p2 + e
-            const int64_t l0 = tl * TW;
-            float *ob = f + (l0 / ra.D0) * (int64_t)L * ra.D0 + (l0 % ra.D0);
+            // (32-bit quotient as in line_base: lines < 2^31; the 64-bit division here was an emulated
+            // sequence of ~100 instructions per thread and tile on the write-out's critical path)
+            const uint32_t l0 = (uint32_t)(tl * TW), lq = l0 / uD0;
+            float *ob = f + (int64_t)lq * L * ra.D0 + (l0 - lq * uD0);
             {
                 __syncthreads();  // the tile's 16 lines are in the warp buffers
                 // thread (c, p2): lines 4c..4c+3 of rows 2 p2, 2 p2 + 1 (one 64-bit read per line).
