@@ -551,13 +551,13 @@ bool fourstep_fast_ok(const Axis1D &ax) {
 cudaError_t fourstep_fast_chunk(const FSArgs<float> &a, int64_t ns, cudaStream_t st) {
     using namespace fsf;
     // MCI_FS_FA_COLS (launch time): 16 = the 512-thread FA kernel (64-byte input runs), default 8
-    static const int fa_cols = getenv("MCI_FS_FA_COLS") ? atoi(getenv("MCI_FS_FA_COLS")) : 8;
+    const int fa_cols = getenv("MCI_FS_FA_COLS") ? atoi(getenv("MCI_FS_FA_COLS")) : 8;
     const size_t fa_sm = fa_cols == 16 ? (size_t)(16 * 1057 + 1024) * 8 : (size_t)(8 * (1056 + 2) + 1024) * 8;
     const int64_t xl = a.K / N1 + 2;
     const size_t fb_sm = (size_t)(4 * 1060 + 2 * xl + 96 + 64) * 8;  // ib aliases fb + G
     // MCI_FS_IC_COLS (launch time): 4 = the 256-thread IC kernel (three CTAs per SM; measured slower,
     // config 4 0.362 vs 0.325 ms: its 32-byte read runs cost more than the occupancy returns), default 8
-    static const int ic_cols = getenv("MCI_FS_IC_COLS") ? atoi(getenv("MCI_FS_IC_COLS")) : 8;
+    const int ic_cols = getenv("MCI_FS_IC_COLS") ? atoi(getenv("MCI_FS_IC_COLS")) : 8;
     const size_t ic_sm = ic_cols == 8 ? (size_t)(16 * 1057 + 1024) * 8 : (size_t)(8 * 1058 + 1024) * 8;
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(mci_fsf_fa<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * 1058 + 1024) * 8))) return e;

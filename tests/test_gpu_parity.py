@@ -380,6 +380,28 @@ def test_cfg4_closed_form_vs_table_vs_generic(monkeypatch):
     assert np.linalg.norm(outs[0][1, pts] - ref) / np.linalg.norm(ref) < F32_TOL
 
 
+def test_cfg4_fa_ic_tile_variants(monkeypatch):
+    """The four-step FA / IC tile-width variants (MCI_FS_FA_COLS=16, MCI_FS_IC_COLS=4: same codelets,
+    another thread mapping) give the default kernels' outputs bit for bit, and those match the oracle."""
+    m = mci()
+    c = synth.CONFIGS[4]
+    M, N, L = c["M"], c["N"], c["L"]
+    g = np.random.default_rng(23).standard_normal((2, M, N)).astype(np.float32)
+    plan = m.Plan(M, N, L, c["bank"])
+    outs = []
+    for env in ({}, {"MCI_FS_FA_COLS": "16"}, {"MCI_FS_IC_COLS": "4"}, {"MCI_FS_FA_COLS": "16", "MCI_FS_IC_COLS": "4"}):
+        for k in ("MCI_FS_FA_COLS", "MCI_FS_IC_COLS"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        outs.append(run_plan(plan, g))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    pts = np.random.default_rng(24).integers(0, L, 48)
+    ref = oracle.delay_eval_points(M, N, L, g[0], pts)
+    assert np.linalg.norm(outs[0][0, pts] - ref) / np.linalg.norm(ref) < F32_TOL
+
+
 # -------------------------------------------------------------------------- config 5 (2D)
 def test_2d_small_vs_oracle():
     m = mci()
