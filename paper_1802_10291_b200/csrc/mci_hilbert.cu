@@ -223,11 +223,8 @@ __global__ void __launch_bounds__(hilk::NT + (MODE == 1 ? 128 : 0), 1)
                 m1 = fmaxf(m1, fabsf(a1));
                 x[j] = mk(a0, a1);
             }
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-                m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-            }
+            m0 = warp_max_nonneg(m0);
+            m1 = warp_max_nonneg(m1);
             if (lane == 0) {
                 smx[warp][0] = m0;
                 smx[warp][1] = m1;

@@ -406,11 +406,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS >= 16 ? 1 : 2) mci_line_kern
                 x[j] = mk(a, b);
             }
         }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-            m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-        }
+        m0 = warp_max_nonneg(m0);
+        m1 = warp_max_nonneg(m1);
         const int E0 = (__float_as_int(m0) >> 23) & 0xff, E1 = (__float_as_int(m1) >> 23) & 0xff;
         const int e0 = E0 == 0 ? 0 : max(-100, min(100, E0 - 126));
         const int e1 = E1 == 0 ? 0 : max(-100, min(100, E1 - 126));

@@ -17,6 +17,11 @@
 #include "mci_fft.cuh"
 
 namespace mci {
+// max over the warp of a non-negative float: non-negative floats order like their bit patterns, so one
+// integer warp reduction (redux.sync) replaces five shuffle + max rounds
+__device__ __forceinline__ float warp_max_nonneg(float m) {
+    return __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
+}
 namespace pkx {
 
 struct pk {

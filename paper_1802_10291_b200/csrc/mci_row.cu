@@ -446,12 +446,9 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
                     m1 = fmaxf(m1, fabsf(a1));
                     if constexpr (MCI_ROW_SCALE2) m2 = fmaxf(m2, fabsf(a2));
                 }
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-                    m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
-                    if constexpr (MCI_ROW_SCALE2) m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
-                }
+                m0 = warp_max_nonneg(m0);
+                m1 = warp_max_nonneg(m1);
+                if constexpr (MCI_ROW_SCALE2) m2 = warp_max_nonneg(m2);
                 if (lane == 0) {
                     smx[grp][warp][0] = m0;
                     smx[grp][warp][1] = m1;

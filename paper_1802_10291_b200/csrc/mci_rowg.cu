@@ -314,9 +314,7 @@ __global__ void __launch_bounds__(512, 1)
                         for (int m = 0; m < 4; ++m) mx[m] = fmaxf(mx[m], fabsf(a[m]));
                     }
 #pragma unroll
-                    for (int o = 16; o; o >>= 1)
-#pragma unroll
-                        for (int m = 0; m < M; ++m) mx[m] = fmaxf(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+                    for (int m = 0; m < M; ++m) mx[m] = warp_max_nonneg(mx[m]);
                     if (lane == 0)
 #pragma unroll
                         for (int m = 0; m < M; ++m) smx[grp][warp][m] = mx[m];
@@ -397,9 +395,7 @@ __global__ void __launch_bounds__(512, 1)
                     // lanes of a warp share c0 (warps 0-1: c0 = 0, warps 2-3: c0 = 1): per-warp maxima
                     // of channels 2 c0, 2 c0 + 1, 2 c0 + 4, 2 c0 + 5
 #pragma unroll
-                    for (int o = 16; o; o >>= 1)
-#pragma unroll
-                        for (int m = 0; m < 4; ++m) mx[m] = fmaxf(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+                    for (int m = 0; m < 4; ++m) mx[m] = warp_max_nonneg(mx[m]);
                     if (lane == 0)
 #pragma unroll
                         for (int m = 0; m < 4; ++m) smx[grp][warp][m] = mx[m];
@@ -478,9 +474,7 @@ __global__ void __launch_bounds__(512, 1)
                         mx[1] = fmaxf(mx[1], fabsf(a1));
                     }
 #pragma unroll
-                    for (int o = 16; o; o >>= 1)
-#pragma unroll
-                        for (int m = 0; m < 2; ++m) mx[m] = fmaxf(mx[m], __shfl_xor_sync(0xffffffffu, mx[m], o));
+                    for (int m = 0; m < 2; ++m) mx[m] = warp_max_nonneg(mx[m]);
                     if (lane == 0) {
                         smx[grp][warp][0] = mx[0];
                         smx[grp][warp][1] = mx[1];
