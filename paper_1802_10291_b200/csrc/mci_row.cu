@@ -103,6 +103,8 @@ constexpr int TM_ITWF = 2;    // inverse pass-2 twiddles (shared memory otherwis
 constexpr int TM_L2PF = 4;    // the store warpgroup prefetches each group's input two rows ahead into L2
 constexpr int TM_STORE = 8;   // outputs, drained by a fourth (store) warpgroup
 constexpr int TM_A2 = 32;     // squared pre-twiddles e^{2 pi i 2p / L}: FFT B's inputs = a^2 x FFT A's
+constexpr int TM_TS = 64;     // no store warpgroup: outputs staged in the group's (dead) exchange buffers in row
+                              // order and written by one 64 KB TMA bulk store per row
 // column map; with TM_STORE the outputs take columns 0..383 and the tables move up by 256
 constexpr int TM_ITW = 0;    // 126 cols: w_j(t) = e^{+2 pi i j t / 4096}, j = 1..63 (inverse pass 2)
 constexpr int TM_FW8 = 128;  // 14 cols: e^{-2 pi i j k / 64}, j = 1..7, k = tid & 7 (forward pass 2)
@@ -212,8 +214,10 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
     static_assert(!C::SMALL_TAB || FW4, "G = 3 uses the 4-warp forward");
     static_assert(!TM || (FW4 && G == 3), "TMEM tables: 3 groups, 4-warp forward");
     constexpr bool TMS = TM & TM_SMALL, TMI = TM & TM_ITWF, PF2 = TM & TM_L2PF, STW = TM & TM_STORE;
+    constexpr bool TS = (TM & TM_TS) != 0;
+    static_assert(!(TS && STW), "TMA bulk stores replace the store warpgroup");
     static_assert(!(STW && TMI), "the outputs leave no TMEM room for the inverse twiddles");
-    static_assert(!PF2 || STW, "the L2 prefetch is issued by the store warpgroup");
+    static_assert(!PF2 || STW || TS, "the L2 prefetch is issued by the store warpgroup (TS: by the compute threads)");
     constexpr int TB = STW ? 256 : 0;  // table column shift
     constexpr int M = C::M, N = C::N, S = C::S, K = C::K, L = C::L;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -414,6 +418,13 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
     if constexpr (STW) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;" ::: "memory");
     for (int64_t row = gid; row < rows; row += gstride) {
         using namespace pkx;
+        if constexpr (TS) {
+            // the previous row's bulk store has read the buffers (its first writer comes after the next
+            // barrier); the row two ahead goes to L2 (96 lanes x 128 B)
+            if (tid == 0) tma_store_wait_read();
+            if (PF2 && tid < M * N * 4 / 128 && row + 2 * gstride < rows)
+                asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(g + (row + 2 * gstride) * (int64_t)(M * N) + 32 * tid));
+        }
         if constexpr (C::STAGED) {
             mbar_wait(&mbar[grp], phase);
             phase ^= 1;
@@ -765,12 +776,12 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
         for (int j = 0; j < 64; ++j) x[j] = mk(buf[swz64(t + 64 * j)]);
         if constexpr (TMI) {
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {  // twiddles j = 4c+1 .. 4c+4 (j <= 63)
-                float2 w[4];
-                tm_ld8(tmA + TM_ITW + 8 * c, w);
+            for (int c = 0; c < 8; ++c) {  // twiddles j = 8c+1 .. 8c+8 (j <= 63)
+                float2 w[8];
+                tm_ld16(tmA + TM_ITW + 16 * c, w);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (4 * c + 1 + i <= 63) x[4 * c + 1 + i] = pkx::cmul(x[4 * c + 1 + i], mk(w[i]));
+                for (int i = 0; i < 8; ++i)
+                    if (8 * c + 1 + i <= 63) x[8 * c + 1 + i] = pkx::cmul(x[8 * c + 1 + i], mk(w[i]));
             }
         } else {
 #pragma unroll
@@ -804,6 +815,16 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             mbar_arrive(tm_full(grp));
             opar ^= 1u;
+        } else if constexpr (TS) {
+            // every thread's pass-2 loads are complete (their values are in x): the group's 64 KB region
+            // [bufA .. bufB) becomes the row's output in memory order, (A.x, A.y, B.x, B.y) per p2
+            group_bar(barid);
+            float2 *so = reinterpret_cast<float2 *>(gbase);
+#pragma unroll
+            for (int j = 0; j < 64; ++j) so[2 * (t + 64 * j) + h] = f2(x[j]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            group_bar(barid);
+            if (tid == 0) tma_store_1d(fo, so, L * 4);
         } else {
 #pragma unroll
             for (int j = 0; j < 64; ++j) {
@@ -811,6 +832,7 @@ __global__ void __launch_bounds__(RowCfg<G, QTAB, FW4, TM>::THREADS, 1)
             }
         }
     }
+    if (TS && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }  // compute warpgroups
     if constexpr (TM) {
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -885,6 +907,12 @@ cudaError_t launch_row(const Axis1D &ax, const void *rowtab, int64_t rows, const
     case 8:  // 3 groups (12 warps), 4-warp forward, untiled inputs, inverse twiddles in shared memory
         return tb.deriv ? row_launch_t<3, false, true>(tb, rows, gg, ff, st)
                         : row_launch_t<3, true, true>(tb, rows, gg, ff, st);
+    case 9:  // no store warpgroup: row-order staging in the exchange buffers + one TMA bulk store per row
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_SMALL | rowk::TM_L2PF | rowk::TM_A2 | rowk::TM_TS>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_SMALL | rowk::TM_L2PF | rowk::TM_A2 | rowk::TM_TS>(tb, rows, gg, ff, st);
+    case 10:  // variant 9 with the inverse pass-2 twiddles in the tensor memory the hand-off no longer needs
+        return tb.deriv ? row_launch_t<3, false, true, rowk::TM_SMALL | rowk::TM_ITWF | rowk::TM_L2PF | rowk::TM_A2 | rowk::TM_TS>(tb, rows, gg, ff, st)
+                        : row_launch_t<3, true, true, rowk::TM_SMALL | rowk::TM_ITWF | rowk::TM_L2PF | rowk::TM_A2 | rowk::TM_TS>(tb, rows, gg, ff, st);
     default:  // 3 compute groups + the store warpgroup (outputs from TMEM, input rows into L2
               // two rows ahead); forward and pre-twiddle tables in TMEM; FFT B's inputs = a^2 x A's
         return tb.deriv ? row_launch_t<3, false, true, rowk::TM_STORE | rowk::TM_SMALL | rowk::TM_L2PF | rowk::TM_A2>(tb, rows, gg, ff, st)

@@ -94,7 +94,7 @@ def rnd(shape, dtype=np.float32, seed=0):
 CASES_1D = [
     # (id, M, N, L, bank, kwargs, batch, env)
     *[(f"row_v{v}_q{q}", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROW_VARIANT": str(v), "MCI_ROW_QTAB": str(q)})
-      for v in range(9) for q in (0, 1)],
+      for v in range(11) for q in (0, 1)],
     ("row_generic", 3, 1024, 16384, FDD, {}, 5, {"MCI_DISABLE_ROW": "1"}),
     ("rowg_3_1024_ex2", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROWG": "1"}),
     ("rowg_3_1024_deriv", 3, 1024, 16384, FDD, {}, 7, {"MCI_ROWG": "2"}),

@@ -551,7 +551,8 @@ def test_host_execute_matches_device():
     (16384, 1, False, 3), (16384, 301, False, 5), (16384, 293, True, 5), (16384, 1, False, 5),
     (16384, 301, False, 7), (16384, 291, True, 7), (16384, 301, False, 8), (16384, 292, True, 8),
     (16384, 2, False, 0), (16384, 3, True, 0), (16384, 301, False, 6), (16384, 7, True, 6), (16384, 301, False, 4), (16384, 300, True, 4),
-    (16384, 1, False, 4)])
+    (16384, 1, False, 4), (16384, 301, False, 9), (16384, 295, True, 9), (16384, 1, False, 9),
+    (16384, 301, False, 10), (16384, 294, True, 10)])
 def test_row_kernel_vs_oracle_and_generic(L, rows, qtab, variant, monkeypatch):
     """The specialised config-2 kernel (mci_row.cu; closed-form Example-2 inverse or
     the Q table; variant 0 = 3 compute groups + a store warpgroup draining the
@@ -559,7 +560,9 @@ def test_row_kernel_vs_oracle_and_generic(L, rows, qtab, variant, monkeypatch):
     formed as a^2 x FFT A's, 1/2 = the 2-group layouts, 3 = all per-thread twiddle
     tables in tensor memory, 4 = variant 0 with the three-product pre-twiddle,
     5 = store warpgroup only, 6 = variant 4 without the prefetch, 7 = forward
-    tables in tensor memory, 8 = the 3-group layout with direct stores) on ragged
+    tables in tensor memory, 8 = the 3-group layout with direct stores, 9 = no store warpgroup:
+    row-order staging in the exchange buffers and one TMA bulk store per row, 10 = 9 with the inverse
+    pass-2 twiddles in tensor memory) on ragged
     batches (group tails); L = 8192 exercises the generic kernel.  Within tolerance
     of the oracle and of the generic fused kernel, and bit-for-bit independent of
     batch size."""
