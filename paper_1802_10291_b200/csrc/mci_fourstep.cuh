@@ -18,6 +18,11 @@ template <typename T> struct Tw2 {
         m &= mask;
         return cmul(__ldg(hi + (m >> lob)), __ldg(lo + (m & ((1 << lob) - 1))));
     }
+    // the same lookup with 32-bit index arithmetic (tables of at most 2^31 entries, |m| < 2^31)
+    __device__ __forceinline__ cv<T> at32(int m) const {
+        const unsigned mm = (unsigned)m & (unsigned)mask;
+        return cmul(__ldg(hi + (mm >> lob)), __ldg(lo + (mm & ((1u << lob) - 1u))));
+    }
 };
 
 template <typename T> struct FSArgs {

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(32 * COLS) mci_fsf_fa(const FSArgs<float> a) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
         const int q1 = i + 32 * j;
-        out[(int64_t)q1 * N2 + n2] = f2(pkx::cmul(x[j], mk(a.twN((int64_t)n2 * q1))));
+        out[q1 * N2 + n2] = f2(pkx::cmul(x[j], mk(a.twN.at32(n2 * q1))));  // n2 q1 < 2^18: 32-bit indices
     }
 }
 
